@@ -1,0 +1,157 @@
+/*
+ * escoin.h — C-ABI of the B200-native Escoin direct sparse convolution
+ * (arXiv 1802.10280, "Escort"/"Escoin").
+ *
+ * The two calls of the method (BASELINE.json north_star):
+ *   escoin_csr_stretch   — CSR build + weight stretching, run once per layer
+ *                          (P:310-322 CSR format, P:437-442 weight stretching)
+ *   escoin_sconv_forward — direct sparse convolution with dynamic indexing
+ *                          (Alg.2, §3.1), bias + ReLU fused
+ * plus handle management around them.  Citations "P:n" are lines of the
+ * paper text; "R#n" are the readings listed in DESIGN.md.
+ *
+ * Conventions (all functions):
+ *   - Return an escoin_status (0 = OK, < 0 = error).  No C++ exception or
+ *     CUDA error ever crosses the ABI; nothing is printed.
+ *   - Pointers are plain host or device pointers as stated per argument;
+ *     "device" means memory of the CUDA device the handle lives on.
+ *   - cuda_stream is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  All device work is asynchronous on that stream.
+ *   - Tensors are fp32, row-major NCHW ("CHW layout"; batch outermost).
+ *   - Weights are square K x K filters, one stride, symmetric zero padding
+ *     (SPEC non-goals S:103: no dilation, no non-square shapes).
+ */
+#ifndef ESCOIN_H_
+#define ESCOIN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ESCOIN_OK = 0,
+  ESCOIN_ERR_NULL = -1,          /* a required pointer argument is NULL */
+  ESCOIN_ERR_SHAPE = -2,         /* a dim < 1, stride < 1, pad < 0, or E < 1 / F < 1 */
+  ESCOIN_ERR_CSR_MISMATCH = -3,  /* forward shape != shape recorded in the handle, or CSR arrays inconsistent */
+  ESCOIN_ERR_NOT_ON_DEVICE = -4, /* forward on a handle with no device copy, or device mismatch */
+  ESCOIN_ERR_OVERFLOW = -5,      /* nnz, C*Hp*Wp or an index exceeds INT32_MAX */
+  ESCOIN_ERR_UNSUPPORTED = -6,   /* no compiled kernel for this (K, stride) / kernel id out of range */
+  ESCOIN_ERR_ALLOC = -7,         /* host or device allocation failed */
+  ESCOIN_ERR_CUDA = -8           /* a CUDA runtime call or kernel launch failed */
+} escoin_status;
+
+/* Opaque handle: one pruned, stretched CONV layer.  Immutable once on the
+ * device, so concurrent forwards on different streams are safe. */
+typedef struct escoin_csr escoin_csr;
+
+/* ---------------------------------------------------------------- stretch
+ * Build the stretched CSR of one layer from its dense pruned weights.
+ *   w      host, caller-owned, read-only, not retained: [M][C][K][K] fp32.
+ *          Grouped convolutions pass the block-diagonal expansion (C = all
+ *          input channels, zeros outside the group; reading R#18).
+ *   M,C    output / input channels; H, W the UNPADDED input extent;
+ *   K      square filter size; stride, pad as in the forward.
+ * Semantics (readings R#3-R#7):
+ *   - entries with w != 0.0f are kept (+0 and -0 dropped), row m in order,
+ *     inside a row ascending (c, kh, kw) — equivalently ascending colidx;
+ *   - colidx = c*Hp*Wp + kh*Wp + kw with Hp = H + 2*pad, Wp = W + 2*pad
+ *     (the offset f(c, kh, kw) into the padded input);
+ *   - rowptr[M+1] prefix counts (int32); value copied bitwise.
+ *   stride is used only to validate E, F >= 1 and is recorded in the handle
+ *   (M is added to the north_star signature, reading R#8).
+ * On success *out owns host copies of rowptr/colidx/value (no device memory
+ * yet).  Errors: NULL, SHAPE, OVERFLOW (nnz or C*Hp*Wp > INT32_MAX), ALLOC. */
+int escoin_csr_stretch(const float* w, int M, int C, int H, int W, int K, int stride, int pad,
+                       escoin_csr** out);
+
+/* Shape and nnz recorded in the handle (any output pointer may be NULL). */
+int escoin_csr_info(const escoin_csr* csr, int* M, int* C, int* H, int* W, int* K, int* stride,
+                    int* pad, int64_t* nnz);
+
+/* Borrow the handle's host arrays (valid until escoin_csr_free): rowptr[M+1],
+ * colidx[nnz], value[nnz].  For bit-exact checks of the stretch.  A handle
+ * made by escoin_csr_wrap_device has host copies too (copied at wrap time). */
+int escoin_csr_host_arrays(const escoin_csr* csr, const int32_t** rowptr, const int32_t** colidx,
+                           const float** value);
+
+/* Upload the CSR to `device` and build the kernel-side derived format
+ * (DS-6: records bucketed by output-channel group and input channel; built
+ * once from the stretched CSR, never part of the bit-exact contract).
+ * Synchronises cuda_stream before returning.  Idempotent.
+ * Errors: NULL, CUDA, ALLOC. */
+int escoin_csr_to_device(escoin_csr* csr, int device, void* cuda_stream);
+
+/* Make a handle around device CSR arrays that already hold a stretched CSR
+ * (e.g. received by an NCCL broadcast on another rank).  The arrays are
+ * BORROWED: the caller keeps them alive and unmodified while the handle
+ * lives.  The handle copies them to the host once (synchronously on
+ * cuda_stream) and builds its own derived format on `device`.
+ * Errors: NULL, SHAPE, CSR_MISMATCH (rowptr[0] != 0, rowptr[M] != nnz, a
+ * decreasing rowptr, or a colidx outside [0, C*Hp*Wp)), OVERFLOW, CUDA, ALLOC. */
+int escoin_csr_wrap_device(const int32_t* d_rowptr, const int32_t* d_colidx, const float* d_value,
+                           int64_t nnz, int M, int C, int H, int W, int K, int stride, int pad,
+                           int device, void* cuda_stream, escoin_csr** out);
+
+/* Free host memory and every device allocation the handle owns.  NULL-safe.
+ * Synchronises the device first (pending forwards may still read it). */
+void escoin_csr_free(escoin_csr* csr);
+
+/* ---------------------------------------------------------------- forward
+ * out[n][m][oh][ow] = act( bias[m] + sum_{j in row m} value[j] *
+ *                          X~[n][colidx[j] + oh*stride*Wp + ow*stride] )
+ * with X~ the zero-padded input (Alg.2 P:389-410 with stride, reading R#1;
+ * padding virtual, R#9), act = ReLU if relu else identity, E/F from
+ * E = (H + 2 pad - K)/stride + 1.
+ *   in    device, [N][C][H][W] fp32, UNPADDED (padding is synthesised on chip).
+ *   out   device, [N][M][E][F] fp32; must not alias in.
+ *   bias  device [M] fp32, or NULL (= 0).      relu  0 or 1.
+ * Shape args must equal those recorded in the handle (else CSR_MISMATCH);
+ * N may be 0 (no-op).  Asynchronous on cuda_stream; no host sync, no
+ * allocation, no workspace.  Returns the launch status; device faults
+ * surface at the caller's next synchronisation.
+ * Numerics: fp32 FMA accumulation from 0 in ascending colidx order per output
+ * channel, then + bias, then ReLU (reading R#10/R#22; no fast-math).
+ * Deterministic: bitwise identical for the same inputs whatever N, the grid,
+ * the kernel variant or the number of GPUs the batch is sharded over. */
+int escoin_sconv_forward(int N, int C, int H, int W, int M, int K, int stride, int pad,
+                         const escoin_csr* csr, const float* in, float* out, const float* bias,
+                         int relu, void* cuda_stream);
+
+/* End-to-end variant for HOST buffers (bench e2e leg): copies h_in
+ * ([N][C][H][W], host; pinned for asynchrony) to d_in, runs the forward into
+ * d_out, copies d_out back to h_out ([N][M][E][F], host).  d_in / d_out are
+ * caller-provided device scratch of those sizes; bias is a DEVICE pointer or
+ * NULL.  Asynchronous on cuda_stream when the host buffers are pinned. */
+int escoin_sconv_forward_hostio(int N, int C, int H, int W, int M, int K, int stride, int pad,
+                                const escoin_csr* csr, const float* h_in, float* h_out,
+                                float* d_in, float* d_out, const float* bias, int relu,
+                                void* cuda_stream);
+
+/* ---------------------------------------------------------------- kernel variants
+ * "Kernel customization" (§3.4): the compiled variants of the
+ * sconv kernel.  Variant 0 is the paper's own mapping (one CTA per (image,
+ * output channel), one thread per output element, CSR row in shared memory,
+ * inputs through the read-only cache, P:491-500 / P:541-556) and accepts
+ * every (K, stride).  The other variants are register-tiled sm_100a kernels
+ * specialised for one (K, stride).  ESCOIN_KERNEL_AUTO lets the library pick.
+ * All variants compute bitwise-identical outputs. */
+#define ESCOIN_KERNEL_AUTO (-1)
+int escoin_kernel_count(void);
+/* Name and (K, stride) of variant id; K = stride = 0 for "any". Strings are static. */
+int escoin_kernel_info(int id, const char** name, int* K, int* stride);
+/* Select the variant used by this handle's forwards (rebuilds the derived
+ * format if needed; synchronous).  Errors: NULL, UNSUPPORTED, CUDA, ALLOC. */
+int escoin_csr_set_kernel(escoin_csr* csr, int id);
+/* The variant the handle currently uses (after AUTO resolution). */
+int escoin_csr_get_kernel(const escoin_csr* csr, int* id);
+
+const char* escoin_status_string(int status);
+/* Library version string, e.g. "escoin-b200 0.1 sm_100a". */
+const char* escoin_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESCOIN_H_ */

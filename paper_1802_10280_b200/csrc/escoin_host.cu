@@ -1,0 +1,614 @@
+// escoin_host.cu — the C-ABI of include/escoin.h: weight stretching, handle
+// lifetime, the kernel-side derived format (DS-6), tiling choice and the
+// forward dispatch.  No exceptions or CUDA errors cross the ABI.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "escoin.h"
+#include "escoin_internal.h"
+
+using namespace escoin;
+
+struct escoin_csr {
+  int M = 0, C = 0, H = 0, W = 0, K = 0, stride = 0, pad = 0, E = 0, F = 0;
+  int64_t nnz = 0;
+  std::vector<int32_t> rowptr, colidx;
+  std::vector<float> value;
+  // device side
+  int device = -1;
+  bool on_device = false;
+  bool borrowed = false;  // CSR arrays borrowed (escoin_csr_wrap_device)
+  int32_t* d_rowptr = nullptr;
+  int32_t* d_colidx = nullptr;
+  float* d_value = nullptr;
+  // selected variant + derived format
+  int kernel = -1;  // 0 = paper mapping, 1.. = tiled variant (index + 1)
+  int2* d_recs = nullptr;
+  int* d_sched = nullptr;
+  int* d_sched_off = nullptr;
+  TiledArgs targs{};  // pointers/tiling filled at DS-6 build; tensors per forward
+};
+
+namespace {
+
+constexpr int64_t kInt32Max = 2147483647LL;
+
+int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+int out_dim(int H, int K, int stride, int pad) {
+  if (H < 1 || K < 1 || stride < 1 || pad < 0) return -1;
+  const int span = H + 2 * pad - K;
+  return span < 0 ? -1 : span / stride + 1;
+}
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? ESCOIN_OK : ESCOIN_ERR_CUDA; }
+
+void free_ds6(escoin_csr* h) {
+  if (h->d_recs) cudaFree(h->d_recs);
+  if (h->d_sched) cudaFree(h->d_sched);
+  if (h->d_sched_off) cudaFree(h->d_sched_off);
+  h->d_recs = nullptr;
+  h->d_sched = nullptr;
+  h->d_sched_off = nullptr;
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) return;
+    ok = (prev == dev) || cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---------------------------------------------------------------- tiling
+struct Tiling {
+  int WM, WP, NB, TR, PR, PC, SR, SC, SCs, plane;
+  double cost;
+};
+
+// Max shared-memory bank-group conflict degree of the window LDS.128 pattern
+// (8 lanes per quarter-warp, 16-byte accesses) for a candidate layout.
+int window_conflicts(const TiledVariant& v, const Tiling& t, int CC) {
+  int worst = 0;
+  for (int wp = 0; wp < t.WP; ++wp) {
+    for (int qtr = 0; qtr < 4; ++qtr) {
+      int cnt[8] = {0};
+      int addrs[8];
+      int na = 0;
+      for (int l = qtr * 8; l < qtr * 8 + 8; ++l) {
+        const int slot = wp * 32 + l;
+        const int per_img = t.TR * t.PC;
+        int img = slot / per_img, pr = (slot % per_img) / t.PC, pc = slot % t.PC;
+        if (img >= t.NB) { img = 0; pr = 0; pc = 0; }
+        const int a = img * CC * t.plane + pr * v.PH * v.S * t.SCs + pc * v.PW * v.S;
+        bool dup = false;
+        for (int i = 0; i < na; ++i) dup |= (addrs[i] == a);
+        if (dup) continue;
+        addrs[na++] = a;
+        cnt[(a / 4) & 7]++;
+      }
+      for (int g = 0; g < 8; ++g) worst = std::max(worst, cnt[g]);
+    }
+  }
+  return worst;
+}
+
+bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, Tiling* best) {
+  const int E = h->E, F = h->F;
+  const int PR = ceil_div(E, v.PH), PC = ceil_div(F, v.PW);
+  const int G = ceil_div(h->M, v.Q);
+  const int P = v.PH * v.PW;
+  const int XH = (v.PH - 1) * v.S + v.K, XW = (v.PW - 1) * v.S + v.K;
+  const double dens = h->nnz / (double(h->M) * h->C * h->K * h->K);
+  bool found = false;
+  for (int WP = 1; WP <= 8; WP *= 2) {
+    const int WM = 8 / WP;
+    const int slots = 32 * WP;
+    if (PC > slots) continue;
+    Tiling t{};
+    t.WM = WM;
+    t.WP = WP;
+    t.PR = PR;
+    t.PC = PC;
+    if (PR * PC >= slots) {
+      t.NB = 1;
+      t.TR = std::min(PR, slots / PC);
+    } else {
+      t.NB = slots / (PR * PC);
+      t.TR = PR;
+    }
+    t.SR = (t.TR * v.PH - 1) * v.S + v.K;
+    t.SC = (t.PC * v.PW - 1) * v.S + v.K;
+    const int SC4 = (t.SC + 3) & ~3;
+    if (t.SR * SC4 > kMaxStagePos * kTiledThreads) continue;
+    // pick row/plane padding that minimises LDS.128 bank-group conflicts
+    int bestc = 1 << 30;
+    for (int sp = 0; sp < 8; ++sp) {
+      const int SCs = SC4 + 4 * sp;
+      if (t.SR * SCs > kMaxStagePos * kTiledThreads) break;
+      for (int pp = 0; pp < 8; ++pp) {
+        Tiling u = t;
+        u.SCs = SCs;
+        u.plane = t.SR * SCs + 4 * pp;
+        const int c = window_conflicts(v, u, CC);
+        if (c < bestc) {
+          bestc = c;
+          t.SCs = u.SCs;
+          t.plane = u.plane;
+        }
+      }
+    }
+    const double lane_util = double(t.NB * t.TR * t.PC) / slots;
+    const double pix_util = double(E) * F / (double(PR * v.PH) * (PC * v.PW));
+    const int B = ceil_div(G, WM);
+    const double warp_util = double(G) / (B * WM);
+    const double compute = v.Q * dens * v.K * v.K * (P + 9) + XH * ((XW + 3) / 4) * (bestc > 1 ? bestc : 1) + 12;
+    const double staging = 3.0 * t.NB * t.SR * t.SCs / kTiledThreads;
+    t.cost = (compute + staging) / (lane_util * pix_util * warp_util * v.Q * P);
+    if (!found || t.cost < best->cost) {
+      *best = t;
+      found = true;
+    }
+  }
+  return found;
+}
+
+// ---------------------------------------------------------------- DS-6
+// Records of output-channel group g (channels g*Q .. g*Q+Q-1) bucketed by
+// input channel c, grouped into m-blocks of WM groups and channel chunks of
+// CC.  Each warp stream of one (m-block, chunk):
+//   for each c with records:  HDR(kHdrBase + c_local)  REC*  END(Q*K*K)
+//   DONE(-1)
+// REC = {code = q*K*K + kh*K + kw, bits(value)} in ascending (q, kh, kw) —
+// i.e. the CSR order of each row.  Built once on the host from the stretched
+// CSR; never part of the bit-exact contract.
+struct DS6 {
+  std::vector<int2> recs;
+  std::vector<int> sched, sched_off;
+  int max_block = 0;
+};
+
+void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, DS6* out) {
+  const int Q = v.Q, K = h->K;
+  const int G = ceil_div(h->M, Q), B = ceil_div(G, WM), NK = ceil_div(h->C, CC);
+  const int64_t HpWp = int64_t(h->H + 2 * h->pad) * (h->W + 2 * h->pad);
+  const int Wp = h->W + 2 * h->pad;
+  const int64_t nbuckets = int64_t(B) * NK * WM * CC;
+  std::vector<int64_t> cnt(nbuckets + 1, 0);
+  std::vector<int64_t> key(h->nnz);
+  std::vector<int> code(h->nnz);
+  for (int m = 0; m < h->M; ++m) {
+    const int g = m / Q, q = m % Q, b = g / WM, wm = g % WM;
+    for (int64_t j = h->rowptr[m]; j < h->rowptr[m + 1]; ++j) {
+      const int64_t off = h->colidx[j];
+      const int c = int(off / HpWp);
+      const int rem = int(off - c * HpWp);
+      const int kh = rem / Wp, kw = rem % Wp;
+      const int k = c / CC, cl = c % CC;
+      key[j] = ((int64_t(b) * NK + k) * WM + wm) * CC + cl;
+      code[j] = (q * K + kh) * K + kw;
+      cnt[key[j] + 1]++;
+    }
+  }
+  for (int64_t i = 0; i < nbuckets; ++i) cnt[i + 1] += cnt[i];
+  std::vector<int2> sorted(h->nnz);
+  {
+    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+    for (int64_t j = 0; j < h->nnz; ++j) {
+      int2 r;
+      r.x = code[j];
+      std::memcpy(&r.y, &h->value[j], 4);
+      sorted[pos[key[j]]++] = r;
+    }
+  }
+  const int END = Q * K * K;
+  out->recs.clear();
+  out->sched.clear();
+  out->sched_off.assign(1, 0);
+  out->max_block = 0;
+  for (int b = 0; b < B; ++b) {
+    for (int k = 0; k < NK; ++k) {
+      const int64_t first = ((int64_t(b) * NK + k) * WM) * CC;
+      const int64_t last = first + int64_t(WM) * CC;
+      if (cnt[last] == cnt[first]) continue;  // chunk inactive for this m-block
+      const int start = int(out->recs.size());
+      std::vector<int> woff(WM);
+      for (int wm = 0; wm < WM; ++wm) {
+        woff[wm] = int(out->recs.size()) - start;
+        for (int cl = 0; cl < CC; ++cl) {
+          const int64_t bk = first + int64_t(wm) * CC + cl;
+          if (cnt[bk + 1] == cnt[bk]) continue;
+          out->recs.push_back(make_int2(kHdrBase + cl, 0));
+          for (int64_t i = cnt[bk]; i < cnt[bk + 1]; ++i) out->recs.push_back(sorted[i]);
+          out->recs.push_back(make_int2(END, 0));
+        }
+        out->recs.push_back(make_int2(kDone, 0));
+      }
+      if (out->recs.size() & 1) out->recs.push_back(make_int2(kDone, 0));
+      const int count = int(out->recs.size()) - start;
+      out->max_block = std::max(out->max_block, count);
+      out->sched.push_back(k);
+      out->sched.push_back(start);
+      out->sched.push_back(count);
+      for (int wm = 0; wm < WM; ++wm) out->sched.push_back(woff[wm]);
+    }
+    out->sched_off.push_back(int(out->sched.size() / (3 + WM)));
+  }
+}
+
+template <typename T>
+int upload(const std::vector<T>& v, T** d, cudaStream_t s) {
+  const size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
+  if (cudaMalloc(reinterpret_cast<void**>(d), bytes) != cudaSuccess) return ESCOIN_ERR_ALLOC;
+  if (!v.empty() && cudaMemcpyAsync(*d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return ESCOIN_ERR_CUDA;
+  return ESCOIN_OK;
+}
+
+// Build + upload the derived format of tiled variant `vi` (index into the table).
+int prepare_tiled(escoin_csr* h, int vi, cudaStream_t s) {
+  int nv = 0;
+  const TiledVariant* tv = tiled_variants(&nv);
+  const TiledVariant& v = tv[vi];
+  int CC = 32;
+  Tiling t{};
+  DS6 ds;
+  size_t smem = 0;
+  for (;; CC /= 2) {
+    if (CC < 1) return ESCOIN_ERR_UNSUPPORTED;
+    if (!choose_tiling(v, h, CC, &t)) return ESCOIN_ERR_UNSUPPORTED;
+    build_ds6(h, v, t.WM, CC, &ds);
+    const size_t stage_f = (size_t(t.NB) * CC * t.plane + 3) & ~size_t(3);
+    const size_t stage_r = (ds.max_block + 1) & ~1;
+    smem = 2 * stage_f * 4 + 2 * stage_r * 8;
+    if (smem <= (v.min_blocks > 1 ? 110 : 220) * 1024) {
+      h->targs.stage_floats = int(stage_f);
+      h->targs.stage_recs = int(std::max<size_t>(stage_r, 2));
+      break;
+    }
+  }
+  free_ds6(h);
+  int rc;
+  if ((rc = upload(ds.recs, &h->d_recs, s)) != ESCOIN_OK) return rc;
+  if ((rc = upload(ds.sched, &h->d_sched, s)) != ESCOIN_OK) return rc;
+  if ((rc = upload(ds.sched_off, &h->d_sched_off, s)) != ESCOIN_OK) return rc;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return ESCOIN_ERR_CUDA;
+  TiledArgs& a = h->targs;
+  a.M = h->M;
+  a.C = h->C;
+  a.H = h->H;
+  a.W = h->W;
+  a.E = h->E;
+  a.F = h->F;
+  a.pad = h->pad;
+  a.PR = t.PR;
+  a.PC = t.PC;
+  a.WM = t.WM;
+  a.WP = t.WP;
+  a.NB = t.NB;
+  a.TR = t.TR;
+  a.SR = t.SR;
+  a.SCs = t.SCs;
+  a.plane = t.plane;
+  a.CC = CC;
+  a.tiles_r = ceil_div(t.PR, t.TR);
+  a.B = int(ds.sched_off.size()) - 1;
+  a.smem_bytes = int(smem);
+  a.recs = h->d_recs;
+  a.sched = h->d_sched;
+  a.sched_off = h->d_sched_off;
+  a.sched_stride = 3 + t.WM;
+  return ESCOIN_OK;
+}
+
+int auto_kernel(const escoin_csr* h) {
+  int nv = 0;
+  const TiledVariant* tv = tiled_variants(&nv);
+  for (int i = 0; i < nv; ++i)
+    if (tv[i].K == h->K && tv[i].S == h->stride) {
+      Tiling t{};
+      if (choose_tiling(tv[i], h, 1, &t)) return i + 1;
+    }
+  return 0;
+}
+
+int set_kernel(escoin_csr* h, int id, cudaStream_t s) {
+  int nv = 0;
+  const TiledVariant* tv = tiled_variants(&nv);
+  if (id == ESCOIN_KERNEL_AUTO) id = auto_kernel(h);
+  if (id < 0 || id > nv) return ESCOIN_ERR_UNSUPPORTED;
+  if (id > 0 && (tv[id - 1].K != h->K || tv[id - 1].S != h->stride)) return ESCOIN_ERR_UNSUPPORTED;
+  if (id > 0) {
+    const int rc = prepare_tiled(h, id - 1, s);
+    if (rc != ESCOIN_OK) return rc;
+  } else {
+    free_ds6(h);
+  }
+  h->kernel = id;
+  return ESCOIN_OK;
+}
+
+int validate_shape(int M, int C, int H, int W, int K, int stride, int pad, int* E, int* F) {
+  if (M < 1 || C < 1 || H < 1 || W < 1 || K < 1 || stride < 1 || pad < 0) return ESCOIN_ERR_SHAPE;
+  *E = out_dim(H, K, stride, pad);
+  *F = out_dim(W, K, stride, pad);
+  if (*E < 1 || *F < 1) return ESCOIN_ERR_SHAPE;
+  const int64_t chw = int64_t(C) * (H + 2 * pad) * (W + 2 * pad);
+  if (chw > kInt32Max || int64_t(M) * C * K * K > kInt32Max) return ESCOIN_ERR_OVERFLOW;
+  return ESCOIN_OK;
+}
+
+}  // namespace
+
+// ================================================================ ABI
+extern "C" {
+
+int escoin_csr_stretch(const float* w, int M, int C, int H, int W, int K, int stride, int pad, escoin_csr** out) {
+  if (!w || !out) return ESCOIN_ERR_NULL;
+  *out = nullptr;
+  int E, F;
+  int rc = validate_shape(M, C, H, W, K, stride, pad, &E, &F);
+  if (rc != ESCOIN_OK) return rc;
+  escoin_csr* h = new (std::nothrow) escoin_csr();
+  if (!h) return ESCOIN_ERR_ALLOC;
+  h->M = M; h->C = C; h->H = H; h->W = W; h->K = K; h->stride = stride; h->pad = pad; h->E = E; h->F = F;
+  const int64_t CRS = int64_t(C) * K * K;
+  const int64_t Hp = H + 2 * pad, Wp = W + 2 * pad;
+  try {
+    h->rowptr.resize(size_t(M) + 1);
+    int64_t nnz = 0;
+    for (int m = 0; m < M; ++m) nnz += CRS - std::count(w + m * CRS, w + (m + 1) * CRS, 0.0f);
+    if (nnz > kInt32Max) { delete h; return ESCOIN_ERR_OVERFLOW; }
+    h->colidx.resize(size_t(nnz));
+    h->value.resize(size_t(nnz));
+    // Row m = filter m in (c, kh, kw) order; keep w != 0.0f
+    // (R#6); colidx = f(c, kh, kw) over the padded input (R#4).
+    int64_t j = 0;
+    h->rowptr[0] = 0;
+    for (int m = 0; m < M; ++m) {
+      const float* wm = w + m * CRS;
+      for (int c = 0; c < C; ++c)
+        for (int kh = 0; kh < K; ++kh)
+          for (int kw = 0; kw < K; ++kw) {
+            const float v = wm[(int64_t(c) * K + kh) * K + kw];
+            if (v != 0.0f) {
+              h->colidx[j] = int32_t((c * Hp + kh) * Wp + kw);
+              h->value[j] = v;
+              ++j;
+            }
+          }
+      h->rowptr[m + 1] = int32_t(j);
+    }
+    h->nnz = nnz;
+  } catch (...) {
+    delete h;
+    return ESCOIN_ERR_ALLOC;
+  }
+  *out = h;
+  return ESCOIN_OK;
+}
+
+int escoin_csr_info(const escoin_csr* h, int* M, int* C, int* H, int* W, int* K, int* stride, int* pad,
+                    int64_t* nnz) {
+  if (!h) return ESCOIN_ERR_NULL;
+  if (M) *M = h->M;
+  if (C) *C = h->C;
+  if (H) *H = h->H;
+  if (W) *W = h->W;
+  if (K) *K = h->K;
+  if (stride) *stride = h->stride;
+  if (pad) *pad = h->pad;
+  if (nnz) *nnz = h->nnz;
+  return ESCOIN_OK;
+}
+
+int escoin_csr_host_arrays(const escoin_csr* h, const int32_t** rowptr, const int32_t** colidx,
+                           const float** value) {
+  if (!h) return ESCOIN_ERR_NULL;
+  if (rowptr) *rowptr = h->rowptr.data();
+  if (colidx) *colidx = h->colidx.data();
+  if (value) *value = h->value.data();
+  return ESCOIN_OK;
+}
+
+int escoin_csr_to_device(escoin_csr* h, int device, void* cuda_stream) {
+  if (!h) return ESCOIN_ERR_NULL;
+  if (h->on_device) return h->device == device ? ESCOIN_OK : ESCOIN_ERR_NOT_ON_DEVICE;
+  DeviceGuard g(device);
+  if (!g.ok) return ESCOIN_ERR_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  int rc;
+  if (!h->borrowed) {
+    if ((rc = upload(h->rowptr, &h->d_rowptr, s)) != ESCOIN_OK) return rc;
+    if ((rc = upload(h->colidx, &h->d_colidx, s)) != ESCOIN_OK) return rc;
+    if ((rc = upload(h->value, &h->d_value, s)) != ESCOIN_OK) return rc;
+  }
+  h->device = device;
+  if ((rc = set_kernel(h, h->kernel < 0 ? ESCOIN_KERNEL_AUTO : h->kernel, s)) != ESCOIN_OK) return rc;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return ESCOIN_ERR_CUDA;
+  h->on_device = true;
+  return ESCOIN_OK;
+}
+
+int escoin_csr_wrap_device(const int32_t* d_rowptr, const int32_t* d_colidx, const float* d_value, int64_t nnz,
+                           int M, int C, int H, int W, int K, int stride, int pad, int device, void* cuda_stream,
+                           escoin_csr** out) {
+  if (!d_rowptr || !out || (nnz > 0 && (!d_colidx || !d_value))) return ESCOIN_ERR_NULL;
+  *out = nullptr;
+  int E, F;
+  int rc = validate_shape(M, C, H, W, K, stride, pad, &E, &F);
+  if (rc != ESCOIN_OK) return rc;
+  if (nnz < 0 || nnz > kInt32Max || nnz > int64_t(M) * C * K * K) return ESCOIN_ERR_CSR_MISMATCH;
+  DeviceGuard g(device);
+  if (!g.ok) return ESCOIN_ERR_CUDA;
+  escoin_csr* h = new (std::nothrow) escoin_csr();
+  if (!h) return ESCOIN_ERR_ALLOC;
+  h->M = M; h->C = C; h->H = H; h->W = W; h->K = K; h->stride = stride; h->pad = pad; h->E = E; h->F = F;
+  h->nnz = nnz;
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  try {
+    h->rowptr.resize(size_t(M) + 1);
+    h->colidx.resize(size_t(nnz));
+    h->value.resize(size_t(nnz));
+  } catch (...) {
+    delete h;
+    return ESCOIN_ERR_ALLOC;
+  }
+  bool ok = cudaMemcpyAsync(h->rowptr.data(), d_rowptr, 4 * (size_t(M) + 1), cudaMemcpyDeviceToHost, s) == cudaSuccess;
+  if (nnz > 0) {
+    ok = ok && cudaMemcpyAsync(h->colidx.data(), d_colidx, 4 * size_t(nnz), cudaMemcpyDeviceToHost, s) == cudaSuccess;
+    ok = ok && cudaMemcpyAsync(h->value.data(), d_value, 4 * size_t(nnz), cudaMemcpyDeviceToHost, s) == cudaSuccess;
+  }
+  ok = ok && cudaStreamSynchronize(s) == cudaSuccess;
+  if (!ok) { delete h; return ESCOIN_ERR_CUDA; }
+  // validate the borrowed CSR
+  const int64_t lim = int64_t(C) * (H + 2 * pad) * (W + 2 * pad);
+  bool good = h->rowptr[0] == 0 && h->rowptr[M] == nnz;
+  for (int m = 0; good && m < M; ++m) good = h->rowptr[m] <= h->rowptr[m + 1];
+  for (int64_t j = 0; good && j < nnz; ++j) good = h->colidx[j] >= 0 && h->colidx[j] < lim;
+  if (!good) { delete h; return ESCOIN_ERR_CSR_MISMATCH; }
+  h->borrowed = true;
+  h->d_rowptr = const_cast<int32_t*>(d_rowptr);
+  h->d_colidx = const_cast<int32_t*>(d_colidx);
+  h->d_value = const_cast<float*>(d_value);
+  rc = escoin_csr_to_device(h, device, cuda_stream);
+  if (rc != ESCOIN_OK) { escoin_csr_free(h); return rc; }
+  *out = h;
+  return ESCOIN_OK;
+}
+
+void escoin_csr_free(escoin_csr* h) {
+  if (!h) return;
+  if (h->device >= 0) {
+    DeviceGuard g(h->device);
+    cudaDeviceSynchronize();
+    free_ds6(h);
+    if (!h->borrowed) {
+      if (h->d_rowptr) cudaFree(h->d_rowptr);
+      if (h->d_colidx) cudaFree(h->d_colidx);
+      if (h->d_value) cudaFree(h->d_value);
+    }
+  }
+  delete h;
+}
+
+int escoin_sconv_forward(int N, int C, int H, int W, int M, int K, int stride, int pad, const escoin_csr* h,
+                         const float* in, float* out, const float* bias, int relu, void* cuda_stream) {
+  if (!h) return ESCOIN_ERR_NULL;
+  if (N < 0) return ESCOIN_ERR_SHAPE;
+  if (C != h->C || H != h->H || W != h->W || M != h->M || K != h->K || stride != h->stride || pad != h->pad)
+    return ESCOIN_ERR_CSR_MISMATCH;
+  if (N == 0) return ESCOIN_OK;
+  if (!in || !out) return ESCOIN_ERR_NULL;
+  if (!h->on_device) return ESCOIN_ERR_NOT_ON_DEVICE;
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != h->device) return ESCOIN_ERR_NOT_ON_DEVICE;
+  if (int64_t(N) * C * H * W > (int64_t(1) << 40)) return ESCOIN_ERR_OVERFLOW;
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  int rc;
+  if (h->kernel == 0) {
+    rc = launch_paper(h->d_rowptr, h->d_colidx, h->d_value, in, out, bias, relu ? 1 : 0, N, C, H, W, M, K, stride,
+                      pad, h->E, h->F, s);
+  } else {
+    int nv = 0;
+    const TiledVariant* tv = tiled_variants(&nv);
+    TiledArgs a = h->targs;
+    a.in = in;
+    a.out = out;
+    a.bias = bias;
+    a.relu = relu ? 1 : 0;
+    a.N = N;
+    a.ntiles = ceil_div(N, a.NB) * a.tiles_r;
+    if (a.ntiles > 65535) return ESCOIN_ERR_OVERFLOW;
+    rc = tv[h->kernel - 1].launch(a, s);
+  }
+  return rc == 0 ? ESCOIN_OK : ESCOIN_ERR_CUDA;
+}
+
+int escoin_sconv_forward_hostio(int N, int C, int H, int W, int M, int K, int stride, int pad, const escoin_csr* h,
+                                const float* h_in, float* h_out, float* d_in, float* d_out, const float* bias,
+                                int relu, void* cuda_stream) {
+  if (!h) return ESCOIN_ERR_NULL;
+  if (N > 0 && (!h_in || !h_out || !d_in || !d_out)) return ESCOIN_ERR_NULL;
+  if (C != h->C || H != h->H || W != h->W || M != h->M || K != h->K || stride != h->stride || pad != h->pad)
+    return ESCOIN_ERR_CSR_MISMATCH;
+  if (N == 0) return ESCOIN_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  const size_t in_b = size_t(N) * C * H * W * 4, out_b = size_t(N) * M * h->E * h->F * 4;
+  if (cudaMemcpyAsync(d_in, h_in, in_b, cudaMemcpyHostToDevice, s) != cudaSuccess) return ESCOIN_ERR_CUDA;
+  const int rc = escoin_sconv_forward(N, C, H, W, M, K, stride, pad, h, d_in, d_out, bias, relu, cuda_stream);
+  if (rc != ESCOIN_OK) return rc;
+  if (cudaMemcpyAsync(h_out, d_out, out_b, cudaMemcpyDeviceToHost, s) != cudaSuccess) return ESCOIN_ERR_CUDA;
+  return ESCOIN_OK;
+}
+
+int escoin_kernel_count(void) {
+  int nv = 0;
+  tiled_variants(&nv);
+  return nv + 1;
+}
+
+int escoin_kernel_info(int id, const char** name, int* K, int* stride) {
+  int nv = 0;
+  const TiledVariant* tv = tiled_variants(&nv);
+  if (id < 0 || id > nv) return ESCOIN_ERR_UNSUPPORTED;
+  if (id == 0) {
+    if (name) *name = "paper_mapping";
+    if (K) *K = 0;
+    if (stride) *stride = 0;
+  } else {
+    if (name) *name = tv[id - 1].name;
+    if (K) *K = tv[id - 1].K;
+    if (stride) *stride = tv[id - 1].S;
+  }
+  return ESCOIN_OK;
+}
+
+int escoin_csr_set_kernel(escoin_csr* h, int id) {
+  if (!h) return ESCOIN_ERR_NULL;
+  if (!h->on_device) {
+    int nv = 0;
+    tiled_variants(&nv);
+    if (id != ESCOIN_KERNEL_AUTO && (id < 0 || id > nv)) return ESCOIN_ERR_UNSUPPORTED;
+    h->kernel = id;  // resolved at escoin_csr_to_device
+    return ESCOIN_OK;
+  }
+  DeviceGuard g(h->device);
+  if (!g.ok) return ESCOIN_ERR_CUDA;
+  cudaDeviceSynchronize();  // no forward may be reading the old derived format
+  return set_kernel(h, id, nullptr);
+}
+
+int escoin_csr_get_kernel(const escoin_csr* h, int* id) {
+  if (!h || !id) return ESCOIN_ERR_NULL;
+  *id = h->kernel;
+  return ESCOIN_OK;
+}
+
+const char* escoin_status_string(int status) {
+  switch (status) {
+    case ESCOIN_OK: return "ok";
+    case ESCOIN_ERR_NULL: return "null pointer argument";
+    case ESCOIN_ERR_SHAPE: return "invalid shape";
+    case ESCOIN_ERR_CSR_MISMATCH: return "shape or CSR does not match the handle";
+    case ESCOIN_ERR_NOT_ON_DEVICE: return "handle not on the current device";
+    case ESCOIN_ERR_OVERFLOW: return "index overflow (int32)";
+    case ESCOIN_ERR_UNSUPPORTED: return "unsupported kernel variant / shape";
+    case ESCOIN_ERR_ALLOC: return "allocation failed";
+    case ESCOIN_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+const char* escoin_version(void) { return "escoin-b200 0.1 sm_100a"; }
+
+}  // extern "C"

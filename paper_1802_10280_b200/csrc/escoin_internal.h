@@ -1,0 +1,53 @@
+// escoin_internal.h — shared between the host library and the kernels.
+// Not part of the public ABI (include/escoin.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace escoin {
+
+constexpr int kTiledThreads = 256;   // 8 warps = WM x WP
+constexpr int kMaxStagePos = 8;      // staged plane positions per thread (SR*SCs <= 2048)
+constexpr int kHdrBase = 1 << 20;    // bucket header record: code = kHdrBase + c_local
+constexpr int kDone = -1;            // end of a warp's record stream for one chunk
+
+// Launch parameters of the register-tiled kernel (see sconv_tiled.cuh).
+struct TiledArgs {
+  const float* in;
+  float* out;
+  const float* bias;
+  int relu;
+  int N, C, H, W, M, E, F, pad;
+  int PR, PC;           // patch grid of one image: ceil(E/PH) x ceil(F/PW)
+  int WM, WP, NB, TR;   // warps along m / along pixels; images and patch rows per CTA
+  int SR, SCs, plane;   // staged slab rows, row stride (words), plane stride (words)
+  int CC;               // input channels per chunk
+  int tiles_r;          // ceil(PR / TR)
+  int B, ntiles;        // grid: m-blocks x pixel tiles
+  int stage_floats;     // floats per slab stage (multiple of 4)
+  int stage_recs;       // records per record stage (even)
+  int smem_bytes;
+  const int2* recs;     // derived format (DS-6) records
+  const int* sched;     // per active chunk: [k, rec_start, rec_count, woff[WM]]
+  const int* sched_off; // [B+1] first entry of each m-block
+  int sched_stride;     // 3 + WM
+};
+
+typedef int (*TiledLaunchFn)(const TiledArgs&, cudaStream_t);
+
+struct TiledVariant {
+  const char* name;
+  int K, S, PH, PW, Q;
+  int min_blocks;  // CTAs per SM the kernel is compiled for (__launch_bounds__)
+  TiledLaunchFn launch;
+};
+
+// Paper-mapping kernel (variant 0), sconv_paper.cu.
+int launch_paper(const int* rowptr, const int* colidx, const float* value, const float* in, float* out,
+                 const float* bias, int relu, int N, int C, int H, int W, int M, int K, int S, int pad, int E,
+                 int F, cudaStream_t s);
+
+const TiledVariant* tiled_variants(int* count);
+
+}  // namespace escoin

@@ -1,0 +1,212 @@
+// sconv_tiled.cuh — register-tiled direct sparse convolution for sm_100a.
+//
+// What it computes: Alg.2 of the paper with dynamic indexing
+// (§3.1), stride and virtual zero padding, bias + ReLU fused:
+//   out[n][m][oh][ow] = act(bias[m] + sum_{j in row m} value[j] *
+//                            X~[n][colidx[j] + oh*S*Wp + ow*S])
+// How:
+//   * CTA = (m-block of WM groups x Q output channels) x (pixel tile of NB
+//     images x TR patch-rows x all PC patch-columns).  Warp (wm, wp): output
+//     channels of group wm, pixel slots [32 wp, 32 wp + 32).  Lane = one
+//     PH x PW output patch.  All lanes of a warp walk the same records, so
+//     every branch is warp-uniform (the paper's "avoid unstructured
+//     computation") and weights are smem broadcasts.
+//   * Input channels are processed in chunks of CC; for each chunk the CTA
+//     stages the zero-padded input slab [NB][CC][SR][SCs] (pad_in fused into
+//     the load via cp.async zero-fill, P:705 / reading R#9) and the chunk's
+//     records into shared memory, double-buffered.
+//   * Per input channel c each lane loads its XH x XW input window into
+//     registers once (vector LDS), then runs the bucket of records of
+//     (group, c): each record = one nonzero weight, dispatched by code
+//     q*K*K + kh*K + kw to PH*PW FFMAs on compile-time registers
+//     (bucket_loop, generated inline PTX).  Partial sums stay in registers
+//     for the whole reduction.
+//   * Accumulation order per output channel: ascending (c, kh, kw) ==
+//     ascending colidx, from 0.0f, fp32 FMA — identical to the paper-mapping
+//     kernel, hence bitwise-identical results across variants.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "escoin_internal.h"
+
+namespace escoin {
+
+template <int K, int S, int PH, int PW, int Q>
+__device__ void bucket_loop(float* acc, const float* x, unsigned& p);
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async4(unsigned dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int K, int S, int PH, int PW, int Q, int MINB>
+__global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const TiledArgs a) {
+  constexpr int P = PH * PW;
+  constexpr int XH = (PH - 1) * S + K, XW = (PW - 1) * S + K;
+  constexpr bool VEC = ((PW * S) % 4) == 0;
+  constexpr int XWV = (XW + 3) / 4;
+
+  extern __shared__ __align__(16) float smem[];
+  float* const slab0 = smem;
+  float* const slab1 = smem + a.stage_floats;
+  int2* const rec0 = reinterpret_cast<int2*>(smem + 2 * a.stage_floats);
+  int2* const rec1 = rec0 + a.stage_recs;
+
+  const int b = blockIdx.x;
+  const int tile = blockIdx.y;
+  const int n0 = (tile / a.tiles_r) * a.NB;
+  const int pr0 = (tile % a.tiles_r) * a.TR;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp % a.WM, wp = warp / a.WM;
+  const int slot = wp * 32 + lane;
+  const int per_img = a.TR * a.PC;
+  int img = slot / per_img;
+  int pr = (slot - img * per_img) / a.PC;
+  int pc = slot - img * per_img - pr * a.PC;
+  const bool active = (img < a.NB) && (n0 + img < a.N) && (pr0 + pr < a.PR);
+  if (!active) { img = 0; pr = 0; pc = 0; }
+  const int win_off = img * a.CC * a.plane + pr * PH * S * a.SCs + pc * PW * S;
+
+  // Staging map: thread owns plane positions pos = tid + i*kTiledThreads.
+  // goff = offset inside one unpadded H x W input plane, or -1 for padding.
+  const int plane_elems = a.SR * a.SCs;
+  int goff[kMaxStagePos];
+#pragma unroll
+  for (int i = 0; i < kMaxStagePos; ++i) {
+    const int pos = threadIdx.x + i * kTiledThreads;
+    goff[i] = -1;
+    if (pos < plane_elems) {
+      const int r = pos / a.SCs, col = pos - r * a.SCs;
+      const int y = pr0 * PH * S - a.pad + r, xg = col - a.pad;
+      if (y >= 0 && y < a.H && xg >= 0 && xg < a.W) goff[i] = y * a.W + xg;
+    }
+  }
+
+  const int* const sched = a.sched + static_cast<int64_t>(a.sched_off[b]) * a.sched_stride;
+  const int nact = a.sched_off[b + 1] - a.sched_off[b];
+  const int64_t HW = static_cast<int64_t>(a.H) * a.W;
+
+  auto stage = [&](int ai, int st) {
+    const int* e = sched + ai * a.sched_stride;
+    const int c0 = e[0] * a.CC, rs = e[1], rc = e[2];
+    const unsigned sb = smem_addr(st ? slab1 : slab0);
+    for (int im = 0; im < a.NB; ++im) {
+      const bool iv = (n0 + im) < a.N;
+      for (int cl = 0; cl < a.CC; ++cl) {
+        const bool pv = iv && (c0 + cl) < a.C;
+        const float* g = a.in + (static_cast<int64_t>(n0 + im) * a.C + (c0 + cl)) * HW;
+        const unsigned sp = sb + 4u * static_cast<unsigned>((im * a.CC + cl) * a.plane);
+#pragma unroll
+        for (int i = 0; i < kMaxStagePos; ++i) {
+          const int pos = threadIdx.x + i * kTiledThreads;
+          if (pos < plane_elems) {
+            const bool v = pv && goff[i] >= 0;
+            cp_async4(sp + 4u * pos, v ? (const void*)(g + goff[i]) : (const void*)a.in, v ? 4 : 0);
+          }
+        }
+      }
+    }
+    const unsigned rb = smem_addr(st ? rec1 : rec0);
+    for (int i = threadIdx.x; i < (rc >> 1); i += kTiledThreads) cp_async16(rb + 16u * i, a.recs + rs + 2 * i);
+    cp_async_commit();
+  };
+
+  float acc[Q * P];
+#pragma unroll
+  for (int i = 0; i < Q * P; ++i) acc[i] = 0.0f;
+
+  if (nact > 0) stage(0, 0);
+  for (int ai = 0; ai < nact; ++ai) {
+    const int st = ai & 1;
+    if (ai + 1 < nact) {
+      stage(ai + 1, st ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const float* slab = st ? slab1 : slab0;
+    const int2* rbase = st ? rec1 : rec0;
+    const unsigned rbase_s = smem_addr(rbase);
+    const int2* wr = rbase + sched[ai * a.sched_stride + 3 + wm];
+    for (;;) {
+      const int2 h = *wr;
+      if (h.x < 0) break;  // DONE
+      const float* src = slab + win_off + (h.x - kHdrBase) * a.plane;
+      float x[XH * XW];
+      if constexpr (VEC) {
+#pragma unroll
+        for (int r = 0; r < XH; ++r) {
+#pragma unroll
+          for (int v = 0; v < XWV; ++v) {
+            const float4 t = *reinterpret_cast<const float4*>(src + r * a.SCs + 4 * v);
+            if (4 * v + 0 < XW) x[r * XW + 4 * v + 0] = t.x;
+            if (4 * v + 1 < XW) x[r * XW + 4 * v + 1] = t.y;
+            if (4 * v + 2 < XW) x[r * XW + 4 * v + 2] = t.z;
+            if (4 * v + 3 < XW) x[r * XW + 4 * v + 3] = t.w;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < XH; ++r)
+#pragma unroll
+          for (int c = 0; c < XW; ++c) x[r * XW + c] = src[r * a.SCs + c];
+      }
+      unsigned p = smem_addr(wr + 1);
+      bucket_loop<K, S, PH, PW, Q>(acc, x, p);
+      wr = rbase + ((p - rbase_s) >> 3);
+    }
+    __syncthreads();
+  }
+
+  // Epilogue (reading R#10): v = acc + bias[m]; ReLU; NCHW store.
+  if (active) {
+    const int n = n0 + img;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int m = (b * a.WM + wm) * Q + q;
+      if (m < a.M) {
+        const float bv = a.bias ? __ldg(a.bias + m) : 0.0f;
+        float* o = a.out + (static_cast<int64_t>(n) * a.M + m) * a.E * a.F;
+#pragma unroll
+        for (int ph = 0; ph < PH; ++ph) {
+          const int oh = (pr0 + pr) * PH + ph;
+#pragma unroll
+          for (int pw = 0; pw < PW; ++pw) {
+            const int ow = pc * PW + pw;
+            if (oh < a.E && ow < a.F) {
+              float v = __fadd_rn(acc[q * P + ph * PW + pw], bv);
+              if (a.relu) v = v > 0.0f ? v : 0.0f;
+              o[oh * a.F + ow] = v;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int K, int S, int PH, int PW, int Q, int MINB>
+int launch_tiled(const TiledArgs& a, cudaStream_t s) {
+  auto kern = sconv_tiled_kernel<K, S, PH, PW, Q, MINB>;
+  if (a.smem_bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  dim3 grid(a.B, a.ntiles);
+  kern<<<grid, kTiledThreads, a.smem_bytes, s>>>(a);
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace escoin
