@@ -1,0 +1,453 @@
+#!/usr/bin/env python
+"""Benchmark of the Escoin direct sparse convolution on B200.
+
+One step = one pass of the hot path over one batch: every sparse CONV layer
+of the workload (default: pruned AlexNet conv2-conv5, BASELINE configs[1]),
+batch 128 per GPU, through escoin_sconv_forward (stretched CSR x dense NCHW,
+bias + ReLU fused).  Inputs resident in HBM; L2 flushed between steps (a
+256 MB write, outside the per-step events).  Multi-GPU: torchrun, one rank
+per GPU, each rank runs its own 128 images (weak scaling; weights broadcast
+once over NCCL; no per-layer collectives); time = MAX over ranks.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle
+instead (the reference arm for this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1802_10280_b200 import inputs, shard, workloads  # noqa: E402
+
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+WL_NAMES = {"alexnet": "pruned AlexNet conv2-conv5 (4 sparse CONV layers)",
+            "googlenet": "pruned GoogLeNet 19 sparse 3x3/5x5 CONV layers",
+            "googlenet_1x1": "pruned GoogLeNet 37 1x1 CONV layers",
+            "resnet50": "pruned ResNet-50 v1 16 sparse 3x3 CONV layers",
+            "tiny": "tiny conv layer N=1 C=16 14x14 M=32 3x3"}
+METRIC = "sparse-conv images/s (whole stack) at batch 128/GPU"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="escoin", choices=["escoin", "reference"])
+    p.add_argument("--workload", default="alexnet", choices=list(WL_NAMES))
+    p.add_argument("--batch", type=int, default=None, help="images per GPU (default: the workload's, 128)")
+    p.add_argument("--sparsity", type=int, default=800, help="per-mille (ASSUMED 800, reading R#14)")
+    p.add_argument("--kernel", type=int, default=-1, help="sconv variant id (-1 = auto)")
+    p.add_argument("--no-baselines", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--out", default=None, help="also write the JSON line to this file")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.rows = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for r in self.rows:
+            f = [x.strip() for x in r.split(",")]
+            if len(f) < 4:
+                continue
+            try:
+                s, m = float(f[0]), float(f[1])
+                bits = int(f[3], 16)
+            except ValueError:
+                continue
+            mx = m
+            if bits & 0x1:  # idle sample: not under load
+                continue
+            sm.append(s)
+            for b, n in REASON_BITS.items():
+                if bits & b:
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ setup
+class LayerRun:
+    pass
+
+
+def setup(args, wl, device, rank, world, torch, escoin):
+    B = args.batch or wl.batch
+    n0 = rank * B  # weak scaling: rank r owns global images [r*B, (r+1)*B)
+    runs = []
+    for L in wl.layers:
+        r = LayerRun()
+        r.L = L
+        if rank == 0:
+            w = inputs.layer_weights(wl.net, L, args.sparsity)
+            bias = inputs.bias(wl.net, L.name, L.M)
+            src = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad)
+            rp, ci, v = src.host_arrays()
+            r.w_dense = w
+        else:
+            rp = ci = v = bias = None
+            r.w_dense = None
+        if world > 1:
+            t = shard.broadcast_csr(rp, ci, v, bias, device)
+            r.d_csr = t[:3]
+            r.bias = t[3]
+            r.csr = escoin.Csr.wrap_device(t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(), t[1].numel(), L.M, L.C,
+                                           L.H, L.W, L.K, L.stride, L.pad, device.index,
+                                           torch.cuda.current_stream().cuda_stream)
+            if args.kernel != -1:
+                r.csr.set_kernel(args.kernel)
+        else:
+            r.csr = src
+            r.csr.set_kernel(args.kernel)
+            r.csr.to_device(device.index, torch.cuda.current_stream().cuda_stream)
+            r.bias = torch.from_numpy(bias).to(device)
+        r.nnz = int(r.csr.info()["nnz"])
+        r.kernel = escoin.kernels()[r.csr.kernel()][1]
+        x = inputs.activations(wl.net, L.name, n0, B, L.C, L.H, L.W)
+        r.h_x = torch.from_numpy(x).pin_memory()
+        r.x = r.h_x.to(device)
+        r.out = torch.empty((B, L.M, L.E, L.F), dtype=torch.float32, device=device)
+        r.h_out = torch.empty((B, L.M, L.E, L.F), dtype=torch.float32).pin_memory()
+        r.flops = 2.0 * B * r.nnz * L.E * L.F
+        r.alg_bytes = 4.0 * (B * L.C * L.H * L.W + B * L.M * L.E * L.F + 2 * r.nnz + L.M + 1 + L.M)
+        runs.append(r)
+    torch.cuda.synchronize()
+    return runs, B
+
+
+def fwd(escoin, r, stream):
+    L = r.L
+    escoin.sconv_forward(r.x.shape[0], L.C, L.H, L.W, L.M, L.K, L.stride, L.pad, r.csr, r.x, r.out, r.bias, True,
+                         stream)
+
+
+def time_device(torch, runs, steps, warmup, flush, step_fn):
+    """Per-step CUDA events around each layer; L2 flushed before every step."""
+    s = torch.cuda.current_stream()
+    for _ in range(warmup):
+        flush.zero_()
+        step_fn()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(runs) + 1)] for _ in range(steps)]
+    for k in range(steps):
+        flush.zero_()
+        ev[k][0].record(s)
+        for i, r in enumerate(runs):
+            step_fn(i)
+            ev[k][i + 1].record(s)
+    torch.cuda.synchronize()
+    per_layer = np.array([[ev[k][i].elapsed_time(ev[k][i + 1]) for i in range(len(runs))] for k in range(steps)])
+    return per_layer  # ms [steps][layers]
+
+
+def cpu_oracle_timed(wl, args, seconds, max_images):
+    """Time only the oracle calls (inputs pre-generated) on a bounded image sample."""
+    import oracle
+    items = []
+    for L in wl.layers:
+        w = inputs.layer_weights(wl.net, L, args.sparsity)
+        items.append((L, oracle.csr_stretch(w, L.H, L.W, L.stride, L.pad), inputs.bias(wl.net, L.name, L.M)))
+    el = 0.0
+    n = 0
+    while n < max_images and el < seconds:
+        for L, (rp, ci, v), b in items:
+            x = inputs.activations(wl.net, L.name, n, 1, L.C, L.H, L.W)
+            ts = time.perf_counter()
+            oracle.sconv(x, rp, ci, v, L.M, L.K, L.stride, L.pad, bias=b, relu=True)
+            el += time.perf_counter() - ts
+        n += 1
+    return n, el, oracle.num_threads()
+
+
+def sm_peak_tflops(torch, device, sm_max_mhz):
+    props = torch.cuda.get_device_properties(device)
+    # FP32 FFMA: 128 lanes/SM x 2 flop x clock (B200_PROFILING / blackwell guide unit counts)
+    return props.multi_processor_count * 128 * 2 * sm_max_mhz * 1e6 / 1e12, props.multi_processor_count
+
+
+def load_traffic(workload):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(path)).get(workload, {})
+    except Exception:
+        return {}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank, world, _ = shard.world()
+    if rank != 0:
+        return 0
+    wl = workloads.workload(args.workload)
+    import oracle
+    items = []
+    for L in wl.layers:
+        w = inputs.layer_weights(wl.net, L, args.sparsity)
+        items.append((L, oracle.csr_stretch(w, L.H, L.W, L.stride, L.pad), inputs.bias(wl.net, L.name, L.M)))
+    per_step_images = 1
+    xs = {L.name: inputs.activations(wl.net, L.name, 0, per_step_images, L.C, L.H, L.W) for L, _, _ in items}
+
+    def step():
+        for L, (rp, ci, v), b in items:
+            oracle.sconv(xs[L.name], rp, ci, v, L.M, L.K, L.stride, L.pad, bias=b, relu=True)
+
+    for _ in range(args.warmup):
+        step()
+    t = []
+    for _ in range(args.steps):
+        ts = time.perf_counter()
+        step()
+        t.append(time.perf_counter() - ts)
+    ms = 1e3 * float(np.mean(t))
+    value = per_step_images / (ms / 1e3)
+    sample = "%d image(s) through all %d layers per step" % (per_step_images, len(items))
+    line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": WL_NAMES[args.workload], "batch_per_gpu": wl.batch,
+                       "sparsity": args.sparsity / 1000.0, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "images/s", "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if args.out:
+        open(args.out, "w").write(json.dumps(line) + "\n")
+    return 0
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    from paper_1802_10280_b200 import escoin
+
+    rank, world, local = shard.world()
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    wl = workloads.workload(args.workload)
+    runs, B = setup(args, wl, device, rank, world, torch, escoin)
+    stream = torch.cuda.current_stream().cuda_stream
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+
+    def step_fn(i=None):
+        if i is None:
+            for r in runs:
+                fwd(escoin, r, stream)
+        else:
+            fwd(escoin, runs[i], stream)
+
+    # ---------------- device-timed region (K steps, barrier + sync both sides)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        wall0 = time.perf_counter()
+        per_layer = time_device(torch, runs, args.steps, args.warmup, flush, step_fn)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms_local = float(per_layer.sum(1).mean())
+    step_ms = shard.max_over_ranks(step_ms_local, device)
+    value = B * world / (step_ms / 1e3)
+    layer_ms = per_layer.mean(0)
+
+    # ---------------- e2e through the C-ABI with host buffers
+    def e2e_step():
+        for r in runs:
+            L = r.L
+            escoin.sconv_forward_hostio(B, L.C, L.H, L.W, L.M, L.K, L.stride, L.pad, r.csr, r.h_x, r.h_out, r.x,
+                                        r.out, r.bias, True, stream)
+
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = shard.max_over_ranks(e0.elapsed_time(e1) / e2e_steps, device)
+    h2d = sum(r.h_x.numel() * 4 for r in runs)
+    d2h = sum(r.h_out.numel() * 4 for r in runs)
+
+    # ---------------- roofline of the dominant kernel
+    peaks = measured_peaks()
+    clocks = clk.summary()
+    sm_max = clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    peak_tf, nsm = sm_peak_tflops(torch, device, sm_max)
+    dom = int(np.argmax(layer_ms))
+    rd = runs[dom]
+    achieved = rd.flops / (layer_ms[dom] / 1e3) / 1e12
+    traffic = load_traffic(args.workload).get(rd.L.name)
+    layers_out = []
+    for r, ms in zip(runs, layer_ms):
+        layers_out.append({"layer": r.L.name, "ms": round(float(ms), 5), "kernel": r.kernel, "nnz": r.nnz,
+                           "gflop": round(r.flops / 1e9, 4),
+                           "tflops": round(r.flops / (ms / 1e3) / 1e12, 3),
+                           "frac_fp32": round(r.flops / (ms / 1e3) / 1e12 / peak_tf, 4),
+                           "alg_gbs": round(r.alg_bytes / (ms / 1e3) / 1e9, 1)})
+
+    line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WL_NAMES[args.workload], "batch_per_gpu": B, "global_batch": B * world,
+                       "sparsity": args.sparsity / 1000.0, "sparsity_note": "ASSUMED 80% (paper prints none)",
+                       "parallelism": "dp%d (batch-sharded, weights replicated)" % world,
+                       "l2": "flushed (256 MB write) before every step, outside the per-step events"},
+            "roofline": {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak_tf, 2),
+                         "unit": "TFLOP/s", "frac": round(achieved / peak_tf, 4), "traffic": traffic,
+                         "kernel": "sconv %s (%s)" % (rd.kernel, rd.L.name),
+                         "peak_basis": "FP32 FFMA %d SMs x 128 lanes x 2 x %.0f MHz (derived, DESIGN.md)" % (
+                             nsm, sm_max),
+                         "hbm_view": {"alg_gbs": round(rd.alg_bytes / (layer_ms[dom] / 1e3) / 1e9, 1),
+                                      "peak_gbs": peaks.get("hbm_gbs")}},
+            "layers": layers_out,
+            "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "images/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": len(runs) * args.steps,
+            "clocks": clocks,
+            "wall_s_timed_region": round(wall, 3)}
+
+    if rank == 0 and world == 1 and not args.no_baselines:
+        line["baselines"] = run_baselines(torch, escoin, runs, flush, stream, args, value)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n, el, cores = cpu_oracle_timed(wl, args, args.cpu_seconds, B)
+        line["cpu_baseline"] = {"value": n / el, "unit": "images/s", "cores": cores, "kind": "oracle",
+                                "sample": "%d image(s) x %d layers, fp64 oracle (OpenMP over (n,m))" % (n, len(runs))}
+    if rank == 0:
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            open(args.out, "w").write(s + "\n")
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_baselines(torch, escoin, runs, flush, stream, args, sconv_value):
+    """im2col+cuBLAS, im2col+cuSPARSE, cuDNN and the paper's own mapping, same inputs/outputs."""
+    import baselines as bl
+    out = {}
+    reps, warm = 5, 2
+    s = torch.cuda.current_stream()
+
+    def time_fn(fn):
+        for _ in range(warm):
+            flush.zero_()
+            fn()
+        torch.cuda.synchronize()
+        tot = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            fn()
+            b.record(s)
+            torch.cuda.synchronize()
+            tot.append(a.elapsed_time(b))
+        return float(np.median(tot))
+
+    B = runs[0].x.shape[0]
+    for mode in ["cublas", "cusparse", "cudnn"]:
+        per = {}
+        try:
+            for r in runs:
+                if mode == "cudnn":
+                    op = bl.CudnnConv(r.L, r.w_dense, r.bias.cpu().numpy(), r.x.device)
+                else:
+                    op = bl.LoweredConv(r.L, r.w_dense, r.bias.cpu().numpy(), r.x.device, mode)
+                y = torch.empty_like(r.out)
+                per[r.L.name] = time_fn(lambda: op(r.x, y))
+                del op, y
+            tot = sum(per.values())
+            out[{"cublas": "im2col+cublas_sgemm", "cusparse": "im2col+cusparse_spmm",
+                 "cudnn": "cudnn_fp32_dense"}[mode]] = {
+                "images_per_s": B / (tot / 1e3), "ms_per_layer": {k: round(v, 4) for k, v in per.items()},
+                "escoin_speedup": round(sconv_value / (B / (tot / 1e3)), 3)}
+        except Exception as e:  # report, do not hide
+            out[mode] = {"error": repr(e)[:300]}
+        torch.cuda.empty_cache()
+    # the paper's Pascal-era mapping (variant 0) on B200, as an ablation
+    per = {}
+    for r in runs:
+        L = r.L
+        c = escoin.Csr.stretch(r.w_dense, L.H, L.W, L.stride, L.pad)
+        c.set_kernel(0)
+        c.to_device(r.x.device.index, stream)
+        per[L.name] = time_fn(lambda: escoin.sconv_forward(B, L.C, L.H, L.W, L.M, L.K, L.stride, L.pad, c, r.x,
+                                                           r.out, r.bias, True, stream))
+        c.free()
+    tot = sum(per.values())
+    out["escoin_paper_mapping"] = {"images_per_s": B / (tot / 1e3),
+                                   "ms_per_layer": {k: round(v, 4) for k, v in per.items()},
+                                   "escoin_speedup": round(sconv_value / (B / (tot / 1e3)), 3)}
+    return out
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -129,12 +129,11 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, Tiling* b
     t.SR = (t.TR * v.PH - 1) * v.S + v.K;
     t.SC = (t.PC * v.PW - 1) * v.S + v.K;
     const int SC4 = (t.SC + 3) & ~3;
-    if (t.SR * SC4 > kMaxStagePos * kTiledThreads) continue;
+    if (t.SR * h->W > kMaxStagePos * kTiledThreads) continue;  // interior floats per staged plane
     // pick row/plane padding that minimises LDS.128 bank-group conflicts
     int bestc = 1 << 30;
     for (int sp = 0; sp < 8; ++sp) {
       const int SCs = SC4 + 4 * sp;
-      if (t.SR * SCs > kMaxStagePos * kTiledThreads) break;
       for (int pp = 0; pp < 8; ++pp) {
         Tiling u = t;
         u.SCs = SCs;
@@ -152,7 +151,7 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, Tiling* b
     const int B = ceil_div(G, WM);
     const double warp_util = double(G) / (B * WM);
     const double compute = v.Q * dens * v.K * v.K * (P + 9) + XH * ((XW + 3) / 4) * (bestc > 1 ? bestc : 1) + 12;
-    const double staging = 3.0 * t.NB * t.SR * t.SCs / kTiledThreads;
+    const double staging = 5.0 * t.NB * std::min(t.SR, h->H) * h->W / kTiledThreads;
     t.cost = (compute + staging) / (lane_util * pix_util * warp_util * v.Q * P);
     if (!found || t.cost < best->cost) {
       *best = t;

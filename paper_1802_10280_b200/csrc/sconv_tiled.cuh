@@ -78,20 +78,23 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   if (!active) { img = 0; pr = 0; pc = 0; }
   const int win_off = img * a.CC * a.plane + pr * PH * S * a.SCs + pc * PW * S;
 
-  // Staging map: thread owns plane positions pos = tid + i*kTiledThreads.
-  // goff = offset inside one unpadded H x W input plane, or -1 for padding.
-  const int plane_elems = a.SR * a.SCs;
-  int goff[kMaxStagePos];
-#pragma unroll
-  for (int i = 0; i < kMaxStagePos; ++i) {
-    const int pos = threadIdx.x + i * kTiledThreads;
-    goff[i] = -1;
-    if (pos < plane_elems) {
-      const int r = pos / a.SCs, col = pos - r * a.SCs;
-      const int y = pr0 * PH * S - a.pad + r, xg = col - a.pad;
-      if (y >= 0 && y < a.H && xg >= 0 && xg < a.W) goff[i] = y * a.W + xg;
-    }
+  // Staging map (pad_in fused, reading R#9).  Every slab cell outside the
+  // real input (padding ring, rows beyond the image) is zeroed once below and
+  // never written again; per chunk only the interior rows are copied.  The
+  // interior of one plane is a CONTIGUOUS run of nrow*W floats in the NCHW
+  // input (rows y0 .. y0+nrow-1), so element e of that run goes to smem cell
+  // (r_lo + e / W) * SCs + pad + e % W; each thread owns e = tid + i*256 and
+  // copies it for every (image, channel) plane of the chunk.
+  const int y_first = pr0 * PH * S - a.pad;               // global row of slab row 0
+  const int r_lo = y_first < 0 ? -y_first : 0;            // first interior slab row
+  const int y0 = y_first + r_lo;                          // its global row (>= 0)
+  const int nrow = max(0, min(a.SR - r_lo, a.H - y0));    // interior rows in the slab
+  const int nint = nrow * a.W;                            // interior floats per plane
+  {
+    float4* z = reinterpret_cast<float4*>(smem);
+    for (int i = threadIdx.x; i < (2 * a.stage_floats) / 4; i += kTiledThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  __syncthreads();
 
   const int* const sched = a.sched + static_cast<int64_t>(a.sched_off[b]) * a.sched_stride;
   const int nact = a.sched_off[b + 1] - a.sched_off[b];
@@ -101,19 +104,26 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
     const int* e = sched + ai * a.sched_stride;
     const int c0 = e[0] * a.CC, rs = e[1], rc = e[2];
     const unsigned sb = smem_addr(st ? slab1 : slab0);
-    for (int im = 0; im < a.NB; ++im) {
-      const bool iv = (n0 + im) < a.N;
-      for (int cl = 0; cl < a.CC; ++cl) {
-        const bool pv = iv && (c0 + cl) < a.C;
-        const float* g = a.in + (static_cast<int64_t>(n0 + im) * a.C + (c0 + cl)) * HW;
-        const unsigned sp = sb + 4u * static_cast<unsigned>((im * a.CC + cl) * a.plane);
-#pragma unroll
-        for (int i = 0; i < kMaxStagePos; ++i) {
-          const int pos = threadIdx.x + i * kTiledThreads;
-          if (pos < plane_elems) {
-            const bool v = pv && goff[i] >= 0;
-            cp_async4(sp + 4u * pos, v ? (const void*)(g + goff[i]) : (const void*)a.in, v ? 4 : 0);
-          }
+    // thread-owned interior elements ee; planes (image, channel) in the inner loop
+    for (int ee = threadIdx.x; ee < nint; ee += kTiledThreads) {
+      const int r = ee / a.W;
+      const unsigned so = sb + 4u * static_cast<unsigned>((r_lo + r) * a.SCs + a.pad + ee - r * a.W);
+      const float* gbase = a.in + static_cast<int64_t>(y0) * a.W + ee;
+      for (int im = 0; im < a.NB; ++im) {
+        const int n = n0 + im;
+        const int ncl = n < a.N ? min(a.CC, a.C - c0) : 0;  // valid planes; the rest are re-zeroed
+        const float* g = gbase + (static_cast<int64_t>(n < a.N ? n : 0) * a.C + c0) * HW;
+        unsigned sp = so + 4u * static_cast<unsigned>(im * a.CC * a.plane);
+        int cl = 0;
+#pragma unroll 4
+        for (; cl < ncl; ++cl) {
+          cp_async4(sp, g, 4);
+          sp += 4u * a.plane;
+          g += HW;
+        }
+        for (; cl < a.CC; ++cl) {
+          cp_async4(sp, a.in, 0);
+          sp += 4u * a.plane;
         }
       }
     }
