@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--batch", type=int, default=None, help="images per GPU (default: the workload's, 128)")
     p.add_argument("--sparsity", type=int, default=800, help="per-mille (ASSUMED 800, reading R#14)")
     p.add_argument("--kernel", type=int, default=-1, help="sconv variant id (-1 = auto)")
+    p.add_argument("--no-autotune", action="store_true", help="skip escoin_csr_autotune at setup")
     p.add_argument("--no-baselines", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -150,11 +151,16 @@ def setup(args, wl, device, rank, world, torch, escoin):
             r.csr.to_device(device.index, torch.cuda.current_stream().cuda_stream)
             r.bias = torch.from_numpy(bias).to(device)
         r.nnz = int(r.csr.info()["nnz"])
-        r.kernel = escoin.kernels()[r.csr.kernel()][1]
         x = inputs.activations(wl.net, L.name, n0, B, L.C, L.H, L.W)
         r.h_x = torch.from_numpy(x).pin_memory()
         r.x = r.h_x.to(device)
         r.out = torch.empty((B, L.M, L.E, L.F), dtype=torch.float32, device=device)
+        r.tune = None
+        if args.kernel == -1 and not args.no_autotune:
+            # kernel customization (paper §3.4): measured once at setup, untimed
+            kid, kms = r.csr.autotune(B, r.x, r.out, r.bias, True, 3, torch.cuda.current_stream().cuda_stream)
+            r.tune = {"kernel_id": kid, "ms": round(kms, 4)}
+        r.kernel = escoin.kernels()[r.csr.kernel()][1]
         r.h_out = torch.empty((B, L.M, L.E, L.F), dtype=torch.float32).pin_memory()
         r.flops = 2.0 * B * r.nnz * L.E * L.F
         r.alg_bytes = 4.0 * (B * L.C * L.H * L.W + B * L.M * L.E * L.F + 2 * r.nnz + L.M + 1 + L.M)

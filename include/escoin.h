@@ -147,6 +147,18 @@ int escoin_csr_set_kernel(escoin_csr* csr, int id);
 /* The variant the handle currently uses (after AUTO resolution). */
 int escoin_csr_get_kernel(const escoin_csr* csr, int* id);
 
+/* Measured kernel customization (§3.4 P:563-564 "the optimization space we
+ * explore includes the grid shape and thread block size"): time every
+ * compiled variant that accepts the handle's (K, stride) — including the
+ * paper mapping — on the caller's buffers (same meaning as
+ * escoin_sconv_forward; `out` is overwritten), `reps` timed forwards each
+ * after one warm-up, and keep the fastest.  Synchronous on cuda_stream.
+ * *best_id (may be NULL) receives the chosen variant, *best_ms its mean time.
+ * All variants give bitwise-identical outputs, so this never changes results.
+ * Errors: as escoin_sconv_forward, plus CUDA/ALLOC from the rebuilds. */
+int escoin_csr_autotune(escoin_csr* csr, int N, const float* in, float* out, const float* bias, int relu,
+                        int reps, void* cuda_stream, int* best_id, float* best_ms);
+
 const char* escoin_status_string(int status);
 /* Library version string, e.g. "escoin-b200 0.1 sm_100a". */
 const char* escoin_version(void);

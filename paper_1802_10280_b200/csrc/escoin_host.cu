@@ -103,6 +103,7 @@ int window_conflicts(const TiledVariant& v, const Tiling& t, int CC) {
 }
 
 bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, Tiling* best) {
+  const double slab_budget = (v.min_blocks > 1 ? 110.0 : 220.0) * 1024 * 0.85;  // leave room for records
   const int E = h->E, F = h->F;
   const int PR = ceil_div(E, v.PH), PC = ceil_div(F, v.PW);
   const int G = ceil_div(h->M, v.Q);
@@ -146,11 +147,20 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, Tiling* b
         }
       }
     }
+    if (2.0 * 4.0 * t.NB * CC * t.plane > slab_budget) continue;  // double-buffered slab must fit
     const double lane_util = double(t.NB * t.TR * t.PC) / slots;
     const double pix_util = double(E) * F / (double(PR * v.PH) * (PC * v.PW));
     const int B = ceil_div(G, WM);
     const double warp_util = double(G) / (B * WM);
-    const double compute = v.Q * dens * v.K * v.K * (P + 9) + XH * ((XW + 3) / 4) * (bestc > 1 ? bestc : 1) + 12;
+    // per input channel and thread: records x (FFMAs + dispatch), window loads,
+    // bucket overhead; dispatch latency is ~60 issue-slot equivalents per record
+    // with 2 CTAs/SM, more with 1; cases beyond ~12 KB of SASS miss the I-cache.
+    const int NC = v.Q * v.K * v.K;
+    const double code_kb = NC * (P + 9) * 16.0 / 1024.0;
+    const double lat = (v.min_blocks > 1 ? 40.0 : 80.0) * (code_kb > 12.0 ? code_kb / 12.0 : 1.0);
+    const bool vec = ((v.PW * v.S) % 4 == 0) || PC == 1;
+    const double win = vec ? XH * ((XW + 3) / 4) * (bestc > 1 ? bestc : 1) : XH * XW;
+    const double compute = v.Q * dens * v.K * v.K * (P + 9 + lat) + win + 30;
     const double staging = 5.0 * t.NB * std::min(t.SR, h->H) * h->W / kTiledThreads;
     t.cost = (compute + staging) / (lane_util * pix_util * warp_util * v.Q * P);
     if (!found || t.cost < best->cost) {
@@ -253,28 +263,40 @@ int upload(const std::vector<T>& v, T** d, cudaStream_t s) {
   return ESCOIN_OK;
 }
 
+// Host-only planning of a tiled variant: tiling, channel chunk CC, derived
+// format and shared-memory budget.  Returns ESCOIN_ERR_UNSUPPORTED when the
+// variant cannot tile this layer.
+int plan_tiled(const escoin_csr* h, const TiledVariant& v, Tiling* t, int* CCout, DS6* ds, size_t* smem,
+               size_t* stage_f_out, size_t* stage_r_out) {
+  for (int CC = 32; CC >= 1; CC /= 2) {
+    if (!choose_tiling(v, h, CC, t)) continue;  // slab too large at this CC: try a smaller chunk
+    build_ds6(h, v, t->WM, CC, ds);
+    const size_t stage_f = (size_t(t->NB) * CC * t->plane + 3) & ~size_t(3);
+    const size_t stage_r = std::max<size_t>((ds->max_block + 1) & ~1, 2);
+    *smem = 2 * stage_f * 4 + 2 * stage_r * 8;
+    if (*smem <= size_t(v.min_blocks > 1 ? 110 : 220) * 1024) {
+      *CCout = CC;
+      *stage_f_out = stage_f;
+      *stage_r_out = stage_r;
+      return ESCOIN_OK;
+    }
+  }
+  return ESCOIN_ERR_UNSUPPORTED;
+}
+
 // Build + upload the derived format of tiled variant `vi` (index into the table).
 int prepare_tiled(escoin_csr* h, int vi, cudaStream_t s) {
   int nv = 0;
   const TiledVariant* tv = tiled_variants(&nv);
   const TiledVariant& v = tv[vi];
-  int CC = 32;
+  int CC = 0;
   Tiling t{};
   DS6 ds;
-  size_t smem = 0;
-  for (;; CC /= 2) {
-    if (CC < 1) return ESCOIN_ERR_UNSUPPORTED;
-    if (!choose_tiling(v, h, CC, &t)) return ESCOIN_ERR_UNSUPPORTED;
-    build_ds6(h, v, t.WM, CC, &ds);
-    const size_t stage_f = (size_t(t.NB) * CC * t.plane + 3) & ~size_t(3);
-    const size_t stage_r = (ds.max_block + 1) & ~1;
-    smem = 2 * stage_f * 4 + 2 * stage_r * 8;
-    if (smem <= (v.min_blocks > 1 ? 110 : 220) * 1024) {
-      h->targs.stage_floats = int(stage_f);
-      h->targs.stage_recs = int(std::max<size_t>(stage_r, 2));
-      break;
-    }
-  }
+  size_t smem = 0, stage_f = 0, stage_r = 0;
+  const int prc = plan_tiled(h, v, &t, &CC, &ds, &smem, &stage_f, &stage_r);
+  if (prc != ESCOIN_OK) return prc;
+  h->targs.stage_floats = int(stage_f);
+  h->targs.stage_recs = int(stage_r);
   free_ds6(h);
   int rc;
   if ((rc = upload(ds.recs, &h->d_recs, s)) != ESCOIN_OK) return rc;
@@ -309,15 +331,22 @@ int prepare_tiled(escoin_csr* h, int vi, cudaStream_t s) {
   return ESCOIN_OK;
 }
 
+// Default variant (before/without escoin_csr_autotune): lowest modelled cost.
 int auto_kernel(const escoin_csr* h) {
   int nv = 0;
   const TiledVariant* tv = tiled_variants(&nv);
+  int best = 0;
+  double best_cost = 0.0;
   for (int i = 0; i < nv; ++i)
     if (tv[i].K == h->K && tv[i].S == h->stride) {
       Tiling t{};
-      if (choose_tiling(tv[i], h, 1, &t)) return i + 1;
+      if (!choose_tiling(tv[i], h, 8, &t)) continue;
+      if (best == 0 || t.cost < best_cost) {
+        best = i + 1;
+        best_cost = t.cost;
+      }
     }
-  return 0;
+  return best;
 }
 
 int set_kernel(escoin_csr* h, int id, cudaStream_t s) {
@@ -587,6 +616,48 @@ int escoin_csr_set_kernel(escoin_csr* h, int id) {
   return set_kernel(h, id, nullptr);
 }
 
+int escoin_csr_autotune(escoin_csr* h, int N, const float* in, float* out, const float* bias, int relu, int reps,
+                        void* cuda_stream, int* best_id, float* best_ms) {
+  if (!h) return ESCOIN_ERR_NULL;
+  if (!h->on_device) return ESCOIN_ERR_NOT_ON_DEVICE;
+  if (reps < 1) reps = 1;
+  DeviceGuard g(h->device);
+  if (!g.ok) return ESCOIN_ERR_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return ESCOIN_ERR_CUDA;
+  int nv = 0;
+  const TiledVariant* tv = tiled_variants(&nv);
+  int best = -1;
+  float best_t = 0.f;
+  int rc = ESCOIN_OK;
+  for (int id = 0; id <= nv && rc == ESCOIN_OK; ++id) {
+    if (id > 0 && (tv[id - 1].K != h->K || tv[id - 1].S != h->stride)) continue;
+    if (cudaStreamSynchronize(s) != cudaSuccess) { rc = ESCOIN_ERR_CUDA; break; }
+    if (set_kernel(h, id, s) != ESCOIN_OK) continue;  // tiling does not fit: skip
+    rc = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
+    if (rc != ESCOIN_OK) break;
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < reps && rc == ESCOIN_OK; ++r)
+      rc = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) != cudaSuccess) { rc = ESCOIN_ERR_CUDA; break; }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+    if (best < 0 || ms < best_t) { best = id; best_t = ms; }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc != ESCOIN_OK) return rc;
+  if (best < 0) return ESCOIN_ERR_UNSUPPORTED;
+  if ((rc = set_kernel(h, best, s)) != ESCOIN_OK) return rc;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return ESCOIN_ERR_CUDA;
+  if (best_id) *best_id = best;
+  if (best_ms) *best_ms = best_t;
+  return ESCOIN_OK;
+}
+
 int escoin_csr_get_kernel(const escoin_csr* h, int* id) {
   if (!h || !id) return ESCOIN_ERR_NULL;
   *id = h->kernel;
@@ -609,5 +680,24 @@ const char* escoin_status_string(int status) {
 }
 
 const char* escoin_version(void) { return "escoin-b200 0.1 sm_100a"; }
+
+/* Internal (not in escoin.h): host-only plan of tiled variant `id` for tests.
+ * out[12] = {WM, WP, NB, TR, PR, PC, SR, SCs, plane, CC, smem_bytes, records}. */
+int escoin_internal_plan(const escoin_csr* h, int id, int64_t* out) {
+  int nv = 0;
+  const TiledVariant* tv = tiled_variants(&nv);
+  if (!h || !out) return ESCOIN_ERR_NULL;
+  if (id < 1 || id > nv) return ESCOIN_ERR_UNSUPPORTED;
+  Tiling t{};
+  DS6 ds;
+  int CC = 0;
+  size_t smem = 0, sf = 0, sr = 0;
+  const int rc = plan_tiled(h, tv[id - 1], &t, &CC, &ds, &smem, &sf, &sr);
+  if (rc != ESCOIN_OK) return rc;
+  const int64_t v[12] = {t.WM, t.WP, t.NB, t.TR, t.PR, t.PC, t.SR, t.SCs, t.plane, CC, int64_t(smem),
+                         int64_t(ds.recs.size())};
+  for (int i = 0; i < 12; ++i) out[i] = v[i];
+  return ESCOIN_OK;
+}
 
 }  // extern "C"

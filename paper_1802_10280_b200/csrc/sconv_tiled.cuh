@@ -54,7 +54,10 @@ template <int K, int S, int PH, int PW, int Q, int MINB>
 __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const TiledArgs a) {
   constexpr int P = PH * PW;
   constexpr int XH = (PH - 1) * S + K, XW = (PW - 1) * S + K;
-  constexpr bool VEC = ((PW * S) % 4) == 0;
+  // Vector (LDS.128) window loads need every lane's window to start on a
+  // 16-byte boundary: true when PW*S is a multiple of 4, or when a patch spans
+  // the whole row (PC == 1, all windows start at column 0).
+  constexpr bool VEC_ALWAYS = ((PW * S) % 4) == 0;
   constexpr int XWV = (XW + 3) / 4;
 
   extern __shared__ __align__(16) float smem[];
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
       if (h.x < 0) break;  // DONE
       const float* src = slab + win_off + (h.x - kHdrBase) * a.plane;
       float x[XH * XW];
-      if constexpr (VEC) {
+      if (VEC_ALWAYS || a.PC == 1) {
 #pragma unroll
         for (int r = 0; r < XH; ++r) {
 #pragma unroll

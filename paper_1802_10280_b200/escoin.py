@@ -30,7 +30,7 @@ EXPORTS = [
     "escoin_csr_stretch", "escoin_csr_info", "escoin_csr_host_arrays", "escoin_csr_to_device",
     "escoin_csr_wrap_device", "escoin_csr_free", "escoin_sconv_forward", "escoin_sconv_forward_hostio",
     "escoin_kernel_count", "escoin_kernel_info", "escoin_csr_set_kernel", "escoin_csr_get_kernel",
-    "escoin_status_string", "escoin_version",
+    "escoin_status_string", "escoin_version", "escoin_csr_autotune",
 ]
 
 
@@ -71,6 +71,7 @@ def lib():
             L.escoin_kernel_info.argtypes = [ci, ctypes.POINTER(ctypes.c_char_p), ip, ip]
             L.escoin_csr_set_kernel.argtypes = [vp, ci]
             L.escoin_csr_get_kernel.argtypes = [vp, ip]
+            L.escoin_csr_autotune.argtypes = [vp, ci, vp, vp, vp, ci, ci, vp, ip, ctypes.POINTER(ctypes.c_float)]
             L.escoin_status_string.argtypes = [ci]
             L.escoin_status_string.restype = ctypes.c_char_p
             L.escoin_version.restype = ctypes.c_char_p
@@ -163,6 +164,14 @@ class Csr:
         k = ctypes.c_int()
         _check("escoin_csr_get_kernel", lib().escoin_csr_get_kernel(self._h, ctypes.byref(k)))
         return k.value
+
+    def autotune(self, N, inp, out, bias=None, relu=False, reps=3, stream=0):
+        """escoin_csr_autotune: time every applicable variant on these buffers, keep the fastest."""
+        bid, bms = ctypes.c_int(), ctypes.c_float()
+        _check("escoin_csr_autotune", lib().escoin_csr_autotune(self._h, N, _ptr(inp), _ptr(out), _ptr(bias),
+                                                                1 if relu else 0, reps, stream, ctypes.byref(bid),
+                                                                ctypes.byref(bms)))
+        return bid.value, bms.value
 
     def free(self):
         if self._h.value:

@@ -275,3 +275,16 @@ def test_wrap_device_rejects_bad_csr():
     with pytest.raises(escoin.EscoinError) as e:
         escoin.Csr.wrap_device(rp.data_ptr(), ci.data_ptr(), v.data_ptr(), 2, 2, 1, 4, 4, 3, 1, 1, 0)
     assert e.value.status == escoin.ERR_CSR_MISMATCH
+
+
+def test_autotune_keeps_bits():
+    L = workloads.alexnet_full()[3]  # conv4, grouped
+    x, w, b = layer_case("alexnet", L, 0, 4)
+    ref_out, csr = run_gpu(w, x, b, 1, 1, True)
+    dx = torch.from_numpy(x).cuda()
+    db = torch.from_numpy(b).cuda()
+    out = torch.empty((4, L.M, L.E, L.F), device="cuda")
+    kid, ms = csr.autotune(4, dx, out, db, True, 2, torch.cuda.current_stream().cuda_stream)
+    assert 0 <= kid < len(escoin.kernels()) and ms > 0 and csr.kernel() == kid
+    out2, _ = run_gpu(w, x, b, 1, 1, True, csr=csr)
+    assert out2.tobytes() == ref_out.tobytes()
