@@ -175,8 +175,8 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, Tiling* b
 // Records of output-channel group g (channels g*Q .. g*Q+Q-1) bucketed by
 // input channel c, grouped into m-blocks of WM groups and channel chunks of
 // CC.  Each warp stream of one (m-block, chunk):
-//   for each c with records:  HDR(kHdrBase + c_local)  REC*  END(Q*K*K)
-//   DONE(-1)
+//   START{kHdrBase, c_first}  then for each c with records:
+//   REC*  END{Q*K*K, c_next}          (c_first / c_next = -1: no more buckets)
 // REC = {code = q*K*K + kh*K + kw, bits(value)} in ascending (q, kh, kw) —
 // i.e. the CSR order of each row.  Built once on the host from the stretched
 // CSR; never part of the bit-exact contract.
@@ -233,14 +233,18 @@ void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, DS6* 
       std::vector<int> woff(WM);
       for (int wm = 0; wm < WM; ++wm) {
         woff[wm] = int(out->recs.size()) - start;
+        // START{kHdrBase, c_first}; per bucket REC* END{END, c_next}; c = -1 ends
+        std::vector<int> cls;
         for (int cl = 0; cl < CC; ++cl) {
           const int64_t bk = first + int64_t(wm) * CC + cl;
-          if (cnt[bk + 1] == cnt[bk]) continue;
-          out->recs.push_back(make_int2(kHdrBase + cl, 0));
-          for (int64_t i = cnt[bk]; i < cnt[bk + 1]; ++i) out->recs.push_back(sorted[i]);
-          out->recs.push_back(make_int2(END, 0));
+          if (cnt[bk + 1] != cnt[bk]) cls.push_back(cl);
         }
-        out->recs.push_back(make_int2(kDone, 0));
+        out->recs.push_back(make_int2(kHdrBase, cls.empty() ? kDone : cls[0]));
+        for (size_t i = 0; i < cls.size(); ++i) {
+          const int64_t bk = first + int64_t(wm) * CC + cls[i];
+          for (int64_t r = cnt[bk]; r < cnt[bk + 1]; ++r) out->recs.push_back(sorted[r]);
+          out->recs.push_back(make_int2(END, i + 1 < cls.size() ? cls[i + 1] : kDone));
+        }
       }
       if (out->recs.size() & 1) out->recs.push_back(make_int2(kDone, 0));
       const int count = int(out->recs.size()) - start;
@@ -272,7 +276,8 @@ int plan_tiled(const escoin_csr* h, const TiledVariant& v, Tiling* t, int* CCout
     if (!choose_tiling(v, h, CC, t)) continue;  // slab too large at this CC: try a smaller chunk
     build_ds6(h, v, t->WM, CC, ds);
     const size_t stage_f = (size_t(t->NB) * CC * t->plane + 3) & ~size_t(3);
-    const size_t stage_r = std::max<size_t>((ds->max_block + 1) & ~1, 2);
+    // +2 slack records: the bucket loop prefetches one record past a warp's last END
+    const size_t stage_r = ((ds->max_block + 1) & ~1) + 2;
     *smem = 2 * stage_f * 4 + 2 * stage_r * 8;
     if (*smem <= size_t(v.min_blocks > 1 ? 110 : 220) * 1024) {
       *CCout = CC;

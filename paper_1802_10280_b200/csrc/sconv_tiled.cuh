@@ -33,8 +33,11 @@
 
 namespace escoin {
 
+// Runs the records of one bucket starting at shared address p; on return p
+// points after the bucket's END record and cl holds END's payload (the next
+// bucket's channel, or -1).
 template <int K, int S, int PH, int PW, int Q>
-__device__ void bucket_loop(float* acc, const float* x, unsigned& p);
+__device__ void bucket_loop(float* acc, const float* x, unsigned& p, int& cl);
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -139,24 +142,22 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
 #pragma unroll
   for (int i = 0; i < Q * P; ++i) acc[i] = 0.0f;
 
+  // One barrier per chunk: after it, stage ai has landed (wait_group 0 +
+  // barrier) and every warp has finished chunk ai-1, so its buffer can take
+  // chunk ai+1, which then streams in under the whole compute of chunk ai.
   if (nact > 0) stage(0, 0);
   for (int ai = 0; ai < nact; ++ai) {
     const int st = ai & 1;
-    if (ai + 1 < nact) {
-      stage(ai + 1, st ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<0>();
     __syncthreads();
-    const float* slab = st ? slab1 : slab0;
-    const int2* rbase = st ? rec1 : rec0;
-    const unsigned rbase_s = smem_addr(rbase);
-    const int2* wr = rbase + sched[ai * a.sched_stride + 3 + wm];
-    for (;;) {
-      const int2 h = *wr;
-      if (h.x < 0) break;  // DONE
-      const float* src = slab + win_off + (h.x - kHdrBase) * a.plane;
+    if (ai + 1 < nact) stage(ai + 1, st ^ 1);
+    const float* slab = (st ? slab1 : slab0) + win_off;
+    const int2* ws = (st ? rec1 : rec0) + sched[ai * a.sched_stride + 3 + wm];
+    // warp stream: START{., c_first}, then per bucket REC* END{END, c_next}; c < 0 ends
+    int cl = ws->y;
+    unsigned p = smem_addr(ws + 1);
+    while (cl >= 0) {
+      const float* src = slab + cl * a.plane;
       float x[XH * XW];
       if (VEC_ALWAYS || a.PC == 1) {
 #pragma unroll
@@ -176,11 +177,8 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
 #pragma unroll
           for (int c = 0; c < XW; ++c) x[r * XW + c] = src[r * a.SCs + c];
       }
-      unsigned p = smem_addr(wr + 1);
-      bucket_loop<K, S, PH, PW, Q>(acc, x, p);
-      wr = rbase + ((p - rbase_s) >> 3);
+      bucket_loop<K, S, PH, PW, Q>(acc, x, p, cl);
     }
-    __syncthreads();
   }
 
   // Epilogue (reading R#10): v = acc + bias[m]; ReLU; NCHW store.

@@ -1,5 +1,6 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu4.txt 2>&1
-timeout 600 python bench.py --no-baselines --no-cpu --out gpurun_out/bench_r01d.json > gpurun_out/bench_r01d.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sconv -c 4 -f -o gpurun_out/prof_r01d python bench.py --steps 1 --warmup 1 --no-baselines --no-cpu > gpurun_out/ncu_r01d.log 2>&1
+TAG=${TAG:-x}
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu_$TAG.txt 2>&1
+timeout 600 python tools/variant_sweep.py alexnet > gpurun_out/sweep_$TAG.log 2>&1
+timeout 600 python bench.py --no-baselines --no-cpu --out gpurun_out/bench_$TAG.json > gpurun_out/bench_$TAG.log 2>&1
