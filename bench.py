@@ -183,12 +183,14 @@ def time_device(torch, runs, steps, warmup, flush, step_fn):
         step_fn()
     torch.cuda.synchronize()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(runs) + 1)] for _ in range(steps)]
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" profiles only these launches
     for k in range(steps):
         flush.zero_()
         ev[k][0].record(s)
         for i, r in enumerate(runs):
             step_fn(i)
             ev[k][i + 1].record(s)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     per_layer = np.array([[ev[k][i].elapsed_time(ev[k][i + 1]) for i in range(len(runs))] for k in range(steps)])
     return per_layer  # ms [steps][layers]

@@ -186,7 +186,7 @@ struct DS6 {
   int max_block = 0;
 };
 
-void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, DS6* out) {
+void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int plane, DS6* out) {
   const int Q = v.Q, K = h->K;
   const int G = ceil_div(h->M, Q), B = ceil_div(G, WM), NK = ceil_div(h->C, CC);
   const int64_t HpWp = int64_t(h->H + 2 * h->pad) * (h->W + 2 * h->pad);
@@ -232,18 +232,48 @@ void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, DS6* 
       const int start = int(out->recs.size());
       std::vector<int> woff(WM);
       for (int wm = 0; wm < WM; ++wm) {
-        woff[wm] = int(out->recs.size()) - start;
-        // START{kHdrBase, c_first}; per bucket REC* END{END, c_next}; c = -1 ends
         std::vector<int> cls;
         for (int cl = 0; cl < CC; ++cl) {
           const int64_t bk = first + int64_t(wm) * CC + cl;
           if (cnt[bk + 1] != cnt[bk]) cls.push_back(cl);
         }
-        out->recs.push_back(make_int2(kHdrBase, cls.empty() ? kDone : cls[0]));
-        for (size_t i = 0; i < cls.size(); ++i) {
-          const int64_t bk = first + int64_t(wm) * CC + cls[i];
-          for (int64_t r = cnt[bk]; r < cnt[bk + 1]; ++r) out->recs.push_back(sorted[r]);
-          out->recs.push_back(make_int2(END, i + 1 < cls.size() ? cls[i + 1] : kDone));
+        if (v.mode == 0 || v.mode == 2) {
+          woff[wm] = int(out->recs.size()) - start;
+          // One stream per warp and chunk, run by ONE inline-PTX dispatch loop:
+          // per bucket NEXT{END, byte offset of channel c's window} REC*, then
+          // DONE{END+1}.  NEXT reloads the input window in registers.
+          for (size_t i = 0; i < cls.size(); ++i) {
+            const int64_t bk = first + int64_t(wm) * CC + cls[i];
+            out->recs.push_back(make_int2(END, cls[i] * plane * 4));
+            for (int64_t r = cnt[bk]; r < cnt[bk + 1]; ++r) out->recs.push_back(sorted[r]);
+          }
+          out->recs.push_back(make_int2(END + 1, 0));
+        } else {
+          // 16-byte units: header {c, 0, 0, 0}, then the dense Q*K*K weights of
+          // the bucket in (tap, q) order, zero-padded to a multiple of 4.
+          if (out->recs.size() & 1) out->recs.push_back(make_int2(0, 0));
+          woff[wm] = int(out->recs.size()) - start;
+          const int NS = Q * K * K, NS4 = (NS + 3) & ~3;
+          std::vector<float> dense(NS4);
+          for (size_t i = 0; i < cls.size(); ++i) {
+            const int64_t bk = first + int64_t(wm) * CC + cls[i];
+            out->recs.push_back(make_int2(cls[i], 0));
+            out->recs.push_back(make_int2(0, 0));
+            std::fill(dense.begin(), dense.end(), 0.0f);
+            for (int64_t r = cnt[bk]; r < cnt[bk + 1]; ++r) {
+              const int cd = sorted[r].x;  // (q*K + kh)*K + kw
+              const int q = cd / (K * K), tap = cd % (K * K);
+              std::memcpy(&dense[tap * Q + q], &sorted[r].y, 4);
+            }
+            for (int i2 = 0; i2 < NS4; i2 += 2) {
+              int2 pr;
+              std::memcpy(&pr.x, &dense[i2], 4);
+              std::memcpy(&pr.y, &dense[i2 + 1], 4);
+              out->recs.push_back(pr);
+            }
+          }
+          out->recs.push_back(make_int2(kDone, 0));
+          out->recs.push_back(make_int2(0, 0));
         }
       }
       if (out->recs.size() & 1) out->recs.push_back(make_int2(kDone, 0));
@@ -274,7 +304,7 @@ int plan_tiled(const escoin_csr* h, const TiledVariant& v, Tiling* t, int* CCout
                size_t* stage_f_out, size_t* stage_r_out) {
   for (int CC = 32; CC >= 1; CC /= 2) {
     if (!choose_tiling(v, h, CC, t)) continue;  // slab too large at this CC: try a smaller chunk
-    build_ds6(h, v, t->WM, CC, ds);
+    build_ds6(h, v, t->WM, CC, t->plane, ds);
     const size_t stage_f = (size_t(t->NB) * CC * t->plane + 3) & ~size_t(3);
     // +2 slack records: the bucket loop prefetches one record past a warp's last END
     const size_t stage_r = ((ds->max_block + 1) & ~1) + 2;

@@ -40,6 +40,7 @@ struct TiledVariant {
   const char* name;
   int K, S, PH, PW, Q;
   int min_blocks;  // CTAs per SM the kernel is compiled for (__launch_bounds__)
+  int mode;        // 0: per-record brx dispatch; 1: dense-bucket mask sweep
   TiledLaunchFn launch;
 };
 

@@ -16,9 +16,9 @@ FFMAs use:
 The dispatch is a warp-uniform indirect branch (PTX ``brx.idx.uni``) over
 the Q*K*K cases — NVVM lowers a C++ switch to a compare tree, so the loop is
 emitted as inline PTX.  The next record is loaded while the current one's
-FFMAs issue.  A bucket ends with an END record (code == Q*K*K) whose
-payload is the next bucket's input channel (or -1), so the warp never
-reads a separate header.
+FFMAs issue.  One loop runs a warp's whole chunk: a NEXT record (code
+Q*K*K) reloads the input window of the next channel in place, DONE
+(Q*K*K+1) leaves.
 
 Usage: gen_sconv.py OUTDIR   (writes variant_<name>.cu + variants_table.inc)
 """
@@ -31,8 +31,22 @@ import sys
 # costs ~65-170 cycles per record per warp, and once the Q*K*K cases exceed
 # ~12 KB of SASS the targets miss the instruction cache (NC=63: 13.5 TFLOP/s
 # vs NC<=36: ~23 TFLOP/s).  So keep NC = Q*K*K <= ~36.
+# mode "brx": per-record indirect dispatch; mode "mask": dense per-bucket
+# weight block swept in fixed (tap, q) order with warp-uniform forward
+# branches over the absent (zero) slots — no indirect branches at all.
+VARIANTS_MASK = [
+    ("m3s1_q4_4x4", 3, 1, 4, 4, 4),
+    ("m3s1_q8_4x4", 3, 1, 4, 4, 8),
+    ("m3s1_q6_4x4", 3, 1, 4, 4, 6),
+    ("m3s1_q4_1x13", 3, 1, 1, 13, 4),
+    ("m5s1_q2_4x4", 5, 1, 4, 4, 2),
+    ("m5s1_q4_4x4", 5, 1, 4, 4, 4),
+    ("m1s1_q12_2x4", 1, 1, 2, 4, 12),
+]
 VARIANTS = [
     ("t3s1_q4_4x4", 3, 1, 4, 4, 4),
+    ("t3s1_q1_4x4", 3, 1, 4, 4, 1),
+    ("t3s1_q2_4x4", 3, 1, 4, 4, 2),
     ("t3s1_q3_4x8", 3, 1, 4, 8, 3),
     ("t3s1_q4_1x13", 3, 1, 1, 13, 4),
     ("t3s1_q3_2x13", 3, 1, 2, 13, 3),
@@ -53,23 +67,37 @@ def min_blocks(K, S, PH, PW, Q):
     return 2 if Q * PH * PW + XH * XW <= 112 else 1
 
 
-def bucket_loop(K, S, PH, PW, Q):
+def chunk_loop(K, S, PH, PW, Q, vec):
+    """One warp's record stream for a whole channel chunk, as one dispatch loop.
+
+    Codes 0..NC-1: FFMA block of (q, kh, kw).  NC (NEXT): payload = byte
+    offset of the next channel's window; reload the XH x XW window registers
+    from shared memory (vector loads if `vec`) and continue.  NC+1: DONE.
+    """
     P = PH * PW
     XH, XW = (PH - 1) * S + K, (PW - 1) * S + K
+    XWV = (XW + 3) // 4
     NC = Q * K * K
     nacc = Q * P
-    pidx = nacc          # "+r"(p): shared address of the first record
-    cidx = nacc + 1      # "=r"(cl): END payload = next bucket's channel (or -1)
-    x0 = nacc + 2        # "f"(x[i]) window registers
+    nx = XH * XW
+    x0 = nacc                # "+f"(x[i]) window registers (reloaded in place)
+    pidx = nacc + nx         # "+r"(p)
+    bidx = pidx + 1          # "r"(wbase): shared address of the warp's window in channel 0
+    ridx = pidx + 2          # "r"(rowb): row stride in bytes
     L = ["{",
-         ".reg .b32 cd, wb, cn, wn;",
-         ".reg .f32 w;",
+         ".reg .b32 cd, wb, cn, wn, wa;",
+         ".reg .f32 w, d0, d1, d2, d3;",
          "ld.shared.v2.b32 {cd, wb}, [%%%d];" % pidx,
          "ld.shared.v2.b32 {cn, wn}, [%%%d+8];" % pidx,
          "add.u32 %%%d, %%%d, 16;" % (pidx, pidx),
          "mov.b32 w, wb;",
-         "ts: .branchtargets " + ", ".join(["L%d" % i for i in range(NC)] + ["LEND"]) + ";",
+         "ts: .branchtargets " + ", ".join(["L%d" % i for i in range(NC)] + ["LNEXT", "LEND"]) + ";",
          "brx.idx.uni cd, ts;"]
+    tail = ["mov.b32 w, wn;",
+            "mov.b32 cd, cn;",
+            "ld.shared.v2.b32 {cn, wn}, [%%%d];" % pidx,
+            "add.u32 %%%d, %%%d, 8;" % (pidx, pidx),
+            "brx.idx.uni cd, ts;"]
     for code in range(NC):
         q, kh, kw = code // (K * K), (code // K) % K, code % K
         L.append("L%d:" % code)
@@ -78,27 +106,100 @@ def bucket_loop(K, S, PH, PW, Q):
                 a = q * P + ph * PW + pw
                 xi = x0 + (ph * S + kh) * XW + (pw * S + kw)
                 L.append("fma.rn.f32 %%%d, w, %%%d, %%%d;" % (a, xi, a))
-        L += ["mov.b32 w, wn;",
-              "mov.b32 cd, cn;",
-              "ld.shared.v2.b32 {cn, wn}, [%%%d];" % pidx,
-              "add.u32 %%%d, %%%d, 8;" % (pidx, pidx),
-              "brx.idx.uni cd, ts;"]
-    L += ["LEND:", "sub.u32 %%%d, %%%d, 8;" % (pidx, pidx), "mov.b32 %%%d, w;" % cidx, "}"]
+        L += tail
+    # NEXT: reload the window of the channel whose byte offset is in w
+    L.append("LNEXT:")
+    L.append("mov.b32 wa, w;")
+    L.append("add.u32 wa, wa, %%%d;" % bidx)
+    for r in range(XH):
+        if vec:
+            for v in range(XWV):
+                regs = []
+                for j in range(4):
+                    c = 4 * v + j
+                    regs.append("%%%d" % (x0 + r * XW + c) if c < XW else "d%d" % j)
+                L.append("ld.shared.v4.f32 {%s}, [wa+%d];" % (", ".join(regs), 16 * v))
+        else:
+            for c in range(XW):
+                L.append("ld.shared.f32 %%%d, [wa+%d];" % (x0 + r * XW + c, 4 * c))
+        if r + 1 < XH:
+            L.append("add.u32 wa, wa, %%%d;" % ridx)
+    L += tail
+    L += ["LEND:", "}"]
     body = "\n".join('      "%s\\n"' % l for l in L)
-    outs = ", ".join('"+f"(acc[%d])' % i for i in range(nacc)) + ', "+r"(p), "=r"(cl)'
-    ins = ", ".join('"f"(x[%d])' % i for i in range(XH * XW))
+    outs = ", ".join('"+f"(acc[%d])' % i for i in range(nacc)) + ", " + \
+        ", ".join('"+f"(x[%d])' % i for i in range(nx)) + ', "+r"(p)'
+    ins = '"r"(wbase), "r"(rowb)'
     return body, outs, ins
 
 
-TEMPLATE = """// GENERATED by gen_sconv.py — do not edit.
-// Variant {name}: K={K} stride={S} patch {PH}x{PW} Q={Q} ({NC} dispatch cases).
+def chunk_loop2(K, S, PH, PW, Q):
+    """FFMA2 variant of chunk_loop: output pixels are processed in horizontal
+    pairs (pw, pw+1) with one fma.rn.f32x2 each; the window is held as pairs
+    (x[r][c], x[r][c+1]) for every start column c, rebuilt on NEXT."""
+    assert PW % 2 == 0 and S == 1
+    P = PH * PW
+    XH, XW = (PH - 1) * S + K, (PW - 1) * S + K
+    XWV = (XW + 3) // 4
+    NP = XW - 1                       # pair start columns per window row
+    NC = Q * K * K
+    nacc = Q * P // 2
+    nx = XH * NP
+    x0 = nacc
+    pidx = nacc + nx
+    bidx, ridx = pidx + 1, pidx + 2
+    L = ["{",
+         ".reg .b32 cd, wb, cn, wn, wa;",
+         ".reg .f32 w, " + ", ".join("t%d" % i for i in range(4 * XWV)) + ";",
+         ".reg .b64 w2;",
+         "ld.shared.v2.b32 {cd, wb}, [%%%d];" % pidx,
+         "ld.shared.v2.b32 {cn, wn}, [%%%d+8];" % pidx,
+         "add.u32 %%%d, %%%d, 16;" % (pidx, pidx),
+         "mov.b32 w, wb;",
+         "ts: .branchtargets " + ", ".join(["L%d" % i for i in range(NC)] + ["LNEXT", "LEND"]) + ";",
+         "brx.idx.uni cd, ts;"]
+    tail = ["mov.b32 w, wn;", "mov.b32 cd, cn;",
+            "ld.shared.v2.b32 {cn, wn}, [%%%d];" % pidx,
+            "add.u32 %%%d, %%%d, 8;" % (pidx, pidx),
+            "brx.idx.uni cd, ts;"]
+    for code in range(NC):
+        q, kh, kw = code // (K * K), (code // K) % K, code % K
+        L.append("L%d:" % code)
+        L.append("mov.b64 w2, {w, w};")
+        for ph in range(PH):
+            for pw in range(0, PW, 2):
+                a = q * (P // 2) + ph * (PW // 2) + pw // 2
+                xi = x0 + (ph + kh) * NP + (pw + kw)
+                L.append("fma.rn.f32x2 %%%d, w2, %%%d, %%%d;" % (a, xi, a))
+        L += tail
+    L.append("LNEXT:")
+    L.append("mov.b32 wa, w;")
+    L.append("add.u32 wa, wa, %%%d;" % bidx)
+    for r in range(XH):
+        for v in range(XWV):
+            L.append("ld.shared.v4.f32 {t%d, t%d, t%d, t%d}, [wa+%d];" % (4 * v, 4 * v + 1, 4 * v + 2, 4 * v + 3, 16 * v))
+        for c in range(NP):
+            L.append("mov.b64 %%%d, {t%d, t%d};" % (x0 + r * NP + c, c, c + 1))
+        if r + 1 < XH:
+            L.append("add.u32 wa, wa, %%%d;" % ridx)
+    L += tail
+    L += ["LEND:", "}"]
+    body = "\n".join('      "%s\\n"' % l for l in L)
+    outs = ", ".join('"+l"(acc[%d])' % i for i in range(nacc)) + ", " + \
+        ", ".join('"+l"(x[%d])' % i for i in range(nx)) + ', "+r"(p)'
+    ins = '"r"(wbase), "r"(rowb)'
+    return body, outs, ins
+
+
+TEMPLATE_F2 = """// GENERATED by gen_sconv.py — do not edit.
+// Variant {name}: K={K} stride={S} patch {PH}x{PW} Q={Q}, FFMA2 pixel pairs ({NC} dispatch cases).
 #include "sconv_tiled.cuh"
 
 namespace escoin {{
 
 template <>
-__device__ __forceinline__ void bucket_loop<{K}, {S}, {PH}, {PW}, {Q}>(float* acc, const float* x, unsigned& p,
-                                                                     int& cl) {{
+__device__ __forceinline__ void chunk_loop2<{K}, {S}, {PH}, {PW}, {Q}>(unsigned long long* acc, unsigned long long* x,
+                                                                     unsigned& p, unsigned wbase, unsigned rowb) {{
   asm volatile(
 {body}
       : {outs}
@@ -107,7 +208,103 @@ __device__ __forceinline__ void bucket_loop<{K}, {S}, {PH}, {PW}, {Q}>(float* ac
 }}
 
 int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
-  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}>(a, s);
+  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 2>(a, s);
+}}
+
+}}  // namespace escoin
+"""
+
+VARIANTS_F2 = [
+    ("f3s1_q1_4x4", 3, 1, 4, 4, 1),
+    ("f3s1_q4_4x4", 3, 1, 4, 4, 4),
+    ("f3s1_q3_4x4", 3, 1, 4, 4, 3),
+    ("f3s1_q2_4x4", 3, 1, 4, 4, 2),
+    ("f5s1_q2_4x4", 5, 1, 4, 4, 2),
+    ("f5s1_q1_4x4", 5, 1, 4, 4, 1),
+]
+
+
+def min_blocks_f2(K, S, PH, PW, Q):
+    XH, XW = (PH - 1) * S + K, (PW - 1) * S + K
+    return 2 if Q * PH * PW + 2 * XH * (XW - 1) <= 112 else 1
+
+
+def bucket_mask(K, S, PH, PW, Q):
+    """Dense-bucket sweep: weights [tap][q] (zeros = absent), slot s = tap*Q + q."""
+    P = PH * PW
+    XH, XW = (PH - 1) * S + K, (PW - 1) * S + K
+    NS = Q * K * K
+    NV = (NS + 3) // 4
+    nacc = Q * P
+    widx = nacc           # "r"(wp): shared address of the bucket's weights
+    x0 = nacc + 1
+    L = ["{", ".reg .pred p;", ".reg .f32 wa0, wa1, wa2, wa3, wb0, wb1, wb2, wb3;",
+         "ld.shared.v4.f32 {wa0, wa1, wa2, wa3}, [%%%d];" % widx]
+    for v in range(NV):
+        cur, nxt = ("wa", "wb") if v % 2 == 0 else ("wb", "wa")
+        if v + 1 < NV:
+            L.append("ld.shared.v4.f32 {%s0, %s1, %s2, %s3}, [%%%d+%d];" % (nxt, nxt, nxt, nxt, widx, 16 * (v + 1)))
+        for lane in range(4):
+            sl = 4 * v + lane
+            if sl >= NS:
+                break
+            t, q = sl // Q, sl % Q
+            kh, kw = t // K, t % K
+            L.append("setp.neu.f32 p, %s%d, 0f00000000;" % (cur, lane))
+            L.append("@!p bra.uni SK%d;" % sl)
+            for ph in range(PH):
+                for pw in range(PW):
+                    a = q * P + ph * PW + pw
+                    xi = x0 + (ph * S + kh) * XW + (pw * S + kw)
+                    L.append("fma.rn.f32 %%%d, %s%d, %%%d, %%%d;" % (a, cur, lane, xi, a))
+            L.append("SK%d:" % sl)
+    L.append("}")
+    body = "\n".join('      "%s\\n"' % l for l in L)
+    outs = ", ".join('"+f"(acc[%d])' % i for i in range(nacc))
+    ins = '"r"(wp), ' + ", ".join('"f"(x[%d])' % i for i in range(XH * XW))
+    return body, outs, ins
+
+
+TEMPLATE_MASK = """// GENERATED by gen_sconv.py — do not edit.
+// Variant {name}: K={K} stride={S} patch {PH}x{PW} Q={Q}, dense-bucket mask sweep ({NS} slots).
+#include "sconv_tiled.cuh"
+
+namespace escoin {{
+
+template <>
+__device__ __forceinline__ void bucket_mask<{K}, {S}, {PH}, {PW}, {Q}>(float* acc, const float* x, unsigned wp) {{
+  asm volatile(
+{body}
+      : {outs}
+      : {ins}
+      : "memory");
+}}
+
+int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
+  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 1>(a, s);
+}}
+
+}}  // namespace escoin
+"""
+
+TEMPLATE = """// GENERATED by gen_sconv.py — do not edit.
+// Variant {name}: K={K} stride={S} patch {PH}x{PW} Q={Q} ({NC} dispatch cases).
+#include "sconv_tiled.cuh"
+
+namespace escoin {{
+
+template <>
+__device__ __forceinline__ void chunk_loop<{K}, {S}, {PH}, {PW}, {Q}>(float* acc, float* x, unsigned& p,
+                                                                    unsigned wbase, unsigned rowb) {{
+  asm volatile(
+{body}
+      : {outs}
+      : {ins}
+      : "memory");
+}}
+
+int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
+  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 0>(a, s);
 }}
 
 }}  // namespace escoin
@@ -118,19 +315,36 @@ def main(outdir):
     os.makedirs(outdir, exist_ok=True)
     table = []
     for name, K, S, PH, PW, Q in VARIANTS:
-        body, outs, ins = bucket_loop(K, S, PH, PW, Q)
+        body, outs, ins = chunk_loop(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0)
         src = TEMPLATE.format(name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs, ins=ins,
                               MINB=min_blocks(K, S, PH, PW, Q))
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q)))
+        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 0))
+    for name, K, S, PH, PW, Q in VARIANTS_MASK:
+        body, outs, ins = bucket_mask(K, S, PH, PW, Q)
+        src = TEMPLATE_MASK.format(name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NS=Q * K * K, body=body, outs=outs,
+                                   ins=ins, MINB=min_blocks(K, S, PH, PW, Q))
+        path = os.path.join(outdir, "variant_%s.cu" % name)
+        if not os.path.exists(path) or open(path).read() != src:
+            open(path, "w").write(src)
+        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 1))
+    for name, K, S, PH, PW, Q in VARIANTS_F2:
+        body, outs, ins = chunk_loop2(K, S, PH, PW, Q)
+        mb = min_blocks_f2(K, S, PH, PW, Q)
+        src = TEMPLATE_F2.format(name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs,
+                                 ins=ins, MINB=mb)
+        path = os.path.join(outdir, "variant_%s.cu" % name)
+        if not os.path.exists(path) or open(path).read() != src:
+            open(path, "w").write(src)
+        table.append((name, K, S, PH, PW, Q, mb, 2))
     keep = set("variant_%s.cu" % t[0] for t in table)
     for f in os.listdir(outdir):
         if f.startswith("variant_") and f.endswith(".cu") and f not in keep:
             os.remove(os.path.join(outdir, f))
     decl = "\n".join("int launch_%s(const TiledArgs&, cudaStream_t);" % t[0] for t in table)
-    rows = "\n".join('  {"%s", %d, %d, %d, %d, %d, %d, &launch_%s},' % (t + (t[0],)) for t in table)
+    rows = "\n".join('  {"%s", %d, %d, %d, %d, %d, %d, %d, &launch_%s},' % (t + (t[0],)) for t in table)
     inc = "// GENERATED by gen_sconv.py — do not edit.\n%s\nstatic const TiledVariant kTiledVariants[] = {\n%s\n};\n" % (
         decl, rows)
     path = os.path.join(outdir, "variants_table.inc")

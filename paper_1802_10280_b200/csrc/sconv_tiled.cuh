@@ -33,11 +33,21 @@
 
 namespace escoin {
 
-// Runs the records of one bucket starting at shared address p; on return p
-// points after the bucket's END record and cl holds END's payload (the next
-// bucket's channel, or -1).
+// Runs a warp's whole record stream of one channel chunk (mode 0): records
+// dispatch FFMA blocks; NEXT records reload the window registers x from
+// wbase + payload (row stride rowb bytes); DONE returns.
 template <int K, int S, int PH, int PW, int Q>
-__device__ void bucket_loop(float* acc, const float* x, unsigned& p, int& cl);
+__device__ void chunk_loop(float* acc, float* x, unsigned& p, unsigned wbase, unsigned rowb);
+
+// Mode 2: same stream as mode 0, FFMA2 on horizontal output-pixel pairs.
+template <int K, int S, int PH, int PW, int Q>
+__device__ void chunk_loop2(unsigned long long* acc, unsigned long long* x, unsigned& p, unsigned wbase,
+                            unsigned rowb);
+
+// Dense-bucket sweep (mode 1): wp = shared address of the bucket's Q*K*K
+// weights in (tap, q) order, zeros for absent taps.
+template <int K, int S, int PH, int PW, int Q>
+__device__ void bucket_mask(float* acc, const float* x, unsigned wp);
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -53,7 +63,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-template <int K, int S, int PH, int PW, int Q, int MINB>
+template <int K, int S, int PH, int PW, int Q, int MINB, int MODE>
 __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const TiledArgs a) {
   constexpr int P = PH * PW;
   constexpr int XH = (PH - 1) * S + K, XW = (PW - 1) * S + K;
@@ -141,6 +151,16 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   float acc[Q * P];
 #pragma unroll
   for (int i = 0; i < Q * P; ++i) acc[i] = 0.0f;
+  float xw[MODE == 0 ? XH * XW : 1];  // mode 0: window registers, reloaded inside chunk_loop
+#pragma unroll
+  for (int i = 0; i < (MODE == 0 ? XH * XW : 1); ++i) xw[i] = 0.0f;
+  constexpr int NACC2 = MODE == 2 ? Q * P / 2 : 1;
+  constexpr int NX2 = MODE == 2 ? XH * (XW - 1) : 1;
+  unsigned long long acc2[NACC2], xw2[NX2];  // mode 2: pairs
+#pragma unroll
+  for (int i = 0; i < NACC2; ++i) acc2[i] = 0ull;
+#pragma unroll
+  for (int i = 0; i < NX2; ++i) xw2[i] = 0ull;
 
   // One barrier per chunk: after it, stage ai has landed (wait_group 0 +
   // barrier) and every warp has finished chunk ai-1, so its buffer can take
@@ -152,13 +172,8 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
     __syncthreads();
     if (ai + 1 < nact) stage(ai + 1, st ^ 1);
     const float* slab = (st ? slab1 : slab0) + win_off;
-    const int2* ws = (st ? rec1 : rec0) + sched[ai * a.sched_stride + 3 + wm];
-    // warp stream: START{., c_first}, then per bucket REC* END{END, c_next}; c < 0 ends
-    int cl = ws->y;
-    unsigned p = smem_addr(ws + 1);
-    while (cl >= 0) {
+    auto load_window = [&](float* x, int cl) {
       const float* src = slab + cl * a.plane;
-      float x[XH * XW];
       if (VEC_ALWAYS || a.PC == 1) {
 #pragma unroll
         for (int r = 0; r < XH; ++r) {
@@ -177,7 +192,35 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
 #pragma unroll
           for (int c = 0; c < XW; ++c) x[r * XW + c] = src[r * a.SCs + c];
       }
-      bucket_loop<K, S, PH, PW, Q>(acc, x, p, cl);
+    };
+    const int2* ws = (st ? rec1 : rec0) + sched[ai * a.sched_stride + 3 + wm];
+    if constexpr (MODE == 0) {
+      unsigned p = smem_addr(ws);
+      chunk_loop<K, S, PH, PW, Q>(acc, xw, p, smem_addr(slab), 4u * a.SCs);
+    } else if constexpr (MODE == 2) {
+      unsigned p = smem_addr(ws);
+      chunk_loop2<K, S, PH, PW, Q>(acc2, xw2, p, smem_addr(slab), 4u * a.SCs);
+    } else {
+      // warp stream: per bucket {c, 0, 0, 0} + Q*K*K weights (16-byte padded); c < 0 ends
+      constexpr int NW4 = (Q * K * K + 3) / 4;
+      const int4* b4 = reinterpret_cast<const int4*>(ws);
+      int cl = b4->x;
+      while (cl >= 0) {
+        float x[XH * XW];
+        load_window(x, cl);
+        const int cl_next = b4[1 + NW4].x;
+        bucket_mask<K, S, PH, PW, Q>(acc, x, smem_addr(b4 + 1));
+        b4 += 1 + NW4;
+        cl = cl_next;
+      }
+    }
+  }
+
+  if constexpr (MODE == 2) {
+#pragma unroll
+    for (int i = 0; i < Q * P / 2; ++i) {
+      acc[2 * i] = __uint_as_float(static_cast<unsigned>(acc2[i] & 0xffffffffull));
+      acc[2 * i + 1] = __uint_as_float(static_cast<unsigned>(acc2[i] >> 32));
     }
   }
 
@@ -208,9 +251,9 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   }
 }
 
-template <int K, int S, int PH, int PW, int Q, int MINB>
+template <int K, int S, int PH, int PW, int Q, int MINB, int MODE>
 int launch_tiled(const TiledArgs& a, cudaStream_t s) {
-  auto kern = sconv_tiled_kernel<K, S, PH, PW, Q, MINB>;
+  auto kern = sconv_tiled_kernel<K, S, PH, PW, Q, MINB, MODE>;
   if (a.smem_bytes > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
