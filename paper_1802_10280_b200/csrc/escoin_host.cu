@@ -2,6 +2,7 @@
 // lifetime, the kernel-side derived format (DS-6), tiling choice and the
 // forward dispatch.  No exceptions or CUDA errors cross the ABI.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -35,6 +36,12 @@ struct escoin_csr {
 namespace {
 
 constexpr int64_t kInt32Max = 2147483647LL;
+// ESCOIN_DEBUG_CODES=1|2: timing experiments only (wrong results) — collapses
+// the dispatch codes to isolate branch-target / instruction-cache effects.
+const int g_debug_code_mode = [] {
+  const char* e = std::getenv("ESCOIN_DEBUG_CODES");
+  return e ? std::atoi(e) : 0;
+}();
 
 int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
@@ -71,7 +78,7 @@ struct DeviceGuard {
 
 // ---------------------------------------------------------------- tiling
 struct Tiling {
-  int WM, WP, NB, TR, PR, PC, SR, SC, SCs, plane;
+  int WM, WP, NB, TR, PR, PC, PCs, SR, SC, SCs, plane;  // PCs >= PC: patch columns per slot row
   double cost;
 };
 
@@ -86,8 +93,9 @@ int window_conflicts(const TiledVariant& v, const Tiling& t, int CC) {
       int na = 0;
       for (int l = qtr * 8; l < qtr * 8 + 8; ++l) {
         const int slot = wp * 32 + l;
-        const int per_img = t.TR * t.PC;
-        int img = slot / per_img, pr = (slot % per_img) / t.PC, pc = slot % t.PC;
+        const int per_img = t.TR * t.PCs;
+        int img = slot / per_img, pr = (slot % per_img) / t.PCs, pc = slot % t.PCs;
+        if (pc >= t.PC) pc = t.PC - 1;  // pad lanes read their neighbour's window (broadcast)
         if (img >= t.NB) { img = 0; pr = 0; pc = 0; }
         const int a = img * CC * t.plane + pr * v.PH * v.S * t.SCs + pc * v.PW * v.S;
         bool dup = false;
@@ -111,20 +119,26 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, Tiling* b
   const int XH = (v.PH - 1) * v.S + v.K, XW = (v.PW - 1) * v.S + v.K;
   const double dens = h->nnz / (double(h->M) * h->C * h->K * h->K);
   bool found = false;
-  for (int WP = 1; WP <= 8; WP *= 2) {
+  for (int WP = 1; WP <= 8; WP *= 2)
+  for (int pcs_opt = 0; pcs_opt < 3; ++pcs_opt) {
+    // slot columns per patch row: PC, or padded to 4 / 8 so quarter-warps of
+    // window loads hit distinct 16-byte bank groups (idle lanes in the pad)
+    const int PCs = pcs_opt == 0 ? PC : pcs_opt == 1 ? ((PC + 3) & ~3) : ((PC + 7) & ~7);
+    if (pcs_opt > 0 && PCs == (pcs_opt == 1 ? PC : ((PC + 3) & ~3))) continue;  // duplicate option
     const int WM = 8 / WP;
     const int slots = 32 * WP;
-    if (PC > slots) continue;
+    if (PCs > slots) continue;
     Tiling t{};
     t.WM = WM;
     t.WP = WP;
     t.PR = PR;
     t.PC = PC;
-    if (PR * PC >= slots) {
+    t.PCs = PCs;
+    if (PR * PCs >= slots) {
       t.NB = 1;
-      t.TR = std::min(PR, slots / PC);
+      t.TR = std::min(PR, slots / PCs);
     } else {
-      t.NB = slots / (PR * PC);
+      t.NB = slots / (PR * PCs);
       t.TR = PR;
     }
     t.SR = (t.TR * v.PH - 1) * v.S + v.K;
@@ -159,10 +173,13 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, Tiling* b
     const double code_kb = NC * (P + 9) * 16.0 / 1024.0;
     const double lat = (v.min_blocks > 1 ? 40.0 : 80.0) * (code_kb > 12.0 ? code_kb / 12.0 : 1.0);
     const bool vec = ((v.PW * v.S) % 4 == 0) || PC == 1;
-    const double win = vec ? XH * ((XW + 3) / 4) * (bestc > 1 ? bestc : 1) : XH * XW;
+    const double win = vec ? XH * ((XW + 3) / 4) * 4.0 * (bestc > 1 ? bestc : 1) : XH * XW;
     const double compute = v.Q * dens * v.K * v.K * (P + 9 + lat) + win + 30;
     const double staging = 5.0 * t.NB * std::min(t.SR, h->H) * h->W / kTiledThreads;
     t.cost = (compute + staging) / (lane_util * pix_util * warp_util * v.Q * P);
+    if (std::getenv("ESCOIN_DEBUG_TILING"))
+      fprintf(stderr, "tiling %s CC=%d WP=%d PCs=%d NB=%d TR=%d SCs=%d plane=%d conflicts=%d cost=%.3f\n", v.name, CC,
+              WP, PCs, t.NB, t.TR, t.SCs, t.plane, bestc, t.cost);
     if (!found || t.cost < best->cost) {
       *best = t;
       found = true;
@@ -205,6 +222,8 @@ void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int p
       const int k = c / CC, cl = c % CC;
       key[j] = ((int64_t(b) * NK + k) * WM + wm) * CC + cl;
       code[j] = (q * K + kh) * K + kw;
+      if (g_debug_code_mode == 1) code[j] = 0;               // experiment: one branch target
+      else if (g_debug_code_mode == 2) code[j] = q * K * K;  // experiment: one target per q
       cnt[key[j] + 1]++;
     }
   }
@@ -306,7 +325,7 @@ int plan_tiled(const escoin_csr* h, const TiledVariant& v, Tiling* t, int* CCout
     if (!choose_tiling(v, h, CC, t)) continue;  // slab too large at this CC: try a smaller chunk
     build_ds6(h, v, t->WM, CC, t->plane, ds);
     const size_t stage_f = (size_t(t->NB) * CC * t->plane + 3) & ~size_t(3);
-    // +2 slack records: the bucket loop prefetches one record past a warp's last END
+    // +2 slack records: the dispatch loop prefetches up to two records past a warp's DONE
     const size_t stage_r = ((ds->max_block + 1) & ~1) + 2;
     *smem = 2 * stage_f * 4 + 2 * stage_r * 8;
     if (*smem <= size_t(v.min_blocks > 1 ? 110 : 220) * 1024) {
@@ -348,6 +367,7 @@ int prepare_tiled(escoin_csr* h, int vi, cudaStream_t s) {
   a.pad = h->pad;
   a.PR = t.PR;
   a.PC = t.PC;
+  a.PCs = t.PCs;
   a.WM = t.WM;
   a.WP = t.WP;
   a.NB = t.NB;
@@ -717,7 +737,7 @@ const char* escoin_status_string(int status) {
 const char* escoin_version(void) { return "escoin-b200 0.1 sm_100a"; }
 
 /* Internal (not in escoin.h): host-only plan of tiled variant `id` for tests.
- * out[12] = {WM, WP, NB, TR, PR, PC, SR, SCs, plane, CC, smem_bytes, records}. */
+ * out[13] = {WM, WP, NB, TR, PR, PC, SR, SCs, plane, CC, smem_bytes, records, PCs}. */
 int escoin_internal_plan(const escoin_csr* h, int id, int64_t* out) {
   int nv = 0;
   const TiledVariant* tv = tiled_variants(&nv);
@@ -729,9 +749,9 @@ int escoin_internal_plan(const escoin_csr* h, int id, int64_t* out) {
   size_t smem = 0, sf = 0, sr = 0;
   const int rc = plan_tiled(h, tv[id - 1], &t, &CC, &ds, &smem, &sf, &sr);
   if (rc != ESCOIN_OK) return rc;
-  const int64_t v[12] = {t.WM, t.WP, t.NB, t.TR, t.PR, t.PC, t.SR, t.SCs, t.plane, CC, int64_t(smem),
-                         int64_t(ds.recs.size())};
-  for (int i = 0; i < 12; ++i) out[i] = v[i];
+  const int64_t v[13] = {t.WM, t.WP, t.NB, t.TR, t.PR, t.PC, t.SR, t.SCs, t.plane, CC, int64_t(smem),
+                         int64_t(ds.recs.size()), t.PCs};
+  for (int i = 0; i < 13; ++i) out[i] = v[i];
   return ESCOIN_OK;
 }
 

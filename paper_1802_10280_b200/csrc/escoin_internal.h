@@ -20,6 +20,7 @@ struct TiledArgs {
   int relu;
   int N, C, H, W, M, E, F, pad;
   int PR, PC;           // patch grid of one image: ceil(E/PH) x ceil(F/PW)
+  int PCs;              // slot columns per patch row (>= PC; lanes with pc >= PC idle)
   int WM, WP, NB, TR;   // warps along m / along pixels; images and patch rows per CTA
   int SR, SCs, plane;   // staged slab rows, row stride (words), plane stride (words)
   int CC;               // input channels per chunk

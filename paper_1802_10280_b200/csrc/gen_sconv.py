@@ -84,18 +84,24 @@ def chunk_loop(K, S, PH, PW, Q, vec):
     pidx = nacc + nx         # "+r"(p)
     bidx = pidx + 1          # "r"(wbase): shared address of the warp's window in channel 0
     ridx = pidx + 2          # "r"(rowb): row stride in bytes
+    # Records are prefetched two ahead: the load issued in case i (record
+    # i+3) is first read by the register rotation at the end of case i+1, so
+    # shared-memory latency under load is covered by a whole case.
     L = ["{",
-         ".reg .b32 cd, wb, cn, wn, wa;",
+         ".reg .b32 cd, wb, cn, wn, cnn, wnn, wa;",
          ".reg .f32 w, d0, d1, d2, d3;",
          "ld.shared.v2.b32 {cd, wb}, [%%%d];" % pidx,
          "ld.shared.v2.b32 {cn, wn}, [%%%d+8];" % pidx,
-         "add.u32 %%%d, %%%d, 16;" % (pidx, pidx),
+         "ld.shared.v2.b32 {cnn, wnn}, [%%%d+16];" % pidx,
+         "add.u32 %%%d, %%%d, 24;" % (pidx, pidx),
          "mov.b32 w, wb;",
          "ts: .branchtargets " + ", ".join(["L%d" % i for i in range(NC)] + ["LNEXT", "LEND"]) + ";",
          "brx.idx.uni cd, ts;"]
     tail = ["mov.b32 w, wn;",
             "mov.b32 cd, cn;",
-            "ld.shared.v2.b32 {cn, wn}, [%%%d];" % pidx,
+            "mov.b32 wn, wnn;",
+            "mov.b32 cn, cnn;",
+            "ld.shared.v2.b32 {cnn, wnn}, [%%%d];" % pidx,
             "add.u32 %%%d, %%%d, 8;" % (pidx, pidx),
             "brx.idx.uni cd, ts;"]
     for code in range(NC):

@@ -86,12 +86,13 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp % a.WM, wp = warp / a.WM;
   const int slot = wp * 32 + lane;
-  const int per_img = a.TR * a.PC;
+  const int per_img = a.TR * a.PCs;
   int img = slot / per_img;
-  int pr = (slot - img * per_img) / a.PC;
-  int pc = slot - img * per_img - pr * a.PC;
-  const bool active = (img < a.NB) && (n0 + img < a.N) && (pr0 + pr < a.PR);
-  if (!active) { img = 0; pr = 0; pc = 0; }
+  int pr = (slot - img * per_img) / a.PCs;
+  int pc = slot - img * per_img - pr * a.PCs;
+  const bool active = (img < a.NB) && (n0 + img < a.N) && (pr0 + pr < a.PR) && (pc < a.PC);
+  if (pc >= a.PC) pc = a.PC - 1;  // pad lanes re-read a neighbour's window: a broadcast, not a bank conflict
+  if (!(img < a.NB) || !(n0 + img < a.N) || !(pr0 + pr < a.PR)) { img = 0; pr = 0; pc = 0; }
   const int win_off = img * a.CC * a.plane + pr * PH * S * a.SCs + pc * PW * S;
 
   // Staging map (pad_in fused, reading R#9).  Every slab cell outside the
