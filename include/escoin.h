@@ -150,7 +150,8 @@ int escoin_csr_get_kernel(const escoin_csr* csr, int* id);
 /* Measured kernel customization (§3.4 P:563-564 "the optimization space we
  * explore includes the grid shape and thread block size"): time every
  * compiled variant that accepts the handle's (K, stride) — including the
- * paper mapping — on the caller's buffers (same meaning as
+ * paper mapping — and, per variant, its best three modelled tilings (CTA
+ * shape, channel chunk), on the caller's buffers (same meaning as
  * escoin_sconv_forward; `out` is overwritten), `reps` timed forwards each
  * after one warm-up, and keep the fastest.  Synchronous on cuda_stream.
  * *best_id (may be NULL) receives the chosen variant, *best_ms its mean time.

@@ -2,6 +2,7 @@
 // lifetime, the kernel-side derived format (DS-6), tiling choice and the
 // forward dispatch.  No exceptions or CUDA errors cross the ABI.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -110,7 +111,8 @@ int window_conflicts(const TiledVariant& v, const Tiling& t, int CC) {
   return worst;
 }
 
-bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, Tiling* best) {
+// All feasible tilings of variant v at channel chunk CC, with modelled cost.
+bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vector<Tiling>* cands) {
   const double slab_budget = (v.min_blocks > 1 ? 110.0 : 220.0) * 1024 * 0.85;  // leave room for records
   const int E = h->E, F = h->F;
   const int PR = ceil_div(E, v.PH), PC = ceil_div(F, v.PW);
@@ -176,14 +178,16 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, Tiling* b
     const double win = vec ? XH * ((XW + 3) / 4) * 4.0 * (bestc > 1 ? bestc : 1) : XH * XW;
     const double compute = v.Q * dens * v.K * v.K * (P + 9 + lat) + win + 30;
     const double staging = 5.0 * t.NB * std::min(t.SR, h->H) * h->W / kTiledThreads;
-    t.cost = (compute + staging) / (lane_util * pix_util * warp_util * v.Q * P);
+    // wave quantisation of the grid at the benchmark batch (128 images)
+    const double nctas = double(ceil_div(128, t.NB)) * ceil_div(PR, t.TR) * B;
+    const double waves = nctas / (148.0 * v.min_blocks);
+    const double wave_eff = waves / std::ceil(waves);
+    t.cost = (compute + staging) / (lane_util * pix_util * warp_util * wave_eff * v.Q * P);
     if (std::getenv("ESCOIN_DEBUG_TILING"))
       fprintf(stderr, "tiling %s CC=%d WP=%d PCs=%d NB=%d TR=%d SCs=%d plane=%d conflicts=%d cost=%.3f\n", v.name, CC,
               WP, PCs, t.NB, t.TR, t.SCs, t.plane, bestc, t.cost);
-    if (!found || t.cost < best->cost) {
-      *best = t;
-      found = true;
-    }
+    cands->push_back(t);
+    found = true;
   }
   return found;
 }
@@ -319,27 +323,46 @@ int upload(const std::vector<T>& v, T** d, cudaStream_t s) {
 // Host-only planning of a tiled variant: tiling, channel chunk CC, derived
 // format and shared-memory budget.  Returns ESCOIN_ERR_UNSUPPORTED when the
 // variant cannot tile this layer.
-int plan_tiled(const escoin_csr* h, const TiledVariant& v, Tiling* t, int* CCout, DS6* ds, size_t* smem,
-               size_t* stage_f_out, size_t* stage_r_out) {
+int plan_tiled(const escoin_csr* h, const TiledVariant& v, int rank, Tiling* t, int* CCout, DS6* ds,
+               size_t* smem, size_t* stage_f_out, size_t* stage_r_out) {
+  // Candidates over every channel-chunk size, ranked by modelled cost (plus the
+  // per-chunk barrier/staging latency ~1/CC); rank 0 is the model's choice,
+  // escoin_csr_autotune also measures ranks 1..2.
+  struct Cand {
+    Tiling t;
+    int CC;
+    double cost;
+  };
+  std::vector<Cand> all;
   for (int CC = 32; CC >= 1; CC /= 2) {
-    if (!choose_tiling(v, h, CC, t)) continue;  // slab too large at this CC: try a smaller chunk
-    build_ds6(h, v, t->WM, CC, t->plane, ds);
-    const size_t stage_f = (size_t(t->NB) * CC * t->plane + 3) & ~size_t(3);
+    std::vector<Tiling> cs;
+    choose_tiling(v, h, CC, &cs);
+    for (const Tiling& tt : cs) all.push_back({tt, CC, tt.cost * (1.0 + 2.0 / CC)});
+  }
+  std::stable_sort(all.begin(), all.end(), [](const Cand& a, const Cand& b) { return a.cost < b.cost; });
+  int seen = 0;
+  for (const Cand& c : all) {
+    DS6 dd;
+    build_ds6(h, v, c.t.WM, c.CC, c.t.plane, &dd);
+    const size_t stage_f = (size_t(c.t.NB) * c.CC * c.t.plane + 3) & ~size_t(3);
     // +2 slack records: the dispatch loop prefetches up to two records past a warp's DONE
-    const size_t stage_r = ((ds->max_block + 1) & ~1) + 2;
-    *smem = 2 * stage_f * 4 + 2 * stage_r * 8;
-    if (*smem <= size_t(v.min_blocks > 1 ? 110 : 220) * 1024) {
-      *CCout = CC;
-      *stage_f_out = stage_f;
-      *stage_r_out = stage_r;
-      return ESCOIN_OK;
-    }
+    const size_t stage_r = ((dd.max_block + 1) & ~1) + 2;
+    const size_t sm = 2 * stage_f * 4 + 2 * stage_r * 8;
+    if (sm > size_t(v.min_blocks > 1 ? 110 : 220) * 1024) continue;
+    if (seen++ < rank) continue;
+    *t = c.t;
+    *CCout = c.CC;
+    *ds = std::move(dd);
+    *smem = sm;
+    *stage_f_out = stage_f;
+    *stage_r_out = stage_r;
+    return ESCOIN_OK;
   }
   return ESCOIN_ERR_UNSUPPORTED;
 }
 
 // Build + upload the derived format of tiled variant `vi` (index into the table).
-int prepare_tiled(escoin_csr* h, int vi, cudaStream_t s) {
+int prepare_tiled(escoin_csr* h, int vi, int rank, cudaStream_t s) {
   int nv = 0;
   const TiledVariant* tv = tiled_variants(&nv);
   const TiledVariant& v = tv[vi];
@@ -347,7 +370,7 @@ int prepare_tiled(escoin_csr* h, int vi, cudaStream_t s) {
   Tiling t{};
   DS6 ds;
   size_t smem = 0, stage_f = 0, stage_r = 0;
-  const int prc = plan_tiled(h, v, &t, &CC, &ds, &smem, &stage_f, &stage_r);
+  const int prc = plan_tiled(h, v, rank, &t, &CC, &ds, &smem, &stage_f, &stage_r);
   if (prc != ESCOIN_OK) return prc;
   h->targs.stage_floats = int(stage_f);
   h->targs.stage_recs = int(stage_r);
@@ -394,24 +417,25 @@ int auto_kernel(const escoin_csr* h) {
   double best_cost = 0.0;
   for (int i = 0; i < nv; ++i)
     if (tv[i].K == h->K && tv[i].S == h->stride) {
-      Tiling t{};
-      if (!choose_tiling(tv[i], h, 8, &t)) continue;
-      if (best == 0 || t.cost < best_cost) {
-        best = i + 1;
-        best_cost = t.cost;
-      }
+      std::vector<Tiling> cs;
+      if (!choose_tiling(tv[i], h, 8, &cs)) continue;
+      for (const Tiling& t : cs)
+        if (best == 0 || t.cost < best_cost) {
+          best = i + 1;
+          best_cost = t.cost;
+        }
     }
   return best;
 }
 
-int set_kernel(escoin_csr* h, int id, cudaStream_t s) {
+int set_kernel(escoin_csr* h, int id, cudaStream_t s, int rank = 0) {
   int nv = 0;
   const TiledVariant* tv = tiled_variants(&nv);
   if (id == ESCOIN_KERNEL_AUTO) id = auto_kernel(h);
   if (id < 0 || id > nv) return ESCOIN_ERR_UNSUPPORTED;
   if (id > 0 && (tv[id - 1].K != h->K || tv[id - 1].S != h->stride)) return ESCOIN_ERR_UNSUPPORTED;
   if (id > 0) {
-    const int rc = prepare_tiled(h, id - 1, s);
+    const int rc = prepare_tiled(h, id - 1, rank, s);
     if (rc != ESCOIN_OK) return rc;
   } else {
     free_ds6(h);
@@ -683,13 +707,16 @@ int escoin_csr_autotune(escoin_csr* h, int N, const float* in, float* out, const
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return ESCOIN_ERR_CUDA;
   int nv = 0;
   const TiledVariant* tv = tiled_variants(&nv);
-  int best = -1;
+  int best = -1, best_rank = 0;
   float best_t = 0.f;
   int rc = ESCOIN_OK;
-  for (int id = 0; id <= nv && rc == ESCOIN_OK; ++id) {
+  constexpr int kRanks = 3;  // tiling candidates measured per variant
+  for (int idr = 0; idr <= nv * kRanks && rc == ESCOIN_OK; ++idr) {
+    const int id = idr / kRanks, rank = idr % kRanks;
+    if (id == 0 && rank > 0) continue;
     if (id > 0 && (tv[id - 1].K != h->K || tv[id - 1].S != h->stride)) continue;
     if (cudaStreamSynchronize(s) != cudaSuccess) { rc = ESCOIN_ERR_CUDA; break; }
-    if (set_kernel(h, id, s) != ESCOIN_OK) continue;  // tiling does not fit: skip
+    if (set_kernel(h, id, s, rank) != ESCOIN_OK) continue;  // no (further) tiling fits: skip
     rc = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
     if (rc != ESCOIN_OK) break;
     cudaEventRecord(e0, s);
@@ -700,13 +727,13 @@ int escoin_csr_autotune(escoin_csr* h, int N, const float* in, float* out, const
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     ms /= reps;
-    if (best < 0 || ms < best_t) { best = id; best_t = ms; }
+    if (best < 0 || ms < best_t) { best = id; best_rank = rank; best_t = ms; }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (rc != ESCOIN_OK) return rc;
   if (best < 0) return ESCOIN_ERR_UNSUPPORTED;
-  if ((rc = set_kernel(h, best, s)) != ESCOIN_OK) return rc;
+  if ((rc = set_kernel(h, best, s, best_rank)) != ESCOIN_OK) return rc;
   if (cudaStreamSynchronize(s) != cudaSuccess) return ESCOIN_ERR_CUDA;
   if (best_id) *best_id = best;
   if (best_ms) *best_ms = best_t;
@@ -747,7 +774,7 @@ int escoin_internal_plan(const escoin_csr* h, int id, int64_t* out) {
   DS6 ds;
   int CC = 0;
   size_t smem = 0, sf = 0, sr = 0;
-  const int rc = plan_tiled(h, tv[id - 1], &t, &CC, &ds, &smem, &sf, &sr);
+  const int rc = plan_tiled(h, tv[id - 1], 0, &t, &CC, &ds, &smem, &sf, &sr);
   if (rc != ESCOIN_OK) return rc;
   const int64_t v[13] = {t.WM, t.WP, t.NB, t.TR, t.PR, t.PC, t.SR, t.SCs, t.plane, CC, int64_t(smem),
                          int64_t(ds.recs.size()), t.PCs};
