@@ -247,7 +247,7 @@ def run_reference(args):
     for L in wl.layers:
         w = inputs.layer_weights(wl.net, L, args.sparsity)
         items.append((L, oracle.csr_stretch(w, L.H, L.W, L.stride, L.pad), inputs.bias(wl.net, L.name, L.M)))
-    per_step_images = 1
+    per_step_images = 8  # a bounded sample of the batch per step (keeps all host cores busy)
     xs = {L.name: inputs.activations(wl.net, L.name, 0, per_step_images, L.C, L.H, L.W) for L, _, _ in items}
 
     def step():
