@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--out", default=None, help="also write the JSON line to this file")
+    p.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N > 1 (tests use gloo)")
+    p.add_argument("--same-device", action="store_true",
+                   help="all ranks on cuda:0 (multi-rank test of the driver on a 1-GPU box; not a measurement)")
     return p.parse_args()
 
 
@@ -287,11 +290,14 @@ def main():
     from paper_1802_10280_b200 import escoin
 
     rank, world, local = shard.world()
-    device = torch.device("cuda", local)
+    device = torch.device("cuda", 0 if args.same_device else local)
     torch.cuda.set_device(device)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=device)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(args.dist_backend)
     wl = workloads.workload(args.workload)
     runs, B = setup(args, wl, device, rank, world, torch, escoin)
     stream = torch.cuda.current_stream().cuda_stream

@@ -288,3 +288,23 @@ def test_autotune_keeps_bits():
     assert 0 <= kid < len(escoin.kernels()) and ms > 0 and csr.kernel() == kid
     out2, _ = run_gpu(w, x, b, 1, 1, True, csr=csr)
     assert out2.tobytes() == ref_out.tobytes()
+
+
+def test_bench_two_ranks_same_device():
+    # the batch-shard driver end to end with 2 ranks (gloo over CUDA tensors, both
+    # on cuda:0): CSR broadcast from rank 0, wrap_device on rank 1, max-over-ranks
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(root, "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "1", "--workload", "tiny", "--no-baselines", "--no-cpu", "--no-autotune",
+           "--dist-backend", "gloo", "--same-device"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 2 and d["value"] > 0
