@@ -98,7 +98,7 @@ int window_conflicts(const TiledVariant& v, const Tiling& t, int CC) {
         int img = slot / per_img, pr = (slot % per_img) / t.PCs, pc = slot % t.PCs;
         if (pc >= t.PC) pc = t.PC - 1;  // pad lanes read their neighbour's window (broadcast)
         if (img >= t.NB) { img = 0; pr = 0; pc = 0; }
-        const int a = img * CC * t.plane + pr * v.PH * v.S * t.SCs + pc * v.PW * v.S;
+        const int a = img * CC * t.plane + pr * v.PH * v.S * t.SCs + pc * v.PW * v.S * (v.mode == 3 ? 2 : 1);
         bool dup = false;
         for (int i = 0; i < na; ++i) dup |= (addrs[i] == a);
         if (dup) continue;
@@ -120,6 +120,7 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
   const int P = v.PH * v.PW;
   const int XH = (v.PH - 1) * v.S + v.K, XW = (v.PW - 1) * v.S + v.K;
   const double dens = h->nnz / (double(h->M) * h->C * h->K * h->K);
+  const int IP = v.mode == 3 ? 2 : 1;  // images per lane; slots and NB count image groups
   bool found = false;
   for (int WP = 1; WP <= 8; WP *= 2)
   for (int pcs_opt = 0; pcs_opt < 3; ++pcs_opt) {
@@ -144,7 +145,7 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
       t.TR = PR;
     }
     t.SR = (t.TR * v.PH - 1) * v.S + v.K;
-    t.SC = (t.PC * v.PW - 1) * v.S + v.K;
+    t.SC = ((t.PC * v.PW - 1) * v.S + v.K) * IP;  // floats per slab row (image pairs interleaved)
     const int SC4 = (t.SC + 3) & ~3;
     if (t.SR * h->W > kMaxStagePos * kTiledThreads) continue;  // interior floats per staged plane
     // pick row/plane padding that minimises LDS.128 bank-group conflicts
@@ -176,10 +177,11 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
     const double lat = (v.min_blocks > 1 ? 40.0 : 80.0) * (code_kb > 12.0 ? code_kb / 12.0 : 1.0);
     const bool vec = ((v.PW * v.S) % 4 == 0) || PC == 1;
     const double win = vec ? XH * ((XW + 3) / 4) * 4.0 * (bestc > 1 ? bestc : 1) : XH * XW;
-    const double compute = v.Q * dens * v.K * v.K * (P + 9 + lat) + win + 30;
-    const double staging = 5.0 * t.NB * std::min(t.SR, h->H) * h->W / kTiledThreads;
+    const double work = v.mode >= 2 ? P / 2.0 * IP + 10 : P + 9;  // issue slots per record
+    const double compute = (v.Q * dens * v.K * v.K * (work + lat) + win + 30) / IP;
+    const double staging = 5.0 * t.NB * IP * std::min(t.SR, h->H) * h->W / kTiledThreads / IP;
     // wave quantisation of the grid at the benchmark batch (128 images)
-    const double nctas = double(ceil_div(128, t.NB)) * ceil_div(PR, t.TR) * B;
+    const double nctas = double(ceil_div(128, t.NB * IP)) * ceil_div(PR, t.TR) * B;
     const double waves = nctas / (148.0 * v.min_blocks);
     const double wave_eff = waves / std::ceil(waves);
     t.cost = (compute + staging) / (lane_util * pix_util * warp_util * wave_eff * v.Q * P);
@@ -260,7 +262,7 @@ void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int p
           const int64_t bk = first + int64_t(wm) * CC + cl;
           if (cnt[bk + 1] != cnt[bk]) cls.push_back(cl);
         }
-        if (v.mode == 0 || v.mode == 2) {
+        if (v.mode == 0 || v.mode == 2 || v.mode == 3) {
           woff[wm] = int(out->recs.size()) - start;
           // One stream per warp and chunk, run by ONE inline-PTX dispatch loop:
           // per bucket NEXT{END, byte offset of channel c's window} REC*, then
@@ -394,6 +396,7 @@ int prepare_tiled(escoin_csr* h, int vi, int rank, cudaStream_t s) {
   a.WM = t.WM;
   a.WP = t.WP;
   a.NB = t.NB;
+  a.IP = v.mode == 3 ? 2 : 1;
   a.TR = t.TR;
   a.SR = t.SR;
   a.SCs = t.SCs;
@@ -634,7 +637,7 @@ int escoin_sconv_forward(int N, int C, int H, int W, int M, int K, int stride, i
     a.bias = bias;
     a.relu = relu ? 1 : 0;
     a.N = N;
-    a.ntiles = ceil_div(N, a.NB) * a.tiles_r;
+    a.ntiles = ceil_div(N, a.NB * a.IP) * a.tiles_r;
     if (a.ntiles > 65535) return ESCOIN_ERR_OVERFLOW;
     rc = tv[h->kernel - 1].launch(a, s);
   }

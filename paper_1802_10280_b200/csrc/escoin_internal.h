@@ -21,7 +21,8 @@ struct TiledArgs {
   int N, C, H, W, M, E, F, pad;
   int PR, PC;           // patch grid of one image: ceil(E/PH) x ceil(F/PW)
   int PCs;              // slot columns per patch row (>= PC; lanes with pc >= PC idle)
-  int WM, WP, NB, TR;   // warps along m / along pixels; images and patch rows per CTA
+  int WM, WP, NB, TR;   // warps along m / along pixels; image groups and patch rows per CTA
+  int IP;               // images per lane (image group size): 2 for mode-3 variants, else 1
   int SR, SCs, plane;   // staged slab rows, row stride (words), plane stride (words)
   int CC;               // input channels per chunk
   int tiles_r;          // ceil(PR / TR)

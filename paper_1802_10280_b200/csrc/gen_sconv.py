@@ -43,19 +43,19 @@ VARIANTS_MASK = [
     ("m5s1_q4_4x4", 5, 1, 4, 4, 4),
     ("m1s1_q12_2x4", 1, 1, 2, 4, 12),
 ]
+# "_s": one shared dispatch site (one small jump table; pays a direct branch
+# and an exposed jump-table load per record) — better when Q*K*K is large.
 VARIANTS = [
     ("t3s1_q4_4x4", 3, 1, 4, 4, 4),
-    ("t3s1_q1_4x4", 3, 1, 4, 4, 1),
+    ("t3s1_q4_4x4_s", 3, 1, 4, 4, 4),
     ("t3s1_q2_4x4", 3, 1, 4, 4, 2),
-    ("t3s1_q3_4x8", 3, 1, 4, 8, 3),
-    ("t3s1_q4_1x13", 3, 1, 1, 13, 4),
-    ("t3s1_q3_2x13", 3, 1, 2, 13, 3),
     ("t3s1_q4_2x7", 3, 1, 2, 7, 4),
-    ("t3s1_q3_2x14", 3, 1, 2, 14, 3),
-    ("t5s1_q1_4x8", 5, 1, 4, 8, 1),
+    ("t3s1_q5_4x4_s", 3, 1, 4, 4, 5),
     ("t5s1_q1_4x4", 5, 1, 4, 4, 1),
+    ("t5s1_q2_4x4_s", 5, 1, 4, 4, 2),
     ("t5s1_q2_4x4", 5, 1, 4, 4, 2),
     ("t1s1_q6_4x4", 1, 1, 4, 4, 6),
+    ("t1s1_q6_4x4_s", 1, 1, 4, 4, 6),
     ("t3s2_q4_2x4", 3, 2, 2, 4, 4),
 ]
 
@@ -67,7 +67,7 @@ def min_blocks(K, S, PH, PW, Q):
     return 2 if Q * PH * PW + XH * XW <= 112 else 1
 
 
-def chunk_loop(K, S, PH, PW, Q, vec):
+def chunk_loop(K, S, PH, PW, Q, vec, single=True):
     """One warp's record stream for a whole channel chunk, as one dispatch loop.
 
     Codes 0..NC-1: FFMA block of (q, kh, kw).  NC (NEXT): payload = byte
@@ -95,8 +95,7 @@ def chunk_loop(K, S, PH, PW, Q, vec):
          "ld.shared.v2.b32 {cnn, wnn}, [%%%d+16];" % pidx,
          "add.u32 %%%d, %%%d, 24;" % (pidx, pidx),
          "mov.b32 w, wb;",
-         "ts: .branchtargets " + ", ".join(["L%d" % i for i in range(NC)] + ["LNEXT", "LEND"]) + ";",
-         "brx.idx.uni cd, ts;"]
+         "ts: .branchtargets " + ", ".join(["L%d" % i for i in range(NC)] + ["LNEXT", "LEND"]) + ";"]
     tail = ["mov.b32 w, wn;",
             "mov.b32 cd, cn;",
             "mov.b32 wn, wnn;",
@@ -104,6 +103,16 @@ def chunk_loop(K, S, PH, PW, Q, vec):
             "ld.shared.v2.b32 {cnn, wnn}, [%%%d];" % pidx,
             "add.u32 %%%d, %%%d, 8;" % (pidx, pidx),
             "brx.idx.uni cd, ts;"]
+    # ONE dispatch site: ptxas emits a jump table per brx.idx, and 38 tables
+    # of 38 entries overflow the constant cache (indexed LDC misses stalled
+    # every record).  Cases end with a direct branch back to DISPATCH.
+    # With single=False every case ends with its own brx.idx (the jump-table
+    # LDC overlaps the case's FFMAs, but each site gets its own table).
+    if single:
+        L += ["bra.uni LFIRST;", "DISPATCH:"] + tail[:-1] + ["LFIRST:", "brx.idx.uni cd, ts;"]
+    else:
+        L.append("brx.idx.uni cd, ts;")
+    back = ["bra.uni DISPATCH;"] if single else tail
     for code in range(NC):
         q, kh, kw = code // (K * K), (code // K) % K, code % K
         L.append("L%d:" % code)
@@ -112,7 +121,7 @@ def chunk_loop(K, S, PH, PW, Q, vec):
                 a = q * P + ph * PW + pw
                 xi = x0 + (ph * S + kh) * XW + (pw * S + kw)
                 L.append("fma.rn.f32 %%%d, w, %%%d, %%%d;" % (a, xi, a))
-        L += tail
+        L += back
     # NEXT: reload the window of the channel whose byte offset is in w
     L.append("LNEXT:")
     L.append("mov.b32 wa, w;")
@@ -130,7 +139,7 @@ def chunk_loop(K, S, PH, PW, Q, vec):
                 L.append("ld.shared.f32 %%%d, [wa+%d];" % (x0 + r * XW + c, 4 * c))
         if r + 1 < XH:
             L.append("add.u32 wa, wa, %%%d;" % ridx)
-    L += tail
+    L += back
     L += ["LEND:", "}"]
     body = "\n".join('      "%s\\n"' % l for l in L)
     outs = ", ".join('"+f"(acc[%d])' % i for i in range(nacc)) + ", " + \
@@ -162,12 +171,12 @@ def chunk_loop2(K, S, PH, PW, Q):
          "ld.shared.v2.b32 {cn, wn}, [%%%d+8];" % pidx,
          "add.u32 %%%d, %%%d, 16;" % (pidx, pidx),
          "mov.b32 w, wb;",
-         "ts: .branchtargets " + ", ".join(["L%d" % i for i in range(NC)] + ["LNEXT", "LEND"]) + ";",
-         "brx.idx.uni cd, ts;"]
+         "ts: .branchtargets " + ", ".join(["L%d" % i for i in range(NC)] + ["LNEXT", "LEND"]) + ";"]
     tail = ["mov.b32 w, wn;", "mov.b32 cd, cn;",
             "ld.shared.v2.b32 {cn, wn}, [%%%d];" % pidx,
             "add.u32 %%%d, %%%d, 8;" % (pidx, pidx),
             "brx.idx.uni cd, ts;"]
+    L += ["bra.uni LFIRST;", "DISPATCH:"] + tail[:-1] + ["LFIRST:", "brx.idx.uni cd, ts;"]
     for code in range(NC):
         q, kh, kw = code // (K * K), (code // K) % K, code % K
         L.append("L%d:" % code)
@@ -177,7 +186,7 @@ def chunk_loop2(K, S, PH, PW, Q):
                 a = q * (P // 2) + ph * (PW // 2) + pw // 2
                 xi = x0 + (ph + kh) * NP + (pw + kw)
                 L.append("fma.rn.f32x2 %%%d, w2, %%%d, %%%d;" % (a, xi, a))
-        L += tail
+        L.append("bra.uni DISPATCH;")
     L.append("LNEXT:")
     L.append("mov.b32 wa, w;")
     L.append("add.u32 wa, wa, %%%d;" % bidx)
@@ -188,13 +197,106 @@ def chunk_loop2(K, S, PH, PW, Q):
             L.append("mov.b64 %%%d, {t%d, t%d};" % (x0 + r * NP + c, c, c + 1))
         if r + 1 < XH:
             L.append("add.u32 wa, wa, %%%d;" % ridx)
-    L += tail
+    L.append("bra.uni DISPATCH;")
     L += ["LEND:", "}"]
     body = "\n".join('      "%s\\n"' % l for l in L)
     outs = ", ".join('"+l"(acc[%d])' % i for i in range(nacc)) + ", " + \
         ", ".join('"+l"(x[%d])' % i for i in range(nx)) + ', "+r"(p)'
     ins = '"r"(wbase), "r"(rowb)'
     return body, outs, ins
+
+
+def chunk_loop3(K, S, PH, PW, Q):
+    """Image-pair variant: every lane holds its patch for two images; the
+    window registers are (image 2g, image 2g+1) pairs loaded straight from the
+    interleaved slab with ld.shared.v2.b64; one fma.rn.f32x2 per pixel, the
+    weight a broadcast scalar operand."""
+    assert S == 1
+    P = PH * PW
+    XH, XW = (PH - 1) * S + K, (PW - 1) * S + K
+    assert XW % 2 == 0
+    NC = Q * K * K
+    nacc = Q * P
+    nx = XH * XW
+    x0 = nacc
+    pidx = nacc + nx
+    bidx, ridx = pidx + 1, pidx + 2
+    L = ["{",
+         ".reg .b32 cd, wb, cn, wn, cnn, wnn, wa;",
+         ".reg .f32 w;",
+         ".reg .b64 w2;",
+         "ld.shared.v2.b32 {cd, wb}, [%%%d];" % pidx,
+         "ld.shared.v2.b32 {cn, wn}, [%%%d+8];" % pidx,
+         "ld.shared.v2.b32 {cnn, wnn}, [%%%d+16];" % pidx,
+         "add.u32 %%%d, %%%d, 24;" % (pidx, pidx),
+         "mov.b32 w, wb;",
+         "ts: .branchtargets " + ", ".join(["L%d" % i for i in range(NC)] + ["LNEXT", "LEND"]) + ";"]
+    tail = ["mov.b32 w, wn;", "mov.b32 cd, cn;", "mov.b32 wn, wnn;", "mov.b32 cn, cnn;",
+            "ld.shared.v2.b32 {cnn, wnn}, [%%%d];" % pidx,
+            "add.u32 %%%d, %%%d, 8;" % (pidx, pidx),
+            "brx.idx.uni cd, ts;"]
+    L += ["bra.uni LFIRST;", "DISPATCH:"] + tail[:-1] + ["LFIRST:", "brx.idx.uni cd, ts;"]
+    for code in range(NC):
+        q, kh, kw = code // (K * K), (code // K) % K, code % K
+        L.append("L%d:" % code)
+        L.append("mov.b64 w2, {w, w};")
+        for ph in range(PH):
+            for pw in range(PW):
+                a = q * P + ph * PW + pw
+                xi = x0 + (ph + kh) * XW + (pw + kw)
+                L.append("fma.rn.f32x2 %%%d, w2, %%%d, %%%d;" % (a, xi, a))
+        L.append("bra.uni DISPATCH;")
+    L.append("LNEXT:")
+    L.append("mov.b32 wa, w;")
+    L.append("add.u32 wa, wa, %%%d;" % bidx)
+    for r in range(XH):
+        for v in range(XW // 2):
+            L.append("ld.shared.v2.b64 {%%%d, %%%d}, [wa+%d];" % (x0 + r * XW + 2 * v, x0 + r * XW + 2 * v + 1, 16 * v))
+        if r + 1 < XH:
+            L.append("add.u32 wa, wa, %%%d;" % ridx)
+    L.append("bra.uni DISPATCH;")
+    L += ["LEND:", "}"]
+    body = "\n".join('      "%s\\n"' % l for l in L)
+    outs = ", ".join('"+l"(acc[%d])' % i for i in range(nacc)) + ", " + \
+        ", ".join('"+l"(x[%d])' % i for i in range(nx)) + ', "+r"(p)'
+    ins = '"r"(wbase), "r"(rowb)'
+    return body, outs, ins
+
+
+TEMPLATE_P3 = """// GENERATED by gen_sconv.py — do not edit.
+// Variant {name}: K={K} stride={S} patch {PH}x{PW} Q={Q}, image-pair FFMA2 ({NC} dispatch cases).
+#include "sconv_tiled.cuh"
+
+namespace escoin {{
+
+template <>
+__device__ __forceinline__ void chunk_loop3<{K}, {S}, {PH}, {PW}, {Q}>(unsigned long long* acc, unsigned long long* x,
+                                                                     unsigned& p, unsigned wbase, unsigned rowb) {{
+  asm volatile(
+{body}
+      : {outs}
+      : {ins}
+      : "memory");
+}}
+
+int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
+  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 3>(a, s);
+}}
+
+}}  // namespace escoin
+"""
+
+VARIANTS_P3 = [
+    ("p3s1_q4_2x4", 3, 1, 2, 4, 4),
+    ("p3s1_q3_2x4", 3, 1, 2, 4, 3),
+    ("p3s1_q2_4x4", 3, 1, 4, 4, 2),
+    ("p5s1_q1_2x4", 5, 1, 2, 4, 1),
+]
+
+
+def min_blocks_p3(K, S, PH, PW, Q):
+    XH, XW = (PH - 1) * S + K, (PW - 1) * S + K
+    return 2 if 2 * (Q * PH * PW + XH * XW) <= 112 else 1
 
 
 TEMPLATE_F2 = """// GENERATED by gen_sconv.py — do not edit.
@@ -321,7 +423,7 @@ def main(outdir):
     os.makedirs(outdir, exist_ok=True)
     table = []
     for name, K, S, PH, PW, Q in VARIANTS:
-        body, outs, ins = chunk_loop(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0)
+        body, outs, ins = chunk_loop(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0, single=name.endswith("_s"))
         src = TEMPLATE.format(name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs, ins=ins,
                               MINB=min_blocks(K, S, PH, PW, Q))
         path = os.path.join(outdir, "variant_%s.cu" % name)
@@ -345,6 +447,15 @@ def main(outdir):
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
         table.append((name, K, S, PH, PW, Q, mb, 2))
+    for name, K, S, PH, PW, Q in VARIANTS_P3:
+        body, outs, ins = chunk_loop3(K, S, PH, PW, Q)
+        mb = min_blocks_p3(K, S, PH, PW, Q)
+        src = TEMPLATE_P3.format(name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs,
+                                 ins=ins, MINB=mb)
+        path = os.path.join(outdir, "variant_%s.cu" % name)
+        if not os.path.exists(path) or open(path).read() != src:
+            open(path, "w").write(src)
+        table.append((name, K, S, PH, PW, Q, mb, 3))
     keep = set("variant_%s.cu" % t[0] for t in table)
     for f in os.listdir(outdir):
         if f.startswith("variant_") and f.endswith(".cu") and f not in keep:

@@ -39,6 +39,13 @@ namespace escoin {
 template <int K, int S, int PH, int PW, int Q>
 __device__ void chunk_loop(float* acc, float* x, unsigned& p, unsigned wbase, unsigned rowb);
 
+// Mode 3: same stream as mode 0; every lane computes its patch for TWO images
+// (an image pair interleaved in shared memory), one FFMA2 per pixel with the
+// weight as a broadcast operand — no register duplication.
+template <int K, int S, int PH, int PW, int Q>
+__device__ void chunk_loop3(unsigned long long* acc, unsigned long long* x, unsigned& p, unsigned wbase,
+                            unsigned rowb);
+
 // Mode 2: same stream as mode 0, FFMA2 on horizontal output-pixel pairs.
 template <int K, int S, int PH, int PW, int Q>
 __device__ void chunk_loop2(unsigned long long* acc, unsigned long long* x, unsigned& p, unsigned wbase,
@@ -72,6 +79,7 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   // the whole row (PC == 1, all windows start at column 0).
   constexpr bool VEC_ALWAYS = ((PW * S) % 4) == 0;
   constexpr int XWV = (XW + 3) / 4;
+  constexpr int IP = MODE == 3 ? 2 : 1;  // images per lane (interleaved innermost in smem)
 
   extern __shared__ __align__(16) float smem[];
   float* const slab0 = smem;
@@ -81,7 +89,7 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
 
   const int b = blockIdx.x;
   const int tile = blockIdx.y;
-  const int n0 = (tile / a.tiles_r) * a.NB;
+  const int n0 = (tile / a.tiles_r) * a.NB * IP;  // a.NB counts image groups of IP images
   const int pr0 = (tile % a.tiles_r) * a.TR;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp % a.WM, wp = warp / a.WM;
@@ -90,10 +98,10 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   int img = slot / per_img;
   int pr = (slot - img * per_img) / a.PCs;
   int pc = slot - img * per_img - pr * a.PCs;
-  const bool active = (img < a.NB) && (n0 + img < a.N) && (pr0 + pr < a.PR) && (pc < a.PC);
+  const bool active = (img < a.NB) && (n0 + img * IP < a.N) && (pr0 + pr < a.PR) && (pc < a.PC);
   if (pc >= a.PC) pc = a.PC - 1;  // pad lanes re-read a neighbour's window: a broadcast, not a bank conflict
-  if (!(img < a.NB) || !(n0 + img < a.N) || !(pr0 + pr < a.PR)) { img = 0; pr = 0; pc = 0; }
-  const int win_off = img * a.CC * a.plane + pr * PH * S * a.SCs + pc * PW * S;
+  if (!(img < a.NB) || !(n0 + img * IP < a.N) || !(pr0 + pr < a.PR)) { img = 0; pr = 0; pc = 0; }
+  const int win_off = img * a.CC * a.plane + pr * PH * S * a.SCs + pc * PW * S * IP;
 
   // Staging map (pad_in fused, reading R#9).  Every slab cell outside the
   // real input (padding ring, rows beyond the image) is zeroed once below and
@@ -124,13 +132,13 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
     // thread-owned interior elements ee; planes (image, channel) in the inner loop
     for (int ee = threadIdx.x; ee < nint; ee += kTiledThreads) {
       const int r = ee / a.W;
-      const unsigned so = sb + 4u * static_cast<unsigned>((r_lo + r) * a.SCs + a.pad + ee - r * a.W);
+      const unsigned so = sb + 4u * static_cast<unsigned>((r_lo + r) * a.SCs + (a.pad + ee - r * a.W) * IP);
       const float* gbase = a.in + static_cast<int64_t>(y0) * a.W + ee;
-      for (int im = 0; im < a.NB; ++im) {
+      for (int im = 0; im < a.NB * IP; ++im) {
         const int n = n0 + im;
         const int ncl = n < a.N ? min(a.CC, a.C - c0) : 0;  // valid planes; the rest are re-zeroed
         const float* g = gbase + (static_cast<int64_t>(n < a.N ? n : 0) * a.C + c0) * HW;
-        unsigned sp = so + 4u * static_cast<unsigned>(im * a.CC * a.plane);
+        unsigned sp = so + 4u * static_cast<unsigned>((im / IP) * a.CC * a.plane + (im % IP));
         int cl = 0;
 #pragma unroll 4
         for (; cl < ncl; ++cl) {
@@ -158,6 +166,13 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   constexpr int NACC2 = MODE == 2 ? Q * P / 2 : 1;
   constexpr int NX2 = MODE == 2 ? XH * (XW - 1) : 1;
   unsigned long long acc2[NACC2], xw2[NX2];  // mode 2: pairs
+  constexpr int NACC3 = MODE == 3 ? Q * P : 1;
+  constexpr int NX3 = MODE == 3 ? XH * XW : 1;
+  unsigned long long acc3[NACC3], xw3[NX3];  // mode 3: (image 2g, image 2g+1) pairs
+#pragma unroll
+  for (int i = 0; i < NACC3; ++i) acc3[i] = 0ull;
+#pragma unroll
+  for (int i = 0; i < NX3; ++i) xw3[i] = 0ull;
 #pragma unroll
   for (int i = 0; i < NACC2; ++i) acc2[i] = 0ull;
 #pragma unroll
@@ -201,6 +216,9 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
     } else if constexpr (MODE == 2) {
       unsigned p = smem_addr(ws);
       chunk_loop2<K, S, PH, PW, Q>(acc2, xw2, p, smem_addr(slab), 4u * a.SCs);
+    } else if constexpr (MODE == 3) {
+      unsigned p = smem_addr(ws);
+      chunk_loop3<K, S, PH, PW, Q>(acc3, xw3, p, smem_addr(slab), 4u * a.SCs);
     } else {
       // warp stream: per bucket {c, 0, 0, 0} + Q*K*K weights (16-byte padded); c < 0 ends
       constexpr int NW4 = (Q * K * K + 3) / 4;
@@ -227,23 +245,32 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
 
   // Epilogue (reading R#10): v = acc + bias[m]; ReLU; NCHW store.
   if (active) {
-    const int n = n0 + img;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int m = (b * a.WM + wm) * Q + q;
-      if (m < a.M) {
-        const float bv = a.bias ? __ldg(a.bias + m) : 0.0f;
-        float* o = a.out + (static_cast<int64_t>(n) * a.M + m) * a.E * a.F;
+    for (int j = 0; j < IP; ++j) {
+      const int n = n0 + img * IP + j;
+      if (n >= a.N) break;
+      if constexpr (MODE == 3) {
 #pragma unroll
-        for (int ph = 0; ph < PH; ++ph) {
-          const int oh = (pr0 + pr) * PH + ph;
+        for (int i = 0; i < Q * P; ++i)
+          acc[i] = __uint_as_float(static_cast<unsigned>(j == 0 ? (acc3[i] & 0xffffffffull) : (acc3[i] >> 32)));
+      }
 #pragma unroll
-          for (int pw = 0; pw < PW; ++pw) {
-            const int ow = pc * PW + pw;
-            if (oh < a.E && ow < a.F) {
-              float v = __fadd_rn(acc[q * P + ph * PW + pw], bv);
-              if (a.relu) v = v > 0.0f ? v : 0.0f;
-              o[oh * a.F + ow] = v;
+      for (int q = 0; q < Q; ++q) {
+        const int m = (b * a.WM + wm) * Q + q;
+        if (m < a.M) {
+          const float bv = a.bias ? __ldg(a.bias + m) : 0.0f;
+          float* o = a.out + (static_cast<int64_t>(n) * a.M + m) * a.E * a.F;
+#pragma unroll
+          for (int ph = 0; ph < PH; ++ph) {
+            const int oh = (pr0 + pr) * PH + ph;
+#pragma unroll
+            for (int pw = 0; pw < PW; ++pw) {
+              const int ow = pc * PW + pw;
+              if (oh < a.E && ow < a.F) {
+                float v = __fadd_rn(acc[q * P + ph * PW + pw], bv);
+                if (a.relu) v = v > 0.0f ? v : 0.0f;
+                o[oh * a.F + ow] = v;
+              }
             }
           }
         }
