@@ -37,6 +37,7 @@ WL_NAMES = {"alexnet": "pruned AlexNet conv2-conv5 (4 sparse CONV layers)",
             "googlenet": "pruned GoogLeNet 19 sparse 3x3/5x5 CONV layers",
             "googlenet_1x1": "pruned GoogLeNet 37 1x1 CONV layers",
             "resnet50": "pruned ResNet-50 v1 16 sparse 3x3 CONV layers",
+            "resnet50_v15": "pruned ResNet-50 v1.5 16 sparse 3x3 CONV layers (3 with stride 2)",
             "tiny": "tiny conv layer N=1 C=16 14x14 M=32 3x3"}
 METRIC = "sparse-conv images/s (whole stack) at batch 128/GPU"
 

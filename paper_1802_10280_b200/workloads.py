@@ -100,7 +100,9 @@ def googlenet_full() -> List[Layer]:
 
 
 # ------------------------------------------------------------------ ResNet-50 v1
-def resnet50_full() -> List[Layer]:
+def resnet50_full(v15: bool = False) -> List[Layer]:
+    """ResNet-50 v1 (Caffe; stride on the first 1x1) or, with v15=True, v1.5
+    (stride on the 3x3 of each downsampling block; NEXT-3 stride-2 workload)."""
     L = [Layer("conv1", 3, 224, 224, 64, 7, 2, 3)]
     stages = [("res2", 3, 64, 256, 56, 1), ("res3", 4, 128, 512, 28, 2),
               ("res4", 6, 256, 1024, 14, 2), ("res5", 3, 512, 2048, 7, 2)]
@@ -112,8 +114,12 @@ def resnet50_full() -> List[Layer]:
             isz = size if b == 0 else osize
             if b == 0:
                 L.append(Layer(bn + "_branch1", cin, isz, isz, out, 1, s, 0))
-            L.append(Layer(bn + "_branch2a", cin if b == 0 else out, isz, isz, mid, 1, s, 0))
-            L.append(Layer(bn + "_branch2b", mid, osize, osize, mid, 3, 1, 1, sparse=True))
+            if v15:  # 1x1 at the input size, stride-2 3x3 (isz -> osize)
+                L.append(Layer(bn + "_branch2a", cin if b == 0 else out, isz, isz, mid, 1, 1, 0))
+                L.append(Layer(bn + "_branch2b", mid, isz, isz, mid, 3, s, 1, sparse=True))
+            else:
+                L.append(Layer(bn + "_branch2a", cin if b == 0 else out, isz, isz, mid, 1, s, 0))
+                L.append(Layer(bn + "_branch2b", mid, osize, osize, mid, 3, 1, 1, sparse=True))
             L.append(Layer(bn + "_branch2c", mid, osize, osize, out, 1, 1, 0))
         cin, size = out, osize
     L.append(_fc("fc1000", 2048, 1000))
@@ -150,6 +156,8 @@ def workload(name: str) -> Workload:
                         [l for l in googlenet_full() if l.kind == "conv" and l.K == 1])
     if name == "resnet50":
         return Workload("resnet50", "resnet50", [l for l in resnet50_full() if l.sparse])
+    if name == "resnet50_v15":  # NEXT-3: three of the 16 sparse 3x3 layers have stride 2
+        return Workload("resnet50_v15", "resnet50_v15", [l for l in resnet50_full(v15=True) if l.sparse])
     raise KeyError(name)
 
 

@@ -368,3 +368,12 @@ def test_table3_reproduced(ex):
         assert abs(macs - ex["macs_M"]) / ex["macs_M"] < 0.015
     if ex["net"] == "alexnet":
         assert round(macs) == 724 and round(weights) == 61
+
+
+def test_resnet50_v15_macs():
+    # v1.5 moves the stride to the 3x3: 4.09G MACs (SURVEY reading R#16), same weights
+    full = workloads.resnet50_full(v15=True)
+    assert abs(sum(l.macs for l in full) / 1e9 - 4.09) < 0.02
+    assert sum(l.weights for l in full) == sum(l.weights for l in workloads.resnet50_full())
+    sparse = [l for l in full if l.sparse]
+    assert len(sparse) == 16 and sum(l.stride == 2 for l in sparse) == 3

@@ -186,7 +186,7 @@ def layer_case(wl, L, n0, n):
     return x, w, b
 
 
-@pytest.mark.parametrize("wl", ["alexnet", "resnet50", "googlenet"])
+@pytest.mark.parametrize("wl", ["alexnet", "resnet50", "googlenet", "resnet50_v15"])
 def test_config_layers_small_batch(wl):
     # every sparse layer of the config, all outputs of N=2 images, default kernel
     for L in workloads.workload(wl).layers:
