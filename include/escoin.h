@@ -66,6 +66,16 @@ typedef struct escoin_csr escoin_csr;
 int escoin_csr_stretch(const float* w, int M, int C, int H, int W, int K, int stride, int pad,
                        escoin_csr** out);
 
+/* Same stretch computed ON THE DEVICE (NEXT-4): d_w is a device pointer to
+ * the dense pruned weights [M][C][K][K] fp32 (caller-owned, read-only, not
+ * retained).  Count / scan / order-preserving compaction kernels on
+ * cuda_stream; the result is bit-identical to escoin_csr_stretch.  The handle
+ * owns the device CSR, also keeps host copies (one D2H), and is returned
+ * already on `device` (derived format built).  Synchronous.
+ * Errors: NULL, SHAPE, OVERFLOW, ALLOC, CUDA. */
+int escoin_csr_stretch_device(const float* d_w, int M, int C, int H, int W, int K, int stride, int pad,
+                              int device, void* cuda_stream, escoin_csr** out);
+
 /* Shape and nnz recorded in the handle (any output pointer may be NULL). */
 int escoin_csr_info(const escoin_csr* csr, int* M, int* C, int* H, int* W, int* K, int* stride,
                     int* pad, int64_t* nnz);

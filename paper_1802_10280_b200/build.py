@@ -1,4 +1,4 @@
-"""Build libescoin.so (method) and libescoin_baselines.so (bench-only baselines).
+"""Build libescoin.so (the method's C-ABI library).
 
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo; IEEE fp32 (no
 --use_fast_math, no FTZ: reading R#22).  cudart is linked statically so the
@@ -21,7 +21,6 @@ GEN = os.path.join(CSRC, "generated")
 OBJ = os.path.join(ROOT, "build", "obj")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libescoin.so")
-BASELIB = os.path.join(PKG, "libescoin_baselines.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -64,15 +63,13 @@ def build(jobs: int | None = None, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         glob.glob(os.path.join(INCLUDE, "*.h")) + [os.path.join(GEN, "variants_table.inc")]
-    core = [os.path.join(CSRC, "escoin_host.cu"), os.path.join(CSRC, "sconv_paper.cu")]
-    base = [os.path.join(CSRC, "baselines.cu")]
-    srcs = core + variants + [s for s in base if os.path.exists(s)]
+    core = [os.path.join(CSRC, "escoin_host.cu"), os.path.join(CSRC, "sconv_paper.cu"),
+            os.path.join(CSRC, "stretch_device.cu")]
+    srcs = core + variants
     jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 4))
     with ThreadPoolExecutor(jobs) as ex:
         objs = dict(zip(srcs, ex.map(lambda s: _compile(s, headers), srcs)))
     _link(LIB, [objs[s] for s in core + variants], [])
-    if all(os.path.exists(s) for s in base):
-        _link(BASELIB, [objs[s] for s in base], ["-L/usr/local/cuda/lib64", "-lcublas", "-lcusparse"])
     if verbose:
         for s in srcs:
             log = os.path.join(OBJ, os.path.basename(s) + ".o.log")

@@ -52,8 +52,6 @@ int out_dim(int H, int K, int stride, int pad) {
   return span < 0 ? -1 : span / stride + 1;
 }
 
-int cuda_status(cudaError_t e) { return e == cudaSuccess ? ESCOIN_OK : ESCOIN_ERR_CUDA; }
-
 void free_ds6(escoin_csr* h) {
   if (h->d_recs) cudaFree(h->d_recs);
   if (h->d_sched) cudaFree(h->d_sched);
@@ -507,6 +505,66 @@ int escoin_csr_stretch(const float* w, int M, int C, int H, int W, int K, int st
   return ESCOIN_OK;
 }
 
+int escoin_csr_stretch_device(const float* d_w, int M, int C, int H, int W, int K, int stride, int pad, int device,
+                              void* cuda_stream, escoin_csr** out) {
+  if (!d_w || !out) return ESCOIN_ERR_NULL;
+  *out = nullptr;
+  int E, F;
+  int rc = validate_shape(M, C, H, W, K, stride, pad, &E, &F);
+  if (rc != ESCOIN_OK) return rc;
+  DeviceGuard g(device);
+  if (!g.ok) return ESCOIN_ERR_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  escoin_csr* h = new (std::nothrow) escoin_csr();
+  if (!h) return ESCOIN_ERR_ALLOC;
+  h->M = M; h->C = C; h->H = H; h->W = W; h->K = K; h->stride = stride; h->pad = pad; h->E = E; h->F = F;
+  h->device = device;
+  const int64_t crs = int64_t(C) * K * K;
+  int* cnt = nullptr;
+  auto fail = [&](int code) {
+    if (cnt) cudaFree(cnt);
+    escoin_csr_free(h);
+    return code;
+  };
+  if (cudaMalloc(&cnt, sizeof(int) * M) != cudaSuccess) return fail(ESCOIN_ERR_ALLOC);
+  if (cudaMalloc(&h->d_rowptr, sizeof(int32_t) * (size_t(M) + 1)) != cudaSuccess) return fail(ESCOIN_ERR_ALLOC);
+  if (launch_stretch_count(d_w, M, crs, cnt, s) != 0) return fail(ESCOIN_ERR_CUDA);
+  if (launch_stretch_scan(cnt, M, h->d_rowptr, s) != 0) return fail(ESCOIN_ERR_CUDA);
+  try {
+    h->rowptr.resize(size_t(M) + 1);
+  } catch (...) {
+    return fail(ESCOIN_ERR_ALLOC);
+  }
+  if (cudaMemcpyAsync(h->rowptr.data(), h->d_rowptr, 4 * (size_t(M) + 1), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return fail(ESCOIN_ERR_CUDA);
+  const int64_t nnz = h->rowptr[M];
+  if (nnz > kInt32Max) return fail(ESCOIN_ERR_OVERFLOW);
+  h->nnz = nnz;
+  const size_t nb = std::max<size_t>(4 * size_t(nnz), 16);
+  if (cudaMalloc(&h->d_colidx, nb) != cudaSuccess || cudaMalloc(&h->d_value, nb) != cudaSuccess)
+    return fail(ESCOIN_ERR_ALLOC);
+  if (launch_stretch_compact(d_w, M, crs, K, H + 2 * pad, W + 2 * pad, h->d_rowptr, h->d_colidx, h->d_value, s) != 0)
+    return fail(ESCOIN_ERR_CUDA);
+  try {
+    h->colidx.resize(size_t(nnz));
+    h->value.resize(size_t(nnz));
+  } catch (...) {
+    return fail(ESCOIN_ERR_ALLOC);
+  }
+  if (nnz > 0 && (cudaMemcpyAsync(h->colidx.data(), h->d_colidx, 4 * size_t(nnz), cudaMemcpyDeviceToHost, s) !=
+                      cudaSuccess ||
+                  cudaMemcpyAsync(h->value.data(), h->d_value, 4 * size_t(nnz), cudaMemcpyDeviceToHost, s) !=
+                      cudaSuccess))
+    return fail(ESCOIN_ERR_CUDA);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return fail(ESCOIN_ERR_CUDA);
+  cudaFree(cnt);
+  cnt = nullptr;
+  if ((rc = escoin_csr_to_device(h, device, cuda_stream)) != ESCOIN_OK) return fail(rc);
+  *out = h;
+  return ESCOIN_OK;
+}
+
 int escoin_csr_info(const escoin_csr* h, int* M, int* C, int* H, int* W, int* K, int* stride, int* pad,
                     int64_t* nnz) {
   if (!h) return ESCOIN_ERR_NULL;
@@ -537,7 +595,7 @@ int escoin_csr_to_device(escoin_csr* h, int device, void* cuda_stream) {
   if (!g.ok) return ESCOIN_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
   int rc;
-  if (!h->borrowed) {
+  if (!h->borrowed && !h->d_rowptr) {  // (device-stretched handles already own their device CSR)
     if ((rc = upload(h->rowptr, &h->d_rowptr, s)) != ESCOIN_OK) return rc;
     if ((rc = upload(h->colidx, &h->d_colidx, s)) != ESCOIN_OK) return rc;
     if ((rc = upload(h->value, &h->d_value, s)) != ESCOIN_OK) return rc;

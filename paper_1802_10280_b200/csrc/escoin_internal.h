@@ -53,4 +53,10 @@ int launch_paper(const int* rowptr, const int* colidx, const float* value, const
 
 const TiledVariant* tiled_variants(int* count);
 
+// Device weight stretching (stretch_device.cu).
+int launch_stretch_count(const float* w, int M, int64_t crs, int* cnt, cudaStream_t s);
+int launch_stretch_scan(const int* cnt, int M, int32_t* rowptr, cudaStream_t s);
+int launch_stretch_compact(const float* w, int M, int64_t crs, int K, int Hp, int Wp, const int32_t* rowptr,
+                           int32_t* colidx, float* value, cudaStream_t s);
+
 }  // namespace escoin

@@ -30,7 +30,7 @@ EXPORTS = [
     "escoin_csr_stretch", "escoin_csr_info", "escoin_csr_host_arrays", "escoin_csr_to_device",
     "escoin_csr_wrap_device", "escoin_csr_free", "escoin_sconv_forward", "escoin_sconv_forward_hostio",
     "escoin_kernel_count", "escoin_kernel_info", "escoin_csr_set_kernel", "escoin_csr_get_kernel",
-    "escoin_status_string", "escoin_version", "escoin_csr_autotune",
+    "escoin_status_string", "escoin_version", "escoin_csr_autotune", "escoin_csr_stretch_device",
 ]
 
 
@@ -59,6 +59,7 @@ def lib():
             pp = ctypes.POINTER(ctypes.c_void_p)
             ip = ctypes.POINTER(ctypes.c_int)
             L.escoin_csr_stretch.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, pp]
+            L.escoin_csr_stretch_device.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, vp, pp]
             L.escoin_csr_info.argtypes = [vp, ip, ip, ip, ip, ip, ip, ip, ctypes.POINTER(cl)]
             L.escoin_csr_host_arrays.argtypes = [vp, pp, pp, pp]
             L.escoin_csr_to_device.argtypes = [vp, ci, vp]
@@ -117,6 +118,14 @@ class Csr:
         h = ctypes.c_void_p()
         _check("escoin_csr_stretch", lib().escoin_csr_stretch(w.ctypes.data, M, C, H, W, K, stride, pad,
                                                               ctypes.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def stretch_device(cls, d_w, M, C, H, W, K, stride, pad, device=0, stream=0) -> "Csr":
+        """escoin_csr_stretch_device on dense pruned weights already on the GPU (pointer or torch tensor)."""
+        h = ctypes.c_void_p()
+        _check("escoin_csr_stretch_device", lib().escoin_csr_stretch_device(
+            _ptr(d_w), M, C, H, W, K, stride, pad, device, stream, ctypes.byref(h)))
         return cls(h.value)
 
     @classmethod

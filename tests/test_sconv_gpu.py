@@ -308,3 +308,34 @@ def test_bench_two_ranks_same_device():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 2 and d["value"] > 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_stretch_device_bit_exact(seed):
+    # NEXT-4: the device stretch equals the host stretch bit for bit (and the oracle's)
+    rng = np.random.default_rng(seed)
+    K = int(rng.choice([1, 3, 5]))
+    M, C, H, W, pad = int(rng.integers(1, 300)), int(rng.integers(1, 40)), 13, 11, K // 2
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) < 0.8] = 0.0
+    w[rng.random(w.shape) < 0.05] = -0.0
+    w.reshape(-1)[:3] = np.float32(1e-42)  # denormals are nonzero
+    d = escoin.Csr.stretch_device(torch.from_numpy(w).cuda(), M, C, H, W, K, 1, pad, 0)
+    h = escoin.Csr.stretch(w, H, W, 1, pad)
+    for a, b in zip(d.host_arrays(), h.host_arrays()):
+        assert a.tobytes() == b.tobytes()
+    orp, oci, ov = oracle.csr_stretch(w, H, W, 1, pad)
+    assert d.host_arrays()[1].tobytes() == oci.tobytes()
+    x = rng.random((2, C, H, W)).astype(np.float32)
+    o1, _ = run_gpu(w, x, None, 1, pad, False, csr=d)
+    o2, _ = run_gpu(w, x, None, 1, pad, False, csr=h.to_device(0))
+    assert o1.tobytes() == o2.tobytes()
+
+
+def test_stretch_device_config_layer():
+    L = workloads.alexnet_full()[3]
+    w = inputs.layer_weights("alexnet", L, 800)
+    d = escoin.Csr.stretch_device(torch.from_numpy(w).cuda(), L.M, L.C, L.H, L.W, L.K, 1, 1, 0)
+    rp, ci, v = oracle.csr_stretch(w, L.H, L.W, 1, 1)
+    a = d.host_arrays()
+    assert a[0].tobytes() == rp.tobytes() and a[1].tobytes() == ci.tobytes() and a[2].tobytes() == v.tobytes()
