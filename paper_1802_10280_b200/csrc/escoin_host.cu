@@ -39,6 +39,10 @@ namespace {
 constexpr int64_t kInt32Max = 2147483647LL;
 // ESCOIN_DEBUG_CODES=1|2: timing experiments only (wrong results) — collapses
 // the dispatch codes to isolate branch-target / instruction-cache effects.
+const int g_debug_kernel = [] {
+  const char* e = std::getenv("ESCOIN_DEBUG_KERNEL");
+  return e ? std::atoi(e) : 0;
+}();
 const int g_debug_code_mode = [] {
   const char* e = std::getenv("ESCOIN_DEBUG_CODES");
   return e ? std::atoi(e) : 0;
@@ -78,6 +82,7 @@ struct DeviceGuard {
 // ---------------------------------------------------------------- tiling
 struct Tiling {
   int WM, WP, NB, TR, PR, PC, PCs, SR, SC, SCs, plane;  // PCs >= PC: patch columns per slot row
+  int flat;                                              // full-row variants: slots over (image, row)
   double cost;
 };
 
@@ -94,6 +99,7 @@ int window_conflicts(const TiledVariant& v, const Tiling& t, int CC) {
         const int slot = wp * 32 + l;
         const int per_img = t.TR * t.PCs;
         int img = slot / per_img, pr = (slot % per_img) / t.PCs, pc = slot % t.PCs;
+        if (t.flat) { img = slot / t.PR; pr = slot % t.PR; pc = 0; }
         if (pc >= t.PC) pc = t.PC - 1;  // pad lanes read their neighbour's window (broadcast)
         if (img >= t.NB) { img = 0; pr = 0; pc = 0; }
         const int a = img * CC * t.plane + pr * v.PH * v.S * t.SCs + pc * v.PW * v.S * (v.mode == 3 ? 2 : 1);
@@ -120,8 +126,10 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
   const double dens = h->nnz / (double(h->M) * h->C * h->K * h->K);
   const int IP = v.mode == 3 ? 2 : 1;  // images per lane; slots and NB count image groups
   bool found = false;
+  if (v.full_row && PC != 1) return false;  // full-row variants need the patch to span the output row
   for (int WP = 1; WP <= 8; WP *= 2)
   for (int pcs_opt = 0; pcs_opt < 3; ++pcs_opt) {
+    if (v.full_row && pcs_opt > 0) continue;
     // slot columns per patch row: PC, or padded to 4 / 8 so quarter-warps of
     // window loads hit distinct 16-byte bank groups (idle lanes in the pad)
     const int PCs = pcs_opt == 0 ? PC : pcs_opt == 1 ? ((PC + 3) & ~3) : ((PC + 7) & ~7);
@@ -135,7 +143,11 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
     t.PR = PR;
     t.PC = PC;
     t.PCs = PCs;
-    if (PR * PCs >= slots) {
+    if (v.full_row) {  // flat (image, row) slots: stage every image a 32*WP-row range can touch
+      t.flat = 1;
+      t.TR = PR;
+      t.NB = ceil_div(slots, PR) + 1;
+    } else if (PR * PCs >= slots) {
       t.NB = 1;
       t.TR = std::min(PR, slots / PCs);
     } else {
@@ -163,7 +175,7 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
       }
     }
     if (2.0 * 4.0 * t.NB * CC * t.plane > slab_budget) continue;  // double-buffered slab must fit
-    const double lane_util = double(t.NB * t.TR * t.PC) / slots;
+    const double lane_util = t.flat ? 1.0 : double(t.NB * t.TR * t.PC) / slots;
     const double pix_util = double(E) * F / (double(PR * v.PH) * (PC * v.PW));
     const int B = ceil_div(G, WM);
     const double warp_util = double(G) / (B * WM);
@@ -179,7 +191,8 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
     const double compute = (v.Q * dens * v.K * v.K * (work + lat) + win + 30) / IP;
     const double staging = 5.0 * t.NB * IP * std::min(t.SR, h->H) * h->W / kTiledThreads / IP;
     // wave quantisation of the grid at the benchmark batch (128 images)
-    const double nctas = double(ceil_div(128, t.NB * IP)) * ceil_div(PR, t.TR) * B;
+    const double nctas = t.flat ? double(ceil_div(128 * PR, slots)) * B
+                                : double(ceil_div(128, t.NB * IP)) * ceil_div(PR, t.TR) * B;
     const double waves = nctas / (148.0 * v.min_blocks);
     const double wave_eff = waves / std::ceil(waves);
     t.cost = (compute + staging) / (lane_util * pix_util * warp_util * wave_eff * v.Q * P);
@@ -395,6 +408,7 @@ int prepare_tiled(escoin_csr* h, int vi, int rank, cudaStream_t s) {
   a.WP = t.WP;
   a.NB = t.NB;
   a.IP = v.mode == 3 ? 2 : 1;
+  a.flat = t.flat;
   a.TR = t.TR;
   a.SR = t.SR;
   a.SCs = t.SCs;
@@ -695,7 +709,8 @@ int escoin_sconv_forward(int N, int C, int H, int W, int M, int K, int stride, i
     a.bias = bias;
     a.relu = relu ? 1 : 0;
     a.N = N;
-    a.ntiles = ceil_div(N, a.NB * a.IP) * a.tiles_r;
+    a.ntiles = a.flat ? ceil_div(N * a.PR, a.WP * 32) : ceil_div(N, a.NB * a.IP) * a.tiles_r;
+    a.debug = g_debug_kernel;
     if (a.ntiles > 65535) return ESCOIN_ERR_OVERFLOW;
     rc = tv[h->kernel - 1].launch(a, s);
   }

@@ -23,6 +23,8 @@ struct TiledArgs {
   int PCs;              // slot columns per patch row (>= PC; lanes with pc >= PC idle)
   int WM, WP, NB, TR;   // warps along m / along pixels; image groups and patch rows per CTA
   int IP;               // images per lane (image group size): 2 for mode-3 variants, else 1
+  int flat;             // 1: full-row patches (PC == 1) over a flat (image, patch-row) index, so one
+                        // warp's 32 rows may span images (no idle lanes for PR not dividing 32)
   int SR, SCs, plane;   // staged slab rows, row stride (words), plane stride (words)
   int CC;               // input channels per chunk
   int tiles_r;          // ceil(PR / TR)
@@ -34,6 +36,7 @@ struct TiledArgs {
   const int* sched;     // per active chunk: [k, rec_start, rec_count, woff[WM]]
   const int* sched_off; // [B+1] first entry of each m-block
   int sched_stride;     // 3 + WM
+  int debug;            // timing experiments only (ESCOIN_DEBUG_KERNEL): 1 skip staging, 2 skip barrier, 4 skip stores
 };
 
 typedef int (*TiledLaunchFn)(const TiledArgs&, cudaStream_t);
@@ -42,7 +45,8 @@ struct TiledVariant {
   const char* name;
   int K, S, PH, PW, Q;
   int min_blocks;  // CTAs per SM the kernel is compiled for (__launch_bounds__)
-  int mode;        // 0: per-record brx dispatch; 1: dense-bucket mask sweep
+  int mode;        // 0: per-record brx dispatch; 1: dense-bucket mask sweep; 2/3: FFMA2
+  int full_row;    // patch spans the whole output row (PC must be 1): vector window loads, flat tiling
   TiledLaunchFn launch;
 };
 

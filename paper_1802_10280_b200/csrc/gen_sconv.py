@@ -49,7 +49,10 @@ VARIANTS = [
     ("t3s1_q4_4x4", 3, 1, 4, 4, 4),
     ("t3s1_q4_4x4_s", 3, 1, 4, 4, 4),
     ("t3s1_q2_4x4", 3, 1, 4, 4, 2),
+    ("t3s1_q3_4x4", 3, 1, 4, 4, 3),
+    ("t3s1_q3_4x4_s", 3, 1, 4, 4, 3),
     ("t3s1_q4_2x7", 3, 1, 2, 7, 4),
+    ("t3s1_q4_1x13_r", 3, 1, 1, 13, 4),
     ("t3s1_q5_4x4_s", 3, 1, 4, 4, 5),
     ("t5s1_q1_4x4", 5, 1, 4, 4, 1),
     ("t5s1_q2_4x4_s", 5, 1, 4, 4, 2),
@@ -423,13 +426,14 @@ def main(outdir):
     os.makedirs(outdir, exist_ok=True)
     table = []
     for name, K, S, PH, PW, Q in VARIANTS:
-        body, outs, ins = chunk_loop(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0, single=name.endswith("_s"))
+        full_row = name.endswith("_r")
+        body, outs, ins = chunk_loop(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0 or full_row, single=name.endswith("_s"))
         src = TEMPLATE.format(name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs, ins=ins,
                               MINB=min_blocks(K, S, PH, PW, Q))
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 0))
+        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 0, 1 if full_row else 0))
     for name, K, S, PH, PW, Q in VARIANTS_MASK:
         body, outs, ins = bucket_mask(K, S, PH, PW, Q)
         src = TEMPLATE_MASK.format(name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NS=Q * K * K, body=body, outs=outs,
@@ -437,7 +441,7 @@ def main(outdir):
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 1))
+        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 1, 0))
     for name, K, S, PH, PW, Q in VARIANTS_F2:
         body, outs, ins = chunk_loop2(K, S, PH, PW, Q)
         mb = min_blocks_f2(K, S, PH, PW, Q)
@@ -446,7 +450,7 @@ def main(outdir):
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, mb, 2))
+        table.append((name, K, S, PH, PW, Q, mb, 2, 0))
     for name, K, S, PH, PW, Q in VARIANTS_P3:
         body, outs, ins = chunk_loop3(K, S, PH, PW, Q)
         mb = min_blocks_p3(K, S, PH, PW, Q)
@@ -455,13 +459,13 @@ def main(outdir):
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, mb, 3))
+        table.append((name, K, S, PH, PW, Q, mb, 3, 0))
     keep = set("variant_%s.cu" % t[0] for t in table)
     for f in os.listdir(outdir):
         if f.startswith("variant_") and f.endswith(".cu") and f not in keep:
             os.remove(os.path.join(outdir, f))
     decl = "\n".join("int launch_%s(const TiledArgs&, cudaStream_t);" % t[0] for t in table)
-    rows = "\n".join('  {"%s", %d, %d, %d, %d, %d, %d, %d, &launch_%s},' % (t + (t[0],)) for t in table)
+    rows = "\n".join('  {"%s", %d, %d, %d, %d, %d, %d, %d, %d, &launch_%s},' % (t + (t[0],)) for t in table)
     inc = "// GENERATED by gen_sconv.py — do not edit.\n%s\nstatic const TiledVariant kTiledVariants[] = {\n%s\n};\n" % (
         decl, rows)
     path = os.path.join(outdir, "variants_table.inc")

@@ -89,15 +89,26 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
 
   const int b = blockIdx.x;
   const int tile = blockIdx.y;
-  const int n0 = (tile / a.tiles_r) * a.NB * IP;  // a.NB counts image groups of IP images
-  const int pr0 = (tile % a.tiles_r) * a.TR;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp % a.WM, wp = warp / a.WM;
   const int slot = wp * 32 + lane;
-  const int per_img = a.TR * a.PCs;
-  int img = slot / per_img;
-  int pr = (slot - img * per_img) / a.PCs;
-  int pc = slot - img * per_img - pr * a.PCs;
+  int n0, pr0, img, pr, pc;
+  if (a.flat) {
+    // flat: slots enumerate (image, patch-row) pairs; this CTA owns 32*WP of them
+    const int g0 = tile * a.WP * 32, g = g0 + slot;
+    n0 = g0 / a.PR;
+    pr0 = 0;
+    img = g / a.PR - n0;
+    pr = g - (g / a.PR) * a.PR;
+    pc = 0;
+  } else {
+    n0 = (tile / a.tiles_r) * a.NB * IP;  // a.NB counts image groups of IP images
+    pr0 = (tile % a.tiles_r) * a.TR;
+    const int per_img = a.TR * a.PCs;
+    img = slot / per_img;
+    pr = (slot - img * per_img) / a.PCs;
+    pc = slot - img * per_img - pr * a.PCs;
+  }
   const bool active = (img < a.NB) && (n0 + img * IP < a.N) && (pr0 + pr < a.PR) && (pc < a.PC);
   if (pc >= a.PC) pc = a.PC - 1;  // pad lanes re-read a neighbour's window: a broadcast, not a bank conflict
   if (!(img < a.NB) || !(n0 + img * IP < a.N) || !(pr0 + pr < a.PR)) { img = 0; pr = 0; pc = 0; }
@@ -185,8 +196,17 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   for (int ai = 0; ai < nact; ++ai) {
     const int st = ai & 1;
     cp_async_wait<0>();
-    __syncthreads();
-    if (ai + 1 < nact) stage(ai + 1, st ^ 1);
+    if (!(a.debug & 2)) __syncthreads();
+    if (ai + 1 < nact) {
+      if (a.debug & 1) {  // timing experiment: records only, input slab left stale
+        const int* e = sched + (ai + 1) * a.sched_stride;
+        const unsigned rb = smem_addr(st ? rec0 : rec1);
+        for (int i = threadIdx.x; i < (e[2] >> 1); i += kTiledThreads) cp_async16(rb + 16u * i, a.recs + e[1] + 2 * i);
+        cp_async_commit();
+      } else {
+        stage(ai + 1, st ^ 1);
+      }
+    }
     const float* slab = (st ? slab1 : slab0) + win_off;
     auto load_window = [&](float* x, int cl) {
       const float* src = slab + cl * a.plane;
@@ -244,7 +264,7 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   }
 
   // Epilogue (reading R#10): v = acc + bias[m]; ReLU; NCHW store.
-  if (active) {
+  if (active && !(a.debug & 4 && acc[0] != 12345.0f)) {
 #pragma unroll
     for (int j = 0; j < IP; ++j) {
       const int n = n0 + img * IP + j;

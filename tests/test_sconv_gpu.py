@@ -25,12 +25,19 @@ def kernel_ids(K, S):
 
 
 def run_gpu(w, x, bias, stride, pad, relu, kernel=escoin.KERNEL_AUTO, csr=None):
+    """Forward through the C-ABI; returns (None, None) when the requested variant
+    cannot tile this shape (ESCOIN_ERR_UNSUPPORTED is a legitimate answer)."""
     M, C, K, _ = w.shape
     N, _, H, W = x.shape
     if csr is None:
         csr = escoin.Csr.stretch(w, H, W, stride, pad)
         csr.set_kernel(kernel)
-        csr.to_device(0)
+        try:
+            csr.to_device(0)
+        except escoin.EscoinError as e:
+            if e.status == escoin.ERR_UNSUPPORTED and kernel != escoin.KERNEL_AUTO:
+                return None, None
+            raise
     dx = torch.from_numpy(np.ascontiguousarray(x)).cuda()
     db = None if bias is None else torch.from_numpy(bias).cuda()
     out = escoin.forward(csr, dx, bias=db, relu=relu)
@@ -66,8 +73,11 @@ def test_tiny_all_kernels(relu, with_bias):
     outs = []
     for k in kernel_ids(L.K, L.stride):
         out, _ = run_gpu(w, x, b, L.stride, L.pad, relu, kernel=k)
+        if out is None:
+            continue
         check(out, ref, scale, b)
         outs.append(out)
+    assert len(outs) >= 2  # the paper mapping and at least one tiled variant
     for o in outs[1:]:  # every variant accumulates in the same order -> identical bits
         assert o.tobytes() == outs[0].tobytes()
 
@@ -95,6 +105,8 @@ def test_parity_grid(case):
     outs = []
     for k in kernel_ids(K, s):
         out, _ = run_gpu(w, x, b, s, p, True, kernel=k)
+        if out is None:
+            continue
         check(out, ref, scale, b)
         outs.append(out)
     for o in outs[1:]:
@@ -114,6 +126,8 @@ def test_exact_integer_regime(case):
     assert np.max(scale) < 2 ** 24
     for k in kernel_ids(K, s):
         out, _ = run_gpu(w, x, b, s, p, False, kernel=k)
+        if out is None:
+            continue
         assert np.array_equal(out.astype(np.float64), ref), "kernel %d not bit-exact" % k
 
 
@@ -133,6 +147,8 @@ def test_one_hot_is_shifted_copy(K, pad):
     E, F = H + 2 * pad - K + 1, W + 2 * pad - K + 1
     for k in kernel_ids(K, 1):
         out, _ = run_gpu(w, x, None, 1, pad, False, kernel=k)
+        if out is None:
+            continue
         for m, (c, kh, kw) in enumerate(taps):
             assert np.array_equal(out[:, m], xp[:, c, kh:kh + E, kw:kw + F]), (k, m)
 
@@ -144,6 +160,8 @@ def test_all_zero_weights_give_bias():
     b = (rng.random(20) - 0.5).astype(np.float32)
     for k in kernel_ids(3, 1):
         out, _ = run_gpu(w, x, b, 1, 1, False, kernel=k)
+        if out is None:
+            continue
         assert np.array_equal(out, np.broadcast_to(b[None, :, None, None], out.shape))
         outr, _ = run_gpu(w, x, b, 1, 1, True, kernel=k)
         assert np.array_equal(outr, np.maximum(out, 0))
@@ -159,6 +177,8 @@ def test_empty_rows_and_ragged_m():
     ref, scale = oracle_ref(w, x, b, 1, 1, False)
     for k in kernel_ids(3, 1):
         out, _ = run_gpu(w, x, b, 1, 1, False, kernel=k)
+        if out is None:
+            continue
         check(out, ref, scale, b)
         assert np.array_equal(out[:, [0, 5, 6, 22]], np.broadcast_to(b[None, [0, 5, 6, 22], None, None],
                                                                     out[:, [0, 5, 6, 22]].shape))
