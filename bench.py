@@ -328,11 +328,17 @@ def main():
     layer_ms = per_layer.mean(0)
 
     # ---------------- e2e through the C-ABI with host buffers
+    # Every step copies each layer's input from pinned host memory, runs the
+    # layer and copies its output back (escoin_sconv_forward_hostio).  Layers
+    # run on their own streams so one layer's H2D overlaps another's compute
+    # and D2H (PCIe is full duplex); each stream serialises its own buffers.
+    e2e_streams = [torch.cuda.Stream(device) for _ in runs]
+
     def e2e_step():
-        for r in runs:
+        for r, st in zip(runs, e2e_streams):
             L = r.L
             escoin.sconv_forward_hostio(B, L.C, L.H, L.W, L.M, L.K, L.stride, L.pad, r.csr, r.h_x, r.h_out, r.x,
-                                        r.out, r.bias, True, stream)
+                                        r.out, r.bias, True, st.cuda_stream)
 
     e2e_steps = max(3, min(args.steps, 20))
     for _ in range(2):
@@ -342,8 +348,12 @@ def main():
         torch.distributed.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    for st in e2e_streams:
+        st.wait_event(e0)
     for _ in range(e2e_steps):
         e2e_step()
+    for st in e2e_streams:
+        torch.cuda.current_stream().wait_stream(st)
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = shard.max_over_ranks(e0.elapsed_time(e1) / e2e_steps, device)
