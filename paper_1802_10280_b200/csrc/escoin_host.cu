@@ -273,7 +273,7 @@ void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int p
           const int64_t bk = first + int64_t(wm) * CC + cl;
           if (cnt[bk + 1] != cnt[bk]) cls.push_back(cl);
         }
-        if (v.mode == 0 || v.mode == 2 || v.mode == 3) {
+        if ((v.mode == 0 || v.mode == 2 || v.mode == 3) && v.rel_d == 0) {
           woff[wm] = int(out->recs.size()) - start;
           // One stream per warp and chunk, run by ONE inline-PTX dispatch loop:
           // per bucket NEXT{END, byte offset of channel c's window} REC*, then
@@ -284,6 +284,30 @@ void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int p
             for (int64_t r = cnt[bk]; r < cnt[bk + 1]; ++r) out->recs.push_back(sorted[r]);
           }
           out->recs.push_back(make_int2(END + 1, 0));
+        } else if (v.rel_d > 0) {
+          // Same stream, 16-byte records {idx, payload, abs, 0}: idx indexes the
+          // predecessor's jump list (full list after START/NEXT; after case c
+          // the D codes following c, then NEXT, DONE, FAR).
+          woff[wm] = int(out->recs.size()) - start;
+          const int D = v.rel_d;
+          int prev = -1;  // -1: START or NEXT (full list)
+          auto emit = [&](int abs, int payload) {
+            int idx;
+            if (prev < 0) idx = abs;
+            else if (abs == END) idx = D;
+            else if (abs == END + 1) idx = D + 1;
+            else if (abs - prev - 1 >= 0 && abs - prev - 1 < D) idx = abs - prev - 1;
+            else idx = D + 2;  // FAR
+            out->recs.push_back(make_int2(idx, payload));
+            out->recs.push_back(make_int2(abs, 0));
+            prev = (abs >= END) ? -1 : abs;
+          };
+          for (size_t i = 0; i < cls.size(); ++i) {
+            const int64_t bk = first + int64_t(wm) * CC + cls[i];
+            emit(END, cls[i] * plane * 4);
+            for (int64_t r = cnt[bk]; r < cnt[bk + 1]; ++r) emit(sorted[r].x, sorted[r].y);
+          }
+          emit(END + 1, 0);
         } else {
           // 16-byte units: header {c, 0, 0, 0}, then the dense Q*K*K weights of
           // the bucket in (tap, q) order, zero-padded to a multiple of 4.
@@ -358,8 +382,9 @@ int plan_tiled(const escoin_csr* h, const TiledVariant& v, int rank, Tiling* t, 
     DS6 dd;
     build_ds6(h, v, c.t.WM, c.CC, c.t.plane, &dd);
     const size_t stage_f = (size_t(c.t.NB) * c.CC * c.t.plane + 3) & ~size_t(3);
-    // +2 slack records: the dispatch loop prefetches up to two records past a warp's DONE
-    const size_t stage_r = ((dd.max_block + 1) & ~1) + 2;
+    // slack: the dispatch loop prefetches up to two records (16 B each for
+    // rel_d variants) past a warp's DONE
+    const size_t stage_r = ((dd.max_block + 1) & ~1) + 4;
     const size_t sm = 2 * stage_f * 4 + 2 * stage_r * 8;
     if (sm > size_t(v.min_blocks > 1 ? 110 : 220) * 1024) continue;
     if (seen++ < rank) continue;

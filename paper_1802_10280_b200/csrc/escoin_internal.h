@@ -47,6 +47,7 @@ struct TiledVariant {
   int min_blocks;  // CTAs per SM the kernel is compiled for (__launch_bounds__)
   int mode;        // 0: per-record brx dispatch; 1: dense-bucket mask sweep; 2/3: FFMA2
   int full_row;    // patch spans the whole output row (PC must be 1): vector window loads, flat tiling
+  int rel_d;       // > 0: 16-byte records with predecessor-relative dispatch indices (chunk_loop_rel)
   TiledLaunchFn launch;
 };
 

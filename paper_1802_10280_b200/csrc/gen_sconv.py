@@ -24,6 +24,7 @@ Usage: gen_sconv.py OUTDIR   (writes variant_<name>.cu + variants_table.inc)
 """
 import os
 import sys
+import zlib
 
 # name, K, S, PH, PW, Q   (Q*PH*PW accumulators; ptxas wants acc <= ~112 regs
 # so accumulators and window registers can sit in opposite register banks)
@@ -34,6 +35,8 @@ import sys
 # mode "brx": per-record indirect dispatch; mode "mask": dense per-bucket
 # weight block swept in fixed (tap, q) order with warp-uniform forward
 # branches over the absent (zero) slots — no indirect branches at all.
+REL_D = 12  # "_x" variants: successor window of the per-case jump tables
+
 VARIANTS_MASK = [
     ("m3s1_q4_4x4", 3, 1, 4, 4, 4),
     ("m3s1_q8_4x4", 3, 1, 4, 4, 8),
@@ -48,6 +51,9 @@ VARIANTS_MASK = [
 VARIANTS = [
     ("t3s1_q4_4x4", 3, 1, 4, 4, 4),
     ("t3s1_q4_4x4_s", 3, 1, 4, 4, 4),
+    ("t3s1_q4_4x4_x", 3, 1, 4, 4, 4),
+    ("t3s1_q5_4x4_x", 3, 1, 4, 4, 5),
+    ("t3s1_q3_4x4_x", 3, 1, 4, 4, 3),
     ("t3s1_q2_4x4", 3, 1, 4, 4, 2),
     ("t3s1_q3_4x4", 3, 1, 4, 4, 3),
     ("t3s1_q3_4x4_s", 3, 1, 4, 4, 3),
@@ -56,6 +62,8 @@ VARIANTS = [
     ("t3s1_q5_4x4_s", 3, 1, 4, 4, 5),
     ("t5s1_q1_4x4", 5, 1, 4, 4, 1),
     ("t5s1_q2_4x4_s", 5, 1, 4, 4, 2),
+    ("t5s1_q2_4x4_x", 5, 1, 4, 4, 2),
+    ("t5s1_q1_4x4_x", 5, 1, 4, 4, 1),
     ("t5s1_q2_4x4", 5, 1, 4, 4, 2),
     ("t1s1_q6_4x4", 1, 1, 4, 4, 6),
     ("t1s1_q6_4x4_s", 1, 1, 4, 4, 6),
@@ -209,6 +217,79 @@ def chunk_loop2(K, S, PH, PW, Q):
     return body, outs, ins
 
 
+def chunk_loop_rel(K, S, PH, PW, Q, vec, D):
+    """chunk_loop with SMALL per-site jump tables.
+
+    ptxas emits one jump table per brx.idx site; with a site per case the
+    tables (NC+2)^2 entries overflow the constant cache and every record's
+    indexed LDC misses (measured: the top stall).  Here records are 16 bytes
+    {idx, payload, abs, 0}: idx indexes the PREDECESSOR's site list.  Case c's
+    list holds only the D codes after c (records of a bucket are sorted by
+    code) plus NEXT, DONE and FAR; FAR re-reads the record's absolute code and
+    dispatches through the one full list (the prologue / NEXT site's).
+    """
+    P = PH * PW
+    XH, XW = (PH - 1) * S + K, (PW - 1) * S + K
+    XWV = (XW + 3) // 4
+    NC = Q * K * K
+    nacc = Q * P
+    nx = XH * XW
+    x0 = nacc
+    pidx = nacc + nx
+    bidx, ridx = pidx + 1, pidx + 2
+    full = ", ".join(["L%d" % i for i in range(NC)] + ["LNEXT", "LEND"])
+    L = ["{",
+         ".reg .b32 cd, wb, cn, wn, cnn, wnn, wa, ab;",
+         ".reg .f32 w, d0, d1, d2, d3;",
+         "ld.shared.v2.b32 {cd, wb}, [%%%d];" % pidx,
+         "ld.shared.v2.b32 {cn, wn}, [%%%d+16];" % pidx,
+         "ld.shared.v2.b32 {cnn, wnn}, [%%%d+32];" % pidx,
+         "add.u32 %%%d, %%%d, 48;" % (pidx, pidx),
+         "mov.b32 w, wb;",
+         "tfull: .branchtargets " + full + ";",
+         "brx.idx.uni cd, tfull;"]
+
+    def tail(site):
+        return ["mov.b32 w, wn;", "mov.b32 cd, cn;", "mov.b32 wn, wnn;", "mov.b32 cn, cnn;",
+                "ld.shared.v2.b32 {cnn, wnn}, [%%%d];" % pidx,
+                "add.u32 %%%d, %%%d, 16;" % (pidx, pidx),
+                "brx.idx.uni cd, %s;" % site]
+
+    for code in range(NC):
+        q, kh, kw = code // (K * K), (code // K) % K, code % K
+        L.append("L%d:" % code)
+        for ph in range(PH):
+            for pw in range(PW):
+                a = q * P + ph * PW + pw
+                xi = x0 + (ph * S + kh) * XW + (pw * S + kw)
+                L.append("fma.rn.f32 %%%d, w, %%%d, %%%d;" % (a, xi, a))
+        succ = ["L%d" % (code + 1 + i) if code + 1 + i < NC else "LFAR" for i in range(D)]
+        L.append("t%d: .branchtargets %s;" % (code, ", ".join(succ + ["LNEXT", "LEND", "LFAR"])))
+        L += tail("t%d" % code)
+    L.append("LNEXT:")
+    L.append("mov.b32 wa, w;")
+    L.append("add.u32 wa, wa, %%%d;" % bidx)
+    for r in range(XH):
+        if vec:
+            for v in range(XWV):
+                regs = ["%%%d" % (x0 + r * XW + 4 * v + j) if 4 * v + j < XW else "d%d" % j for j in range(4)]
+                L.append("ld.shared.v4.f32 {%s}, [wa+%d];" % (", ".join(regs), 16 * v))
+        else:
+            for c in range(XW):
+                L.append("ld.shared.f32 %%%d, [wa+%d];" % (x0 + r * XW + c, 4 * c))
+        if r + 1 < XH:
+            L.append("add.u32 wa, wa, %%%d;" % ridx)
+    L += tail("tfull")
+    # FAR: the record being dispatched sits 3 records behind p; its abs field
+    L += ["LFAR:", "ld.shared.b32 ab, [%%%d+-40];" % pidx, "brx.idx.uni ab, tfull;"]
+    L += ["LEND:", "}"]
+    body = "\n".join('      "%s\\n"' % l for l in L)
+    outs = ", ".join('"+f"(acc[%d])' % i for i in range(nacc)) + ", " + \
+        ", ".join('"+f"(x[%d])' % i for i in range(nx)) + ', "+r"(p)'
+    ins = '"r"(wbase), "r"(rowb)'
+    return body, outs, ins
+
+
 def chunk_loop3(K, S, PH, PW, Q):
     """Image-pair variant: every lane holds its patch for two images; the
     window registers are (image 2g, image 2g+1) pairs loaded straight from the
@@ -273,7 +354,7 @@ TEMPLATE_P3 = """// GENERATED by gen_sconv.py — do not edit.
 namespace escoin {{
 
 template <>
-__device__ __forceinline__ void chunk_loop3<{K}, {S}, {PH}, {PW}, {Q}>(unsigned long long* acc, unsigned long long* x,
+__device__ __forceinline__ void chunk_loop3<{K}, {S}, {PH}, {PW}, {Q}, {TAG}>(unsigned long long* acc, unsigned long long* x,
                                                                      unsigned& p, unsigned wbase, unsigned rowb) {{
   asm volatile(
 {body}
@@ -283,7 +364,7 @@ __device__ __forceinline__ void chunk_loop3<{K}, {S}, {PH}, {PW}, {Q}>(unsigned 
 }}
 
 int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
-  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 3>(a, s);
+  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 3, {TAG}>(a, s);
 }}
 
 }}  // namespace escoin
@@ -309,7 +390,7 @@ TEMPLATE_F2 = """// GENERATED by gen_sconv.py — do not edit.
 namespace escoin {{
 
 template <>
-__device__ __forceinline__ void chunk_loop2<{K}, {S}, {PH}, {PW}, {Q}>(unsigned long long* acc, unsigned long long* x,
+__device__ __forceinline__ void chunk_loop2<{K}, {S}, {PH}, {PW}, {Q}, {TAG}>(unsigned long long* acc, unsigned long long* x,
                                                                      unsigned& p, unsigned wbase, unsigned rowb) {{
   asm volatile(
 {body}
@@ -319,7 +400,7 @@ __device__ __forceinline__ void chunk_loop2<{K}, {S}, {PH}, {PW}, {Q}>(unsigned 
 }}
 
 int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
-  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 2>(a, s);
+  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 2, {TAG}>(a, s);
 }}
 
 }}  // namespace escoin
@@ -383,7 +464,7 @@ TEMPLATE_MASK = """// GENERATED by gen_sconv.py — do not edit.
 namespace escoin {{
 
 template <>
-__device__ __forceinline__ void bucket_mask<{K}, {S}, {PH}, {PW}, {Q}>(float* acc, const float* x, unsigned wp) {{
+__device__ __forceinline__ void bucket_mask<{K}, {S}, {PH}, {PW}, {Q}, {TAG}>(float* acc, const float* x, unsigned wp) {{
   asm volatile(
 {body}
       : {outs}
@@ -392,7 +473,7 @@ __device__ __forceinline__ void bucket_mask<{K}, {S}, {PH}, {PW}, {Q}>(float* ac
 }}
 
 int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
-  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 1>(a, s);
+  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 1, {TAG}>(a, s);
 }}
 
 }}  // namespace escoin
@@ -405,7 +486,7 @@ TEMPLATE = """// GENERATED by gen_sconv.py — do not edit.
 namespace escoin {{
 
 template <>
-__device__ __forceinline__ void chunk_loop<{K}, {S}, {PH}, {PW}, {Q}>(float* acc, float* x, unsigned& p,
+__device__ __forceinline__ void chunk_loop<{K}, {S}, {PH}, {PW}, {Q}, {TAG}>(float* acc, float* x, unsigned& p,
                                                                     unsigned wbase, unsigned rowb) {{
   asm volatile(
 {body}
@@ -415,7 +496,7 @@ __device__ __forceinline__ void chunk_loop<{K}, {S}, {PH}, {PW}, {Q}>(float* acc
 }}
 
 int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
-  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 0>(a, s);
+  return launch_tiled<{K}, {S}, {PH}, {PW}, {Q}, {MINB}, 0, {TAG}>(a, s);
 }}
 
 }}  // namespace escoin
@@ -427,45 +508,51 @@ def main(outdir):
     table = []
     for name, K, S, PH, PW, Q in VARIANTS:
         full_row = name.endswith("_r")
-        body, outs, ins = chunk_loop(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0 or full_row, single=name.endswith("_s"))
-        src = TEMPLATE.format(name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs, ins=ins,
+        rel = name.endswith("_x")
+        if rel:
+            body, outs, ins = chunk_loop_rel(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0, D=REL_D)
+        else:
+            body, outs, ins = chunk_loop(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0 or full_row,
+                                         single=name.endswith("_s"))
+        src = TEMPLATE.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs, ins=ins,
                               MINB=min_blocks(K, S, PH, PW, Q))
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 0, 1 if full_row else 0))
+        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 0, 1 if full_row else 0,
+                      REL_D if rel else 0))
     for name, K, S, PH, PW, Q in VARIANTS_MASK:
         body, outs, ins = bucket_mask(K, S, PH, PW, Q)
-        src = TEMPLATE_MASK.format(name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NS=Q * K * K, body=body, outs=outs,
+        src = TEMPLATE_MASK.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NS=Q * K * K, body=body, outs=outs,
                                    ins=ins, MINB=min_blocks(K, S, PH, PW, Q))
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 1, 0))
+        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 1, 0, 0))
     for name, K, S, PH, PW, Q in VARIANTS_F2:
         body, outs, ins = chunk_loop2(K, S, PH, PW, Q)
         mb = min_blocks_f2(K, S, PH, PW, Q)
-        src = TEMPLATE_F2.format(name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs,
+        src = TEMPLATE_F2.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs,
                                  ins=ins, MINB=mb)
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, mb, 2, 0))
+        table.append((name, K, S, PH, PW, Q, mb, 2, 0, 0))
     for name, K, S, PH, PW, Q in VARIANTS_P3:
         body, outs, ins = chunk_loop3(K, S, PH, PW, Q)
         mb = min_blocks_p3(K, S, PH, PW, Q)
-        src = TEMPLATE_P3.format(name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs,
+        src = TEMPLATE_P3.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs,
                                  ins=ins, MINB=mb)
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, mb, 3, 0))
+        table.append((name, K, S, PH, PW, Q, mb, 3, 0, 0))
     keep = set("variant_%s.cu" % t[0] for t in table)
     for f in os.listdir(outdir):
         if f.startswith("variant_") and f.endswith(".cu") and f not in keep:
             os.remove(os.path.join(outdir, f))
     decl = "\n".join("int launch_%s(const TiledArgs&, cudaStream_t);" % t[0] for t in table)
-    rows = "\n".join('  {"%s", %d, %d, %d, %d, %d, %d, %d, %d, &launch_%s},' % (t + (t[0],)) for t in table)
+    rows = "\n".join('  {"%s", %d, %d, %d, %d, %d, %d, %d, %d, %d, &launch_%s},' % (t + (t[0],)) for t in table)
     inc = "// GENERATED by gen_sconv.py — do not edit.\n%s\nstatic const TiledVariant kTiledVariants[] = {\n%s\n};\n" % (
         decl, rows)
     path = os.path.join(outdir, "variants_table.inc")

@@ -36,24 +36,24 @@ namespace escoin {
 // Runs a warp's whole record stream of one channel chunk (mode 0): records
 // dispatch FFMA blocks; NEXT records reload the window registers x from
 // wbase + payload (row stride rowb bytes); DONE returns.
-template <int K, int S, int PH, int PW, int Q>
+template <int K, int S, int PH, int PW, int Q, int TAG>
 __device__ void chunk_loop(float* acc, float* x, unsigned& p, unsigned wbase, unsigned rowb);
 
 // Mode 3: same stream as mode 0; every lane computes its patch for TWO images
 // (an image pair interleaved in shared memory), one FFMA2 per pixel with the
 // weight as a broadcast operand — no register duplication.
-template <int K, int S, int PH, int PW, int Q>
+template <int K, int S, int PH, int PW, int Q, int TAG>
 __device__ void chunk_loop3(unsigned long long* acc, unsigned long long* x, unsigned& p, unsigned wbase,
                             unsigned rowb);
 
 // Mode 2: same stream as mode 0, FFMA2 on horizontal output-pixel pairs.
-template <int K, int S, int PH, int PW, int Q>
+template <int K, int S, int PH, int PW, int Q, int TAG>
 __device__ void chunk_loop2(unsigned long long* acc, unsigned long long* x, unsigned& p, unsigned wbase,
                             unsigned rowb);
 
 // Dense-bucket sweep (mode 1): wp = shared address of the bucket's Q*K*K
 // weights in (tap, q) order, zeros for absent taps.
-template <int K, int S, int PH, int PW, int Q>
+template <int K, int S, int PH, int PW, int Q, int TAG>
 __device__ void bucket_mask(float* acc, const float* x, unsigned wp);
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
@@ -70,7 +70,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-template <int K, int S, int PH, int PW, int Q, int MINB, int MODE>
+template <int K, int S, int PH, int PW, int Q, int MINB, int MODE, int TAG>
 __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const TiledArgs a) {
   constexpr int P = PH * PW;
   constexpr int XH = (PH - 1) * S + K, XW = (PW - 1) * S + K;
@@ -232,13 +232,13 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
     const int2* ws = (st ? rec1 : rec0) + sched[ai * a.sched_stride + 3 + wm];
     if constexpr (MODE == 0) {
       unsigned p = smem_addr(ws);
-      chunk_loop<K, S, PH, PW, Q>(acc, xw, p, smem_addr(slab), 4u * a.SCs);
+      chunk_loop<K, S, PH, PW, Q, TAG>(acc, xw, p, smem_addr(slab), 4u * a.SCs);
     } else if constexpr (MODE == 2) {
       unsigned p = smem_addr(ws);
-      chunk_loop2<K, S, PH, PW, Q>(acc2, xw2, p, smem_addr(slab), 4u * a.SCs);
+      chunk_loop2<K, S, PH, PW, Q, TAG>(acc2, xw2, p, smem_addr(slab), 4u * a.SCs);
     } else if constexpr (MODE == 3) {
       unsigned p = smem_addr(ws);
-      chunk_loop3<K, S, PH, PW, Q>(acc3, xw3, p, smem_addr(slab), 4u * a.SCs);
+      chunk_loop3<K, S, PH, PW, Q, TAG>(acc3, xw3, p, smem_addr(slab), 4u * a.SCs);
     } else {
       // warp stream: per bucket {c, 0, 0, 0} + Q*K*K weights (16-byte padded); c < 0 ends
       constexpr int NW4 = (Q * K * K + 3) / 4;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
         float x[XH * XW];
         load_window(x, cl);
         const int cl_next = b4[1 + NW4].x;
-        bucket_mask<K, S, PH, PW, Q>(acc, x, smem_addr(b4 + 1));
+        bucket_mask<K, S, PH, PW, Q, TAG>(acc, x, smem_addr(b4 + 1));
         b4 += 1 + NW4;
         cl = cl_next;
       }
@@ -299,9 +299,9 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   }
 }
 
-template <int K, int S, int PH, int PW, int Q, int MINB, int MODE>
+template <int K, int S, int PH, int PW, int Q, int MINB, int MODE, int TAG>
 int launch_tiled(const TiledArgs& a, cudaStream_t s) {
-  auto kern = sconv_tiled_kernel<K, S, PH, PW, Q, MINB, MODE>;
+  auto kern = sconv_tiled_kernel<K, S, PH, PW, Q, MINB, MODE, TAG>;
   if (a.smem_bytes > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
