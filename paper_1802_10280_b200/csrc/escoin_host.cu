@@ -83,8 +83,17 @@ struct DeviceGuard {
 struct Tiling {
   int WM, WP, NB, TR, PR, PC, PCs, SR, SC, SCs, plane;  // PCs >= PC: patch columns per slot row
   int flat;                                              // full-row variants: slots over (image, row)
+  int mos;                                               // > 0: mosaic of the batch, mos images per super-row
   double cost;
 };
+
+// Mosaic tiling (stride 1, "same" padding): the batch is laid out as ONE
+// super-image, images on a grid of `mos` columns, separated by pad zero
+// rows/columns (the zero ring of one image is the neighbour's), so 4x4
+// patches tile 13x13 or 14x14 images with little waste.  Super-image size for
+// a batch of N images:
+int mosaic_rows(const escoin_csr* h, int mos, int N) { return ceil_div(N, mos) * (h->H + h->pad) - h->pad; }
+int mosaic_cols(const escoin_csr* h, int mos) { return mos * (h->W + h->pad) - h->pad; }
 
 // Max shared-memory bank-group conflict degree of the window LDS.128 pattern
 // (8 lanes per quarter-warp, 16-byte accesses) for a candidate layout.
@@ -127,26 +136,39 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
   const int IP = v.mode == 3 ? 2 : 1;  // images per lane; slots and NB count image groups
   bool found = false;
   if (v.full_row && PC != 1) return false;  // full-row variants need the patch to span the output row
+  const bool mos_ok = v.S == 1 && v.mode != 3 && !v.full_row && 2 * h->pad + 1 == h->K && E == h->H && F == h->W;
+  const char* mos_env = std::getenv("ESCOIN_MOSAIC");  // experiments/tests: only mosaic width k (0 = off)
+  const int mos_force = mos_env ? std::atoi(mos_env) : -1;
+  for (int mos = 0; mos <= (mos_ok ? 4 : 0); ++mos)
   for (int WP = 1; WP <= 8; WP *= 2)
   for (int pcs_opt = 0; pcs_opt < 3; ++pcs_opt) {
     if (v.full_row && pcs_opt > 0) continue;
+    if (mos_force >= 0 && mos != mos_force && mos_ok) continue;
+    // mosaic: one tall super-image of the whole (benchmark-size) batch
+    const int PRm = mos ? ceil_div(mosaic_rows(h, mos, 128), v.PH) : PR;
+    const int PCm = mos ? ceil_div(mosaic_cols(h, mos), v.PW) : PC;
     // slot columns per patch row: PC, or padded to 4 / 8 so quarter-warps of
     // window loads hit distinct 16-byte bank groups (idle lanes in the pad)
-    const int PCs = pcs_opt == 0 ? PC : pcs_opt == 1 ? ((PC + 3) & ~3) : ((PC + 7) & ~7);
-    if (pcs_opt > 0 && PCs == (pcs_opt == 1 ? PC : ((PC + 3) & ~3))) continue;  // duplicate option
+    const int PCs = pcs_opt == 0 ? PCm : pcs_opt == 1 ? ((PCm + 3) & ~3) : ((PCm + 7) & ~7);
+    if (pcs_opt > 0 && PCs == (pcs_opt == 1 ? PCm : ((PCm + 3) & ~3))) continue;  // duplicate option
     const int WM = 8 / WP;
     const int slots = 32 * WP;
     if (PCs > slots) continue;
     Tiling t{};
     t.WM = WM;
     t.WP = WP;
-    t.PR = PR;
-    t.PC = PC;
+    t.PR = PRm;
+    t.PC = PCm;
     t.PCs = PCs;
+    t.mos = mos;
     if (v.full_row) {  // flat (image, row) slots: stage every image a 32*WP-row range can touch
       t.flat = 1;
       t.TR = PR;
       t.NB = ceil_div(slots, PR) + 1;
+    } else if (mos) {
+      t.NB = 1;
+      t.TR = slots / PCs;
+      if (t.TR * PCs < slots * 3 / 4) continue;  // too many idle lanes
     } else if (PR * PCs >= slots) {
       t.NB = 1;
       t.TR = std::min(PR, slots / PCs);
@@ -176,7 +198,8 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
     }
     if (2.0 * 4.0 * t.NB * CC * t.plane > slab_budget) continue;  // double-buffered slab must fit
     const double lane_util = t.flat ? 1.0 : double(t.NB * t.TR * t.PC) / slots;
-    const double pix_util = double(E) * F / (double(PR * v.PH) * (PC * v.PW));
+    const double pix_util = mos ? 128.0 * E * F / (double(PRm * v.PH) * (PCm * v.PW))
+                                : double(E) * F / (double(PR * v.PH) * (PC * v.PW));
     const int B = ceil_div(G, WM);
     const double warp_util = double(G) / (B * WM);
     // per input channel and thread: records x (FFMAs + dispatch), window loads,
@@ -189,16 +212,18 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
     const double win = vec ? XH * ((XW + 3) / 4) * 4.0 * (bestc > 1 ? bestc : 1) : XH * XW;
     const double work = v.mode >= 2 ? P / 2.0 * IP + 10 : P + 9;  // issue slots per record
     const double compute = (v.Q * dens * v.K * v.K * (work + lat) + win + 30) / IP;
-    const double staging = 5.0 * t.NB * IP * std::min(t.SR, h->H) * h->W / kTiledThreads / IP;
+    const double staging = mos ? 5.0 * t.SR * mos * h->W / kTiledThreads
+                               : 5.0 * t.NB * IP * std::min(t.SR, h->H) * h->W / kTiledThreads / IP;
     // wave quantisation of the grid at the benchmark batch (128 images)
     const double nctas = t.flat ? double(ceil_div(128 * PR, slots)) * B
+                         : mos  ? double(ceil_div(PRm, t.TR)) * B
                                 : double(ceil_div(128, t.NB * IP)) * ceil_div(PR, t.TR) * B;
     const double waves = nctas / (148.0 * v.min_blocks);
     const double wave_eff = waves / std::ceil(waves);
     t.cost = (compute + staging) / (lane_util * pix_util * warp_util * wave_eff * v.Q * P);
     if (std::getenv("ESCOIN_DEBUG_TILING"))
-      fprintf(stderr, "tiling %s CC=%d WP=%d PCs=%d NB=%d TR=%d SCs=%d plane=%d conflicts=%d cost=%.3f\n", v.name, CC,
-              WP, PCs, t.NB, t.TR, t.SCs, t.plane, bestc, t.cost);
+      fprintf(stderr, "tiling %s CC=%d mos=%d WP=%d PCs=%d NB=%d TR=%d SCs=%d plane=%d conflicts=%d cost=%.3f\n",
+              v.name, CC, mos, WP, PCs, t.NB, t.TR, t.SCs, t.plane, bestc, t.cost);
     cands->push_back(t);
     found = true;
   }
@@ -361,7 +386,7 @@ int upload(const std::vector<T>& v, T** d, cudaStream_t s) {
 // format and shared-memory budget.  Returns ESCOIN_ERR_UNSUPPORTED when the
 // variant cannot tile this layer.
 int plan_tiled(const escoin_csr* h, const TiledVariant& v, int rank, Tiling* t, int* CCout, DS6* ds,
-               size_t* smem, size_t* stage_f_out, size_t* stage_r_out) {
+               size_t* smem, size_t* stage_f_out, size_t* stage_r_out, int* nstages) {
   // Candidates over every channel-chunk size, ranked by modelled cost (plus the
   // per-chunk barrier/staging latency ~1/CC); rank 0 is the model's choice,
   // escoin_csr_autotune also measures ranks 1..2.
@@ -377,23 +402,56 @@ int plan_tiled(const escoin_csr* h, const TiledVariant& v, int rank, Tiling* t, 
     for (const Tiling& tt : cs) all.push_back({tt, CC, tt.cost * (1.0 + 2.0 / CC)});
   }
   std::stable_sort(all.begin(), all.end(), [](const Cand& a, const Cand& b) { return a.cost < b.cost; });
-  int seen = 0;
-  for (const Cand& c : all) {
+  // Feasible plans of the best candidates, each at the deepest pipeline that
+  // fits (3 stages let warps drift two chunks apart; 2 stages lock them to one
+  // — modelled as +12% time); ESCOIN_STAGES forces a depth (experiments).
+  struct Plan {
+    size_t ci;
+    int ns;
+    size_t stage_f, stage_r, sm;
+    double cost;
+  };
+  std::vector<Plan> plans;
+  std::vector<DS6> dss;
+  const size_t limit = size_t(v.min_blocks > 1 ? 110 : 220) * 1024;
+  int force = 0;
+  if (const char* e = std::getenv("ESCOIN_STAGES")) force = std::max(2, std::min(kMaxStages, std::atoi(e)));
+  for (size_t ci = 0; ci < all.size() && plans.size() < size_t(rank) + 6; ++ci) {
+    const Cand& c = all[ci];
+    // ranks are distinct geometries (a different CC alone barely changes time)
+    bool dup = false;
+    for (const Plan& q : plans) {
+      const Tiling& u = all[q.ci].t;
+      dup |= u.mos == c.t.mos && u.WP == c.t.WP && u.PCs == c.t.PCs && u.NB == c.t.NB && u.TR == c.t.TR;
+    }
+    if (dup) continue;
     DS6 dd;
     build_ds6(h, v, c.t.WM, c.CC, c.t.plane, &dd);
     const size_t stage_f = (size_t(c.t.NB) * c.CC * c.t.plane + 3) & ~size_t(3);
     // slack: the dispatch loop prefetches up to two records (16 B each for
     // rel_d variants) past a warp's DONE
     const size_t stage_r = ((dd.max_block + 1) & ~1) + 4;
-    const size_t sm = 2 * stage_f * 4 + 2 * stage_r * 8;
-    if (sm > size_t(v.min_blocks > 1 ? 110 : 220) * 1024) continue;
-    if (seen++ < rank) continue;
-    *t = c.t;
-    *CCout = c.CC;
-    *ds = std::move(dd);
-    *smem = sm;
-    *stage_f_out = stage_f;
-    *stage_r_out = stage_r;
+    int ns = force ? force : 3;
+    while (ns > 2 && size_t(ns) * (stage_f * 4 + stage_r * 8) > limit) --ns;
+    const size_t sm = size_t(ns) * (stage_f * 4 + stage_r * 8);
+    if (sm > limit) continue;
+    plans.push_back({dss.size(), ns, stage_f, stage_r, sm, c.cost * (ns == 2 ? 1.12 : 1.0)});
+    dss.push_back(std::move(dd));
+    plans.back().ci = ci;
+  }
+  std::vector<size_t> order(plans.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return plans[x].cost < plans[y].cost; });
+  if (size_t(rank) < order.size()) {
+    const size_t pi = order[rank];
+    const Plan& p = plans[pi];
+    *nstages = p.ns;
+    *t = all[p.ci].t;
+    *CCout = all[p.ci].CC;
+    *ds = std::move(dss[pi]);
+    *smem = p.sm;
+    *stage_f_out = p.stage_f;
+    *stage_r_out = p.stage_r;
     return ESCOIN_OK;
   }
   return ESCOIN_ERR_UNSUPPORTED;
@@ -408,8 +466,10 @@ int prepare_tiled(escoin_csr* h, int vi, int rank, cudaStream_t s) {
   Tiling t{};
   DS6 ds;
   size_t smem = 0, stage_f = 0, stage_r = 0;
-  const int prc = plan_tiled(h, v, rank, &t, &CC, &ds, &smem, &stage_f, &stage_r);
+  int ns = 2;
+  const int prc = plan_tiled(h, v, rank, &t, &CC, &ds, &smem, &stage_f, &stage_r, &ns);
   if (prc != ESCOIN_OK) return prc;
+  h->targs.NS = ns;
   h->targs.stage_floats = int(stage_f);
   h->targs.stage_recs = int(stage_r);
   free_ds6(h);
@@ -434,6 +494,7 @@ int prepare_tiled(escoin_csr* h, int vi, int rank, cudaStream_t s) {
   a.NB = t.NB;
   a.IP = v.mode == 3 ? 2 : 1;
   a.flat = t.flat;
+  a.mos = t.mos;
   a.TR = t.TR;
   a.SR = t.SR;
   a.SCs = t.SCs;
@@ -734,7 +795,11 @@ int escoin_sconv_forward(int N, int C, int H, int W, int M, int K, int stride, i
     a.bias = bias;
     a.relu = relu ? 1 : 0;
     a.N = N;
-    a.ntiles = a.flat ? ceil_div(N * a.PR, a.WP * 32) : ceil_div(N, a.NB * a.IP) * a.tiles_r;
+    if (a.mos) {  // the super-image grows with N
+      a.PR = ceil_div(mosaic_rows(h, a.mos, N), tv[h->kernel - 1].PH);
+      a.tiles_r = ceil_div(a.PR, a.TR);
+    }
+    a.ntiles = a.mos ? a.tiles_r : a.flat ? ceil_div(N * a.PR, a.WP * 32) : ceil_div(N, a.NB * a.IP) * a.tiles_r;
     a.debug = g_debug_kernel;
     if (a.ntiles > 65535) return ESCOIN_ERR_OVERFLOW;
     rc = tv[h->kernel - 1].launch(a, s);
@@ -811,7 +876,7 @@ int escoin_csr_autotune(escoin_csr* h, int N, const float* in, float* out, const
   int best = -1, best_rank = 0;
   float best_t = 0.f;
   int rc = ESCOIN_OK;
-  constexpr int kRanks = 3;  // tiling candidates measured per variant
+  constexpr int kRanks = 4;  // tiling candidates (distinct geometries) measured per variant
   for (int idr = 0; idr <= nv * kRanks && rc == ESCOIN_OK; ++idr) {
     const int id = idr / kRanks, rank = idr % kRanks;
     if (id == 0 && rank > 0) continue;
@@ -865,7 +930,7 @@ const char* escoin_status_string(int status) {
 const char* escoin_version(void) { return "escoin-b200 0.1 sm_100a"; }
 
 /* Internal (not in escoin.h): host-only plan of tiled variant `id` for tests.
- * out[13] = {WM, WP, NB, TR, PR, PC, SR, SCs, plane, CC, smem_bytes, records, PCs}. */
+ * out[14] = {WM, WP, NB, TR, PR, PC, SR, SCs, plane, CC, smem_bytes, records, PCs, stages}. */
 int escoin_internal_plan(const escoin_csr* h, int id, int64_t* out) {
   int nv = 0;
   const TiledVariant* tv = tiled_variants(&nv);
@@ -875,11 +940,12 @@ int escoin_internal_plan(const escoin_csr* h, int id, int64_t* out) {
   DS6 ds;
   int CC = 0;
   size_t smem = 0, sf = 0, sr = 0;
-  const int rc = plan_tiled(h, tv[id - 1], 0, &t, &CC, &ds, &smem, &sf, &sr);
+  int ns = 2;
+  const int rc = plan_tiled(h, tv[id - 1], 0, &t, &CC, &ds, &smem, &sf, &sr, &ns);
   if (rc != ESCOIN_OK) return rc;
-  const int64_t v[13] = {t.WM, t.WP, t.NB, t.TR, t.PR, t.PC, t.SR, t.SCs, t.plane, CC, int64_t(smem),
-                         int64_t(ds.recs.size()), t.PCs};
-  for (int i = 0; i < 13; ++i) out[i] = v[i];
+  const int64_t v[14] = {t.WM, t.WP, t.NB, t.TR, t.PR, t.PC, t.SR, t.SCs, t.plane, CC, int64_t(smem),
+                         int64_t(ds.recs.size()), t.PCs, ns};
+  for (int i = 0; i < 14; ++i) out[i] = v[i];
   return ESCOIN_OK;
 }
 

@@ -8,6 +8,7 @@
 namespace escoin {
 
 constexpr int kTiledThreads = 256;   // 8 warps = WM x WP
+constexpr int kMaxStages = 4;       // smem pipeline depth limit (mbarrier pairs per CTA)
 constexpr int kMaxStagePos = 8;      // staged plane positions per thread (SR*SCs <= 2048)
 constexpr int kHdrBase = 1 << 20;    // bucket header record: code = kHdrBase + c_local
 constexpr int kDone = -1;            // end of a warp's record stream for one chunk
@@ -25,10 +26,13 @@ struct TiledArgs {
   int IP;               // images per lane (image group size): 2 for mode-3 variants, else 1
   int flat;             // 1: full-row patches (PC == 1) over a flat (image, patch-row) index, so one
                         // warp's 32 rows may span images (no idle lanes for PR not dividing 32)
+  int mos;              // > 0: mosaic tiling — the batch is one super-image with `mos` images per
+                        // super-row, periods H+pad / W+pad (shared zero separators); NB = 1
   int SR, SCs, plane;   // staged slab rows, row stride (words), plane stride (words)
   int CC;               // input channels per chunk
   int tiles_r;          // ceil(PR / TR)
   int B, ntiles;        // grid: m-blocks x pixel tiles
+  int NS;               // shared-memory stages (2..kMaxStages), mbarrier-pipelined
   int stage_floats;     // floats per slab stage (multiple of 4)
   int stage_recs;       // records per record stage (even)
   int smem_bytes;
@@ -36,7 +40,7 @@ struct TiledArgs {
   const int* sched;     // per active chunk: [k, rec_start, rec_count, woff[WM]]
   const int* sched_off; // [B+1] first entry of each m-block
   int sched_stride;     // 3 + WM
-  int debug;            // timing experiments only (ESCOIN_DEBUG_KERNEL): 1 skip staging, 2 skip barrier, 4 skip stores
+  int debug;            // timing experiments only (ESCOIN_DEBUG_KERNEL): 1 skip input staging, 4 skip stores
 };
 
 typedef int (*TiledLaunchFn)(const TiledArgs&, cudaStream_t);

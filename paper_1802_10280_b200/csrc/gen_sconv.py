@@ -59,6 +59,9 @@ VARIANTS = [
     ("t3s1_q3_4x4_s", 3, 1, 4, 4, 3),
     ("t3s1_q4_2x7", 3, 1, 2, 7, 4),
     ("t3s1_q4_1x13_r", 3, 1, 1, 13, 4),
+    ("t3s1_q3_1x13_r", 3, 1, 1, 13, 3),
+    ("t3s1_q4_1x13_rx", 3, 1, 1, 13, 4),
+    ("t3s1_q3_1x13_rx", 3, 1, 1, 13, 3),
     ("t3s1_q5_4x4_s", 3, 1, 4, 4, 5),
     ("t5s1_q1_4x4", 5, 1, 4, 4, 1),
     ("t5s1_q2_4x4_s", 5, 1, 4, 4, 2),
@@ -507,10 +510,10 @@ def main(outdir):
     os.makedirs(outdir, exist_ok=True)
     table = []
     for name, K, S, PH, PW, Q in VARIANTS:
-        full_row = name.endswith("_r")
+        full_row = name.endswith("_r") or name.endswith("_rx")
         rel = name.endswith("_x")
         if rel:
-            body, outs, ins = chunk_loop_rel(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0, D=REL_D)
+            body, outs, ins = chunk_loop_rel(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0 or full_row, D=REL_D)
         else:
             body, outs, ins = chunk_loop(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0 or full_row,
                                          single=name.endswith("_s"))

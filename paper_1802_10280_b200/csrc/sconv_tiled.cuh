@@ -66,9 +66,28 @@ __device__ __forceinline__ void cp_async4(unsigned dst, const void* src, int src
 __device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+// Completion of this thread's outstanding cp.async copies counts as one
+// arrival on the mbarrier (whose expected count covers every thread).
+__device__ __forceinline__ void cp_async_arrive(unsigned bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
 
 template <int K, int S, int PH, int PW, int Q, int MINB, int MODE, int TAG>
 __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const TiledArgs a) {
@@ -81,11 +100,14 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   constexpr int XWV = (XW + 3) / 4;
   constexpr int IP = MODE == 3 ? 2 : 1;  // images per lane (interleaved innermost in smem)
 
+  // NS stages of {input slab, records}; stage s: slab smem + s*stage_floats,
+  // records recbase + s*stage_recs.  full[s]: the chunk's copies landed (one
+  // cp.async arrival per thread); empty[s]: every warp finished reading it.
   extern __shared__ __align__(16) float smem[];
-  float* const slab0 = smem;
-  float* const slab1 = smem + a.stage_floats;
-  int2* const rec0 = reinterpret_cast<int2*>(smem + 2 * a.stage_floats);
-  int2* const rec1 = rec0 + a.stage_recs;
+  __shared__ __align__(8) unsigned long long bars[2 * kMaxStages];
+  const int NS = a.NS;
+  int2* const recbase = reinterpret_cast<int2*>(smem + NS * a.stage_floats);
+  const unsigned full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[kMaxStages]);
 
   const int b = blockIdx.x;
   const int tile = blockIdx.y;
@@ -128,7 +150,13 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   const int nint = nrow * a.W;                            // interior floats per plane
   {
     float4* z = reinterpret_cast<float4*>(smem);
-    for (int i = threadIdx.x; i < (2 * a.stage_floats) / 4; i += kTiledThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = threadIdx.x; i < (NS * a.stage_floats) / 4; i += kTiledThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full0 + 8u * s, kTiledThreads);
+      mbar_init(empty0 + 8u * s, kTiledThreads / 32);
+    }
   }
   __syncthreads();
 
@@ -136,10 +164,42 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   const int nact = a.sched_off[b + 1] - a.sched_off[b];
   const int64_t HW = static_cast<int64_t>(a.H) * a.W;
 
-  auto stage = [&](int ai, int st) {
+  // Stage chunk ai into buffer ai % NS (after every warp released the chunk
+  // that used it before), then arrive on full[ai % NS] when the copies land.
+  auto stage = [&](int ai) {
+    const int st = ai % NS;
+    if (ai >= NS) mbar_wait(empty0 + 8u * st, ((ai / NS) - 1) & 1);
     const int* e = sched + ai * a.sched_stride;
     const int c0 = e[0] * a.CC, rs = e[1], rc = e[2];
-    const unsigned sb = smem_addr(st ? slab1 : slab0);
+    const unsigned sb = smem_addr(smem + st * a.stage_floats);
+    if (a.mos && (!(a.debug & 1) || ai < NS)) {
+      // mosaic: slab row r = super input row y_first + r; segment (r, image
+      // column j) holds W floats of image n = block * mos + j, or stays zero
+      // (separator rows, rows above the batch, images beyond N)
+      const int RP = a.H + a.pad, CP = a.W + a.pad;
+      const int ncl = min(a.CC, a.C - c0);
+      for (int ee = threadIdx.x; ee < a.SR * a.mos * a.W; ee += kTiledThreads) {
+        const int t = ee / a.W, x = ee - t * a.W;
+        const int r = t / a.mos, j = t - r * a.mos;
+        const int Y = y_first + r;
+        if (Y < 0) continue;
+        const int blk = Y / RP, y = Y - blk * RP, n = blk * a.mos + j;
+        if (y >= a.H || n >= a.N) continue;
+        unsigned sp = sb + 4u * static_cast<unsigned>(r * a.SCs + a.pad + j * CP + x);
+        const float* g = a.in + ((static_cast<int64_t>(n) * a.C + c0) * a.H + y) * a.W + x;
+        int cl = 0;
+#pragma unroll 4
+        for (; cl < ncl; ++cl) {
+          cp_async4(sp, g, 4);
+          sp += 4u * a.plane;
+          g += HW;
+        }
+        for (; cl < a.CC; ++cl) {
+          cp_async4(sp, a.in, 0);
+          sp += 4u * a.plane;
+        }
+      }
+    } else if (!(a.debug & 1) || ai < NS)
     // thread-owned interior elements ee; planes (image, channel) in the inner loop
     for (int ee = threadIdx.x; ee < nint; ee += kTiledThreads) {
       const int r = ee / a.W;
@@ -163,9 +223,9 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
         }
       }
     }
-    const unsigned rb = smem_addr(st ? rec1 : rec0);
+    const unsigned rb = smem_addr(recbase + st * a.stage_recs);
     for (int i = threadIdx.x; i < (rc >> 1); i += kTiledThreads) cp_async16(rb + 16u * i, a.recs + rs + 2 * i);
-    cp_async_commit();
+    cp_async_arrive(full0 + 8u * st);
   };
 
   float acc[Q * P];
@@ -189,25 +249,17 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
 #pragma unroll
   for (int i = 0; i < NX2; ++i) xw2[i] = 0ull;
 
-  // One barrier per chunk: after it, stage ai has landed (wait_group 0 +
-  // barrier) and every warp has finished chunk ai-1, so its buffer can take
-  // chunk ai+1, which then streams in under the whole compute of chunk ai.
-  if (nact > 0) stage(0, 0);
+  // Pipeline without CTA barriers: chunk ai+1 is issued at the top of
+  // iteration ai into buffer (ai+1) % NS, which requires every warp to have
+  // released chunk ai+1-NS.  With NS = 3 a warp may run up to two chunks ahead
+  // of the slowest warp (per-warp record counts differ chunk by chunk), where a
+  // per-chunk __syncthreads would make every chunk cost the slowest warp's time.
+  if (nact > 0) stage(0);
   for (int ai = 0; ai < nact; ++ai) {
-    const int st = ai & 1;
-    cp_async_wait<0>();
-    if (!(a.debug & 2)) __syncthreads();
-    if (ai + 1 < nact) {
-      if (a.debug & 1) {  // timing experiment: records only, input slab left stale
-        const int* e = sched + (ai + 1) * a.sched_stride;
-        const unsigned rb = smem_addr(st ? rec0 : rec1);
-        for (int i = threadIdx.x; i < (e[2] >> 1); i += kTiledThreads) cp_async16(rb + 16u * i, a.recs + e[1] + 2 * i);
-        cp_async_commit();
-      } else {
-        stage(ai + 1, st ^ 1);
-      }
-    }
-    const float* slab = (st ? slab1 : slab0) + win_off;
+    const int st = ai % NS;
+    if (ai + 1 < nact) stage(ai + 1);
+    mbar_wait(full0 + 8u * st, (ai / NS) & 1);
+    const float* slab = smem + st * a.stage_floats + win_off;
     auto load_window = [&](float* x, int cl) {
       const float* src = slab + cl * a.plane;
       if (VEC_ALWAYS || a.PC == 1) {
@@ -229,7 +281,7 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
           for (int c = 0; c < XW; ++c) x[r * XW + c] = src[r * a.SCs + c];
       }
     };
-    const int2* ws = (st ? rec1 : rec0) + sched[ai * a.sched_stride + 3 + wm];
+    const int2* ws = recbase + st * a.stage_recs + sched[ai * a.sched_stride + 3 + wm];
     if constexpr (MODE == 0) {
       unsigned p = smem_addr(ws);
       chunk_loop<K, S, PH, PW, Q, TAG>(acc, xw, p, smem_addr(slab), 4u * a.SCs);
@@ -253,6 +305,8 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
         cl = cl_next;
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8u * st);
   }
 
   if constexpr (MODE == 2) {
@@ -264,7 +318,44 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
   }
 
   // Epilogue (reading R#10): v = acc + bias[m]; ReLU; NCHW store.
-  if (active && !(a.debug & 4 && acc[0] != 12345.0f)) {
+  if (a.mos) {
+    // mosaic: super output row R -> (image block, oh), column X -> (image column, ow)
+    if (active && !(a.debug & 4 && acc[0] != 12345.0f)) {
+      const int RP = a.H + a.pad, CP = a.W + a.pad;
+      int rb[PH], ro[PH], cj[PW], co[PW];
+#pragma unroll
+      for (int ph = 0; ph < PH; ++ph) {
+        const int R = (pr0 + pr) * PH + ph;
+        rb[ph] = R / RP;
+        ro[ph] = R - rb[ph] * RP;
+      }
+#pragma unroll
+      for (int pw = 0; pw < PW; ++pw) {
+        const int X = pc * PW + pw;
+        cj[pw] = X / CP;
+        co[pw] = X - cj[pw] * CP;
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int m = (b * a.WM + wm) * Q + q;
+        if (m < a.M) {
+          const float bv = a.bias ? __ldg(a.bias + m) : 0.0f;
+#pragma unroll
+          for (int ph = 0; ph < PH; ++ph) {
+#pragma unroll
+            for (int pw = 0; pw < PW; ++pw) {
+              const int n = rb[ph] * a.mos + cj[pw];
+              if (ro[ph] < a.H && co[pw] < a.W && cj[pw] < a.mos && n < a.N) {
+                float v = __fadd_rn(acc[q * P + ph * PW + pw], bv);
+                if (a.relu) v = v > 0.0f ? v : 0.0f;
+                a.out[((static_cast<int64_t>(n) * a.M + m) * a.E + ro[ph]) * a.F + co[pw]] = v;
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (active && !(a.debug & 4 && acc[0] != 12345.0f)) {
 #pragma unroll
     for (int j = 0; j < IP; ++j) {
       const int n = n0 + img * IP + j;

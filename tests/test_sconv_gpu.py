@@ -113,6 +113,45 @@ def test_parity_grid(case):
         assert o.tobytes() == outs[0].tobytes()
 
 
+# ------------------------------------------------------------------ mosaic tiling
+MOSAIC_GRID = [  # N, C, H, W, M, K, pad — "same" padding, stride 1 (where mosaic applies)
+    (5, 12, 13, 13, 40, 3, 1), (7, 9, 14, 14, 33, 3, 1), (3, 10, 7, 7, 20, 3, 1), (3, 6, 27, 27, 17, 5, 2),
+    (1, 8, 13, 13, 16, 3, 1), (9, 5, 6, 9, 12, 3, 1),
+]
+
+
+@pytest.mark.parametrize("mos", [1, 2, 3, 4])
+@pytest.mark.parametrize("case", MOSAIC_GRID)
+def test_mosaic_tiling_parity(case, mos, monkeypatch):
+    # the batch laid out as one super-image (mos images per super-row, shared
+    # zero separators): same values, same bits as the per-image tiling
+    N, C, H, W, M, K, p = case
+    rng = np.random.default_rng(7 + mos)
+    x = rng.random((N, C, H, W)).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.25] = 0.0
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    ref, scale = oracle_ref(w, x, b, 1, p, True)
+    monkeypatch.setenv("ESCOIN_MOSAIC", "0")
+    base = {k: run_gpu(w, x, b, 1, p, True, kernel=k)[0] for k in kernel_ids(K, 1) if k != 0}
+    monkeypatch.setenv("ESCOIN_MOSAIC", str(mos))
+    ran = 0
+    for k, o0 in base.items():
+        out, _ = run_gpu(w, x, b, 1, p, True, kernel=k)
+        if out is None:
+            continue
+        check(out, ref, scale, b)
+        if o0 is not None:
+            assert out.tobytes() == o0.tobytes(), k
+        ran += 1
+    assert ran >= 1
+
+
+def test_mosaic_full_batch_sampled(monkeypatch):
+    monkeypatch.setenv("ESCOIN_MOSAIC", "2")
+    test_full_batch_sampled("alexnet", "conv3")
+
+
 # ------------------------------------------------------------------ exact regimes
 @pytest.mark.parametrize("case", [(2, 16, 14, 14, 32, 3, 1, 1), (2, 24, 13, 13, 20, 5, 1, 2),
                                   (1, 32, 28, 28, 16, 3, 1, 1), (2, 40, 7, 7, 50, 1, 1, 0)])
