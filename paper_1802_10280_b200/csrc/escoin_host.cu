@@ -298,7 +298,38 @@ void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int p
           const int64_t bk = first + int64_t(wm) * CC + cl;
           if (cnt[bk + 1] != cnt[bk]) cls.push_back(cl);
         }
-        if ((v.mode == 0 || v.mode == 2 || v.mode == 3) && v.rel_d == 0) {
+        if (v.link) {
+          // Linked stream: header {idx(item0)}, then item i = {idx(item i+1)
+          // relative to item i's jump list, payload(i)} (+ {abs(i+1), 0} when
+          // rel_d > 0); items: NEXT{END, window offset} REC* ... DONE{END+1}.
+          woff[wm] = int(out->recs.size()) - start;
+          std::vector<int2> items;
+          for (size_t i = 0; i < cls.size(); ++i) {
+            const int64_t bk = first + int64_t(wm) * CC + cls[i];
+            items.push_back(make_int2(END, cls[i] * plane * 4));
+            for (int64_t r = cnt[bk]; r < cnt[bk + 1]; ++r) items.push_back(sorted[r]);
+          }
+          items.push_back(make_int2(END + 1, 0));
+          const int D = v.rel_d;
+          auto enc = [&](int pred, int abs) {  // pred < 0: START / NEXT (full list)
+            if (D == 0 || pred < 0 || pred >= END) return abs;
+            if (abs == END) return D;
+            if (abs == END + 1) return D + 1;
+            if (abs - pred - 1 >= 0 && abs - pred - 1 < D) return abs - pred - 1;
+            return D + 2;  // FAR
+          };
+          auto put = [&](int idx, int payload, int abs) {
+            out->recs.push_back(make_int2(idx, payload));
+            if (D > 0) out->recs.push_back(make_int2(abs, 0));
+          };
+          put(items[0].x, 0, items[0].x);
+          for (size_t i = 0; i < items.size(); ++i) {
+            const bool last = i + 1 == items.size();
+            const int nabs = last ? 0 : items[i + 1].x;
+            put(last ? 0 : enc(items[i].x, nabs), items[i].y, nabs);
+          }
+          if (out->recs.size() & 1) out->recs.push_back(make_int2(0, 0));
+        } else if ((v.mode == 0 || v.mode == 2 || v.mode == 3) && v.rel_d == 0) {
           woff[wm] = int(out->recs.size()) - start;
           // One stream per warp and chunk, run by ONE inline-PTX dispatch loop:
           // per bucket NEXT{END, byte offset of channel c's window} REC*, then

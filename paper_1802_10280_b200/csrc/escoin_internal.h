@@ -52,6 +52,7 @@ struct TiledVariant {
   int mode;        // 0: per-record brx dispatch; 1: dense-bucket mask sweep; 2/3: FFMA2
   int full_row;    // patch spans the whole output row (PC must be 1): vector window loads, flat tiling
   int rel_d;       // > 0: 16-byte records with predecessor-relative dispatch indices (chunk_loop_rel)
+  int link;        // 1: linked records {idx(next), payload(self)} behind a header (chunk_loop_link)
   TiledLaunchFn launch;
 };
 

@@ -24,6 +24,7 @@ Usage: gen_sconv.py OUTDIR   (writes variant_<name>.cu + variants_table.inc)
 """
 import os
 import sys
+import re
 import zlib
 
 # name, K, S, PH, PW, Q   (Q*PH*PW accumulators; ptxas wants acc <= ~112 regs
@@ -52,6 +53,9 @@ VARIANTS = [
     ("t3s1_q4_4x4", 3, 1, 4, 4, 4),
     ("t3s1_q4_4x4_s", 3, 1, 4, 4, 4),
     ("t3s1_q4_4x4_x", 3, 1, 4, 4, 4),
+    ("t3s1_q4_4x4_n", 3, 1, 4, 4, 4),
+    ("t3s1_q4_4x4_nx", 3, 1, 4, 4, 4),
+    ("t3s1_q3_4x4_nx", 3, 1, 4, 4, 3),
     ("t3s1_q5_4x4_x", 3, 1, 4, 4, 5),
     ("t3s1_q3_4x4_x", 3, 1, 4, 4, 3),
     ("t3s1_q2_4x4", 3, 1, 4, 4, 2),
@@ -66,6 +70,8 @@ VARIANTS = [
     ("t5s1_q1_4x4", 5, 1, 4, 4, 1),
     ("t5s1_q2_4x4_s", 5, 1, 4, 4, 2),
     ("t5s1_q2_4x4_x", 5, 1, 4, 4, 2),
+    ("t5s1_q2_4x4_nx", 5, 1, 4, 4, 2),
+    ("t5s1_q1_4x4_nx", 5, 1, 4, 4, 1),
     ("t5s1_q1_4x4_x", 5, 1, 4, 4, 1),
     ("t5s1_q2_4x4", 5, 1, 4, 4, 2),
     ("t1s1_q6_4x4", 1, 1, 4, 4, 6),
@@ -293,6 +299,87 @@ def chunk_loop_rel(K, S, PH, PW, Q, vec, D):
     return body, outs, ins
 
 
+def chunk_loop_link(K, S, PH, PW, Q, vec, D):
+    """Dispatch loop over LINKED records: record r = {idx(r+1), payload(r)}
+    (plus {abs(r+1), 0} when D > 0), so the jump-table load for the next
+    dispatch uses a register that is ready on entry to the case, and the
+    record prefetch rotates only two registers (w, c).  Per record: LDS.64,
+    pointer add, table index, LDC, 2 MOV, BRX (vs 4 MOV + 2 loads' worth of
+    bookkeeping in chunk_loop).  The stream starts with a header {idx(first)}.
+
+    D == 0: every case's jump list is the full list (idx = absolute code).
+    D > 0 : case c's list is the D codes after c + NEXT, DONE, FAR (small
+            constant-cache footprint); FAR re-dispatches via the full list from
+            the absolute code stored in the record.
+    """
+    P = PH * PW
+    XH, XW = (PH - 1) * S + K, (PW - 1) * S + K
+    XWV = (XW + 3) // 4
+    NC = Q * K * K
+    nacc = Q * P
+    nx = XH * XW
+    x0 = nacc
+    pidx = nacc + nx
+    bidx, ridx = pidx + 1, pidx + 2
+    RS = 16 if D > 0 else 8
+    full = ", ".join(["L%d" % i for i in range(NC)] + ["LNEXT", "LEND"])
+    L = ["{",
+         ".reg .b32 c, lc, lw, wb, wa, t, ab;",
+         ".reg .f32 w, d0, d1, d2, d3;",
+         "ld.shared.b32 t, [%%%d];" % pidx,
+         "ld.shared.v2.b32 {c, wb}, [%%%d+%d];" % (pidx, RS),
+         "add.u32 %%%d, %%%d, %d;" % (pidx, pidx, 2 * RS),
+         "mov.b32 w, wb;",
+         "tfull: .branchtargets " + full + ";",
+         "brx.idx.uni t, tfull;"]
+
+    def head():
+        return ["ld.shared.v2.b32 {lc, lw}, [%%%d];" % pidx, "add.u32 %%%d, %%%d, %d;" % (pidx, pidx, RS)]
+
+    def tail(site):
+        return ["mov.b32 t, c;", "mov.b32 w, lw;", "mov.b32 c, lc;", "brx.idx.uni t, %s;" % site]
+
+    for code in range(NC):
+        q, kh, kw = code // (K * K), (code // K) % K, code % K
+        L.append("L%d:" % code)
+        L += head()
+        for ph in range(PH):
+            for pw in range(PW):
+                a = q * P + ph * PW + pw
+                xi = x0 + (ph * S + kh) * XW + (pw * S + kw)
+                L.append("fma.rn.f32 %%%d, w, %%%d, %%%d;" % (a, xi, a))
+        if D > 0:
+            succ = ["L%d" % (code + 1 + i) if code + 1 + i < NC else "LFAR" for i in range(D)]
+            L.append("t%d: .branchtargets %s;" % (code, ", ".join(succ + ["LNEXT", "LEND", "LFAR"])))
+            L += tail("t%d" % code)
+        else:
+            L += tail("tfull")
+    L.append("LNEXT:")
+    L += head()
+    L.append("mov.b32 wa, w;")
+    L.append("add.u32 wa, wa, %%%d;" % bidx)
+    for r in range(XH):
+        if vec:
+            for v in range(XWV):
+                regs = ["%%%d" % (x0 + r * XW + 4 * v + j) if 4 * v + j < XW else "d%d" % j for j in range(4)]
+                L.append("ld.shared.v4.f32 {%s}, [wa+%d];" % (", ".join(regs), 16 * v))
+        else:
+            for c in range(XW):
+                L.append("ld.shared.f32 %%%d, [wa+%d];" % (x0 + r * XW + c, 4 * c))
+        if r + 1 < XH:
+            L.append("add.u32 wa, wa, %%%d;" % ridx)
+    L += tail("tfull")
+    if D > 0:
+        # FAR: dispatching record r+1 from case r; p = &rec[r+2]; abs(r+1) in rec[r]
+        L += ["LFAR:", "ld.shared.b32 ab, [%%%d+%d];" % (pidx, -2 * RS + 8), "brx.idx.uni ab, tfull;"]
+    L += ["LEND:", "}"]
+    body = "\n".join('      "%s\\n"' % l for l in L)
+    outs = ", ".join('"+f"(acc[%d])' % i for i in range(nacc)) + ", " + \
+        ", ".join('"+f"(x[%d])' % i for i in range(nx)) + ', "+r"(p)'
+    ins = '"r"(wbase), "r"(rowb)'
+    return body, outs, ins
+
+
 def chunk_loop3(K, S, PH, PW, Q):
     """Image-pair variant: every lane holds its patch for two images; the
     window registers are (image 2g, image 2g+1) pairs loaded straight from the
@@ -510,20 +597,25 @@ def main(outdir):
     os.makedirs(outdir, exist_ok=True)
     table = []
     for name, K, S, PH, PW, Q in VARIANTS:
-        full_row = name.endswith("_r") or name.endswith("_rx")
-        rel = name.endswith("_x")
-        if rel:
-            body, outs, ins = chunk_loop_rel(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0 or full_row, D=REL_D)
+        # suffix letters: r = full-row tiling, s = single dispatch site,
+        # x = relative (small) jump tables, n = linked records
+        last = name.split("_")[-1]
+        sfx = "" if re.match(r"^\d+x\d+$", last) else last
+        full_row, rel, link = "r" in sfx, "x" in sfx, "n" in sfx
+        vec = (PW * S) % 4 == 0 or full_row
+        if link:
+            body, outs, ins = chunk_loop_link(K, S, PH, PW, Q, vec=vec, D=REL_D if rel else 0)
+        elif rel:
+            body, outs, ins = chunk_loop_rel(K, S, PH, PW, Q, vec=vec, D=REL_D)
         else:
-            body, outs, ins = chunk_loop(K, S, PH, PW, Q, vec=(PW * S) % 4 == 0 or full_row,
-                                         single=name.endswith("_s"))
+            body, outs, ins = chunk_loop(K, S, PH, PW, Q, vec=vec, single="s" in sfx)
         src = TEMPLATE.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs, ins=ins,
                               MINB=min_blocks(K, S, PH, PW, Q))
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
         table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 0, 1 if full_row else 0,
-                      REL_D if rel else 0))
+                      REL_D if rel else 0, 1 if link else 0))
     for name, K, S, PH, PW, Q in VARIANTS_MASK:
         body, outs, ins = bucket_mask(K, S, PH, PW, Q)
         src = TEMPLATE_MASK.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NS=Q * K * K, body=body, outs=outs,
@@ -531,7 +623,7 @@ def main(outdir):
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 1, 0, 0))
+        table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 1, 0, 0, 0))
     for name, K, S, PH, PW, Q in VARIANTS_F2:
         body, outs, ins = chunk_loop2(K, S, PH, PW, Q)
         mb = min_blocks_f2(K, S, PH, PW, Q)
@@ -540,7 +632,7 @@ def main(outdir):
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, mb, 2, 0, 0))
+        table.append((name, K, S, PH, PW, Q, mb, 2, 0, 0, 0))
     for name, K, S, PH, PW, Q in VARIANTS_P3:
         body, outs, ins = chunk_loop3(K, S, PH, PW, Q)
         mb = min_blocks_p3(K, S, PH, PW, Q)
@@ -549,13 +641,13 @@ def main(outdir):
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, S, PH, PW, Q, mb, 3, 0, 0))
+        table.append((name, K, S, PH, PW, Q, mb, 3, 0, 0, 0))
     keep = set("variant_%s.cu" % t[0] for t in table)
     for f in os.listdir(outdir):
         if f.startswith("variant_") and f.endswith(".cu") and f not in keep:
             os.remove(os.path.join(outdir, f))
     decl = "\n".join("int launch_%s(const TiledArgs&, cudaStream_t);" % t[0] for t in table)
-    rows = "\n".join('  {"%s", %d, %d, %d, %d, %d, %d, %d, %d, %d, &launch_%s},' % (t + (t[0],)) for t in table)
+    rows = "\n".join('  {"%s", %d, %d, %d, %d, %d, %d, %d, %d, %d, %d, &launch_%s},' % (t + (t[0],)) for t in table)
     inc = "// GENERATED by gen_sconv.py — do not edit.\n%s\nstatic const TiledVariant kTiledVariants[] = {\n%s\n};\n" % (
         decl, rows)
     path = os.path.join(outdir, "variants_table.inc")
