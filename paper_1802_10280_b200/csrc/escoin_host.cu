@@ -328,6 +328,7 @@ void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int p
             const int nabs = last ? 0 : items[i + 1].x;
             put(last ? 0 : enc(items[i].x, nabs), items[i].y, nabs);
           }
+          put(0, 0, 0);  // depth-2 loops prefetch one record past DONE
           if (out->recs.size() & 1) out->recs.push_back(make_int2(0, 0));
         } else if ((v.mode == 0 || v.mode == 2 || v.mode == 3) && v.rel_d == 0) {
           woff[wm] = int(out->recs.size()) - start;

@@ -56,6 +56,7 @@ VARIANTS = [
     ("t3s1_q4_4x4_n", 3, 1, 4, 4, 4),
     ("t3s1_q4_4x4_nx", 3, 1, 4, 4, 4),
     ("t3s1_q3_4x4_nx", 3, 1, 4, 4, 3),
+
     ("t3s1_q5_4x4_x", 3, 1, 4, 4, 5),
     ("t3s1_q3_4x4_x", 3, 1, 4, 4, 3),
     ("t3s1_q2_4x4", 3, 1, 4, 4, 2),
@@ -72,6 +73,7 @@ VARIANTS = [
     ("t5s1_q2_4x4_x", 5, 1, 4, 4, 2),
     ("t5s1_q2_4x4_nx", 5, 1, 4, 4, 2),
     ("t5s1_q1_4x4_nx", 5, 1, 4, 4, 1),
+
     ("t5s1_q1_4x4_x", 5, 1, 4, 4, 1),
     ("t5s1_q2_4x4", 5, 1, 4, 4, 2),
     ("t1s1_q6_4x4", 1, 1, 4, 4, 6),
@@ -299,7 +301,7 @@ def chunk_loop_rel(K, S, PH, PW, Q, vec, D):
     return body, outs, ins
 
 
-def chunk_loop_link(K, S, PH, PW, Q, vec, D):
+def chunk_loop_link(K, S, PH, PW, Q, vec, D, depth=1):
     """Dispatch loop over LINKED records: record r = {idx(r+1), payload(r)}
     (plus {abs(r+1), 0} when D > 0), so the jump-table load for the next
     dispatch uses a register that is ready on entry to the case, and the
@@ -324,20 +326,27 @@ def chunk_loop_link(K, S, PH, PW, Q, vec, D):
     RS = 16 if D > 0 else 8
     full = ", ".join(["L%d" % i for i in range(NC)] + ["LNEXT", "LEND"])
     L = ["{",
-         ".reg .b32 c, lc, lw, wb, wa, t, ab;",
+         ".reg .b32 c, lc, lw, lc2, lw2, wb, wa, t, ab;",
          ".reg .f32 w, d0, d1, d2, d3;",
          "ld.shared.b32 t, [%%%d];" % pidx,
-         "ld.shared.v2.b32 {c, wb}, [%%%d+%d];" % (pidx, RS),
-         "add.u32 %%%d, %%%d, %d;" % (pidx, pidx, 2 * RS),
-         "mov.b32 w, wb;",
-         "tfull: .branchtargets " + full + ";",
-         "brx.idx.uni t, tfull;"]
+         "ld.shared.v2.b32 {c, wb}, [%%%d+%d];" % (pidx, RS)]
+    if depth == 2:  # also record 1: {idx(r2), w(r1)}
+        L.append("ld.shared.v2.b32 {lc, lw}, [%%%d+%d];" % (pidx, 2 * RS))
+    L += ["add.u32 %%%d, %%%d, %d;" % (pidx, pidx, (3 if depth == 2 else 2) * RS),
+          "mov.b32 w, wb;",
+          "tfull: .branchtargets " + full + ";",
+          "brx.idx.uni t, tfull;"]
 
     def head():
+        if depth == 2:  # depth 2 = depth 1 with the record load issued at the TAIL (after the
+            return []   # moves that free its registers), so a whole dispatch hides its latency
         return ["ld.shared.v2.b32 {lc, lw}, [%%%d];" % pidx, "add.u32 %%%d, %%%d, %d;" % (pidx, pidx, RS)]
 
     def tail(site):
-        return ["mov.b32 t, c;", "mov.b32 w, lw;", "mov.b32 c, lc;", "brx.idx.uni t, %s;" % site]
+        mv = ["mov.b32 t, c;", "mov.b32 w, lw;", "mov.b32 c, lc;"]
+        if depth == 2:
+            mv += ["ld.volatile.shared.v2.b32 {lc, lw}, [%%%d];" % pidx, "add.u32 %%%d, %%%d, %d;" % (pidx, pidx, RS)]
+        return mv + ["brx.idx.uni t, %s;" % site]
 
     for code in range(NC):
         q, kh, kw = code // (K * K), (code // K) % K, code % K
@@ -370,8 +379,9 @@ def chunk_loop_link(K, S, PH, PW, Q, vec, D):
             L.append("add.u32 wa, wa, %%%d;" % ridx)
     L += tail("tfull")
     if D > 0:
-        # FAR: dispatching record r+1 from case r; p = &rec[r+2]; abs(r+1) in rec[r]
-        L += ["LFAR:", "ld.shared.b32 ab, [%%%d+%d];" % (pidx, -2 * RS + 8), "brx.idx.uni ab, tfull;"]
+        # FAR: dispatching record r+1 from case r; p = &rec[r+2] (depth 1) or
+        # &rec[r+3] (depth 2); abs(r+1) is in rec[r]
+        L += ["LFAR:", "ld.shared.b32 ab, [%%%d+%d];" % (pidx, -(3 if depth == 2 else 2) * RS + 8), "brx.idx.uni ab, tfull;"]
     L += ["LEND:", "}"]
     body = "\n".join('      "%s\\n"' % l for l in L)
     outs = ", ".join('"+f"(acc[%d])' % i for i in range(nacc)) + ", " + \
@@ -604,7 +614,8 @@ def main(outdir):
         full_row, rel, link = "r" in sfx, "x" in sfx, "n" in sfx
         vec = (PW * S) % 4 == 0 or full_row
         if link:
-            body, outs, ins = chunk_loop_link(K, S, PH, PW, Q, vec=vec, D=REL_D if rel else 0)
+            body, outs, ins = chunk_loop_link(K, S, PH, PW, Q, vec=vec, D=REL_D if rel else 0,
+                                              depth=2 if "2" in sfx else 1)
         elif rel:
             body, outs, ins = chunk_loop_rel(K, S, PH, PW, Q, vec=vec, D=REL_D)
         else:
