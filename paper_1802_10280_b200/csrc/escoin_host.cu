@@ -125,7 +125,47 @@ int window_conflicts(const TiledVariant& v, const Tiling& t, int CC) {
 }
 
 // All feasible tilings of variant v at channel chunk CC, with modelled cost.
+// Mode 4 (1x1 row blocks, sconv_1x1.cuh): candidates over WP at chunk CC.
+// plane = TP (pixels per CTA tile, one slab row per channel).
+bool choose_tiling_1x1(const TiledVariant& v, const escoin_csr* h, int CC, std::vector<Tiling>* cands) {
+  if (h->K != 1 || h->stride != 1 || h->pad != 0) return false;
+  const int R = v.Q, V = v.PW, HW = h->H * h->W;
+  const double dens = h->nnz / (double(h->M) * h->C);
+  const double u = 1.0 - std::pow(1.0 - dens, R);  // fraction of channels a warp visits
+  const int G = ceil_div(h->M, R);
+  bool found = false;
+  for (int WP = 1; WP <= 8; WP *= 2) {
+    Tiling t{};
+    t.WM = 8 / WP;
+    t.WP = WP;
+    t.NB = 1;
+    t.plane = 32 * V * WP;  // TP
+    const int TP = t.plane;
+    if (2.0 * 4.0 * CC * TP > 110.0 * 1024 * 0.85) continue;
+    if (TP / ((HW % 4 == 0) ? 4 : 1) > 4 * kTiledThreads) continue;  // staging units per thread (kMaxQ)
+    const int B = ceil_div(G, t.WM);
+    const double warp_util = double(G) / (B * t.WM);
+    const double ntiles = std::ceil(128.0 * HW / TP);
+    const double pix_util = 128.0 * HW / (ntiles * TP);
+    const double waves = ntiles * B / (148.0 * v.min_blocks);
+    const double wave_eff = waves / std::ceil(waves);
+    // issue slots per input channel and lane: visited records x (FFMAs + loads)
+    // + staging (TP/256 16-byte copies per channel, ~8 slots each)
+    // mode 4 visits u*C channels with R*V FFMAs each; mode 5 visits every
+    // nonzero once (V FFMAs + V/4 LDS.128 that cost as much as the FFMAs)
+    const double compute = v.mode == 5 ? dens * R * (2.0 * V + 4) : u * (R * V + 2.0 * V / 4 + 8);
+    const double staging = (HW % 4 == 0 ? 8.0 / 4 : 8.0) * TP / kTiledThreads;
+    t.cost = (compute + staging) / (dens * R * V * pix_util * warp_util * wave_eff);
+    if (std::getenv("ESCOIN_DEBUG_TILING"))
+      fprintf(stderr, "tiling %s CC=%d WP=%d TP=%d cost=%.3f\n", v.name, CC, WP, TP, t.cost);
+    cands->push_back(t);
+    found = true;
+  }
+  return found;
+}
+
 bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vector<Tiling>* cands) {
+  if (v.mode >= 4) return choose_tiling_1x1(v, h, CC, cands);
   const double slab_budget = (v.min_blocks > 1 ? 110.0 : 220.0) * 1024 * 0.85;  // leave room for records
   const int E = h->E, F = h->F;
   const int PR = ceil_div(E, v.PH), PC = ceil_div(F, v.PW);
@@ -245,7 +285,94 @@ struct DS6 {
   int max_block = 0;
 };
 
+// Mode 4 streams: per (m-block, chunk, warp) a header {count} and one record
+// per input channel where any of the warp's R rows has a nonzero:
+// {byte offset of the channel's slab row, w[0..R-1]} (absent weights +0.0f),
+// padded to 16-byte units.  Ascending c == the CSR order of every row.
+void build_ds_1x1(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int TP, DS6* out) {
+  const int R = v.Q, M = h->M, C = h->C;
+  const int G = ceil_div(M, R), B = ceil_div(G, WM), NK = ceil_div(C, CC);
+  const int RS2 = 2 * ((1 + R + 3) / 4);  // int2 units per record
+  const int64_t HW = int64_t(h->H) * h->W;
+  std::vector<float> wd(size_t(M) * C, 0.0f);
+  std::vector<unsigned char> nz(size_t(M) * C, 0);
+  for (int m = 0; m < M; ++m)
+    for (int64_t j = h->rowptr[m]; j < h->rowptr[m + 1]; ++j) {
+      const int c = int(h->colidx[j] / HW);
+      wd[size_t(m) * C + c] = h->value[j];
+      nz[size_t(m) * C + c] = 1;
+    }
+  out->recs.clear();
+  out->sched.clear();
+  out->sched_off.assign(1, 0);
+  out->max_block = 0;
+  std::vector<int> woff(WM);
+  for (int b = 0; b < B; ++b) {
+    for (int k = 0; k < NK; ++k) {
+      const int start = int(out->recs.size());
+      int total = 0;
+      for (int wm = 0; wm < WM; ++wm) {
+        woff[wm] = int(out->recs.size()) - start;
+        const int g = b * WM + wm;
+        if (v.mode == 5) {
+          // header: R counts (16-byte padded); then row by row {byte offset, w}
+          const size_t hdr = out->recs.size();
+          const int nh2 = 2 * ((R + 3) / 4);
+          for (int i = 0; i < nh2; ++i) out->recs.push_back(make_int2(0, 0));
+          for (int r = 0; r < R; ++r) {
+            const int m = g * R + r;
+            int cnt = 0;
+            for (int cl = 0; cl < CC && g < G && m < M; ++cl) {
+              const int c = k * CC + cl;
+              if (c >= C) break;
+              if (!nz[size_t(m) * C + c]) continue;
+              int wb;
+              std::memcpy(&wb, &wd[size_t(m) * C + c], 4);
+              out->recs.push_back(make_int2(cl * TP * 4, wb));
+              ++cnt;
+            }
+            reinterpret_cast<int*>(&out->recs[hdr])[r] = cnt;
+            total += cnt;
+          }
+          if (out->recs.size() & 1) out->recs.push_back(make_int2(0, 0));
+          continue;
+        }
+        const size_t hdr = out->recs.size();
+        out->recs.push_back(make_int2(0, 0));
+        out->recs.push_back(make_int2(0, 0));
+        int cnt = 0;
+        for (int cl = 0; cl < CC && g < G; ++cl) {
+          const int c = k * CC + cl;
+          if (c >= C) break;
+          bool any = false;
+          for (int r = 0; r < R && g * R + r < M; ++r) any |= nz[size_t(g * R + r) * C + c] != 0;
+          if (!any) continue;
+          std::vector<int> rec(RS2 * 2, 0);
+          rec[0] = cl * TP * 4;
+          for (int r = 0; r < R && g * R + r < M; ++r) std::memcpy(&rec[1 + r], &wd[size_t(g * R + r) * C + c], 4);
+          for (int i = 0; i < RS2; ++i) out->recs.push_back(make_int2(rec[2 * i], rec[2 * i + 1]));
+          ++cnt;
+        }
+        out->recs[hdr].x = cnt;
+        total += cnt;
+      }
+      if (total == 0) {  // chunk inactive for this m-block
+        out->recs.resize(start);
+        continue;
+      }
+      const int count = int(out->recs.size()) - start;
+      out->max_block = std::max(out->max_block, count);
+      out->sched.push_back(k);
+      out->sched.push_back(start);
+      out->sched.push_back(count);
+      for (int wm = 0; wm < WM; ++wm) out->sched.push_back(woff[wm]);
+    }
+    out->sched_off.push_back(int(out->sched.size() / (3 + WM)));
+  }
+}
+
 void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int plane, DS6* out) {
+  if (v.mode >= 4) return build_ds_1x1(h, v, WM, CC, plane, out);
   const int Q = v.Q, K = h->K;
   const int G = ceil_div(h->M, Q), B = ceil_div(G, WM), NK = ceil_div(h->C, CC);
   const int64_t HpWp = int64_t(h->H + 2 * h->pad) * (h->W + 2 * h->pad);
@@ -532,7 +659,9 @@ int prepare_tiled(escoin_csr* h, int vi, int rank, cudaStream_t s) {
   a.SCs = t.SCs;
   a.plane = t.plane;
   a.CC = CC;
-  a.tiles_r = ceil_div(t.PR, t.TR);
+  a.tiles_r = v.mode >= 4 ? 1 : ceil_div(t.PR, t.TR);
+  a.TP = t.plane;
+  a.vec16 = (h->H * h->W) % 4 == 0 ? 1 : 0;
   a.B = int(ds.sched_off.size()) - 1;
   a.smem_bytes = int(smem);
   a.recs = h->d_recs;
@@ -831,7 +960,10 @@ int escoin_sconv_forward(int N, int C, int H, int W, int M, int K, int stride, i
       a.PR = ceil_div(mosaic_rows(h, a.mos, N), tv[h->kernel - 1].PH);
       a.tiles_r = ceil_div(a.PR, a.TR);
     }
-    a.ntiles = a.mos ? a.tiles_r : a.flat ? ceil_div(N * a.PR, a.WP * 32) : ceil_div(N, a.NB * a.IP) * a.tiles_r;
+    if (tv[h->kernel - 1].mode >= 4)
+      a.ntiles = int((int64_t(N) * H * W + a.TP - 1) / a.TP);
+    else
+      a.ntiles = a.mos ? a.tiles_r : a.flat ? ceil_div(N * a.PR, a.WP * 32) : ceil_div(N, a.NB * a.IP) * a.tiles_r;
     a.debug = g_debug_kernel;
     if (a.ntiles > 65535) return ESCOIN_ERR_OVERFLOW;
     rc = tv[h->kernel - 1].launch(a, s);

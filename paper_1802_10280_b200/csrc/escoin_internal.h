@@ -29,6 +29,7 @@ struct TiledArgs {
   int mos;              // > 0: mosaic tiling — the batch is one super-image with `mos` images per
                         // super-row, periods H+pad / W+pad (shared zero separators); NB = 1
   int SR, SCs, plane;   // staged slab rows, row stride (words), plane stride (words)
+  int TP, vec16;        // mode 4 (1x1): pixels per CTA tile (flat over the batch); HW % 4 == 0
   int CC;               // input channels per chunk
   int tiles_r;          // ceil(PR / TR)
   int B, ntiles;        // grid: m-blocks x pixel tiles
@@ -49,7 +50,7 @@ struct TiledVariant {
   const char* name;
   int K, S, PH, PW, Q;
   int min_blocks;  // CTAs per SM the kernel is compiled for (__launch_bounds__)
-  int mode;        // 0: per-record brx dispatch; 1: dense-bucket mask sweep; 2/3: FFMA2
+  int mode;        // 0: per-record brx dispatch; 1: dense-bucket mask sweep; 2/3: FFMA2; 4: 1x1 row blocks
   int full_row;    // patch spans the whole output row (PC must be 1): vector window loads, flat tiling
   int rel_d;       // > 0: 16-byte records with predecessor-relative dispatch indices (chunk_loop_rel)
   int link;        // 1: linked records {idx(next), payload(self)} behind a header (chunk_loop_link)

@@ -506,6 +506,43 @@ int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
 }}  // namespace escoin
 """
 
+# 1x1 row-block variants (mode 4, sconv_1x1.cuh): name, R rows per warp, V pixels per lane
+VARIANTS_1X1 = [
+    ("d1_r4_v8", 4, 8),
+    ("d1_r4_v4", 4, 4),
+    ("d1_r3_v8", 3, 8),
+    ("d1_r2_v8", 2, 8),
+    ("d1_r6_v8", 6, 8),
+    ("d1_r8_v4", 8, 4),
+    ("d1_r4_v16", 4, 16),
+    ("s1_r4_v8", 4, 8),
+    ("s1_r8_v8", 8, 8),
+    ("s1_r4_v4", 4, 4),
+    ("s1_r8_v4", 8, 4),
+    ("s1_r2_v16", 2, 16),
+    ("s1_r4_v16", 4, 16),
+    ("s1_r2_v4", 2, 4),
+    ("s1_r1_v4", 1, 4),
+    ("s1_r1_v8", 1, 8),
+    ("s1_r2_v2", 2, 2),
+    ("s1_r4_v2", 4, 2),
+    ("s1_r2_v1", 2, 1),
+    ("s1_r8_v2", 8, 2),
+]
+
+TEMPLATE_1X1 = """// GENERATED by gen_sconv.py — do not edit.
+// Variant {name}: 1x1 {kind}, R={R} rows per warp, V={V} pixels per lane.
+#include "sconv_1x1.cuh"
+
+namespace escoin {{
+
+int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
+  return launch_1x1<{R}, {V}, {MINB}, {TAG}, {SP}>(a, s);
+}}
+
+}}  // namespace escoin
+"""
+
 VARIANTS_F2 = [
     ("f3s1_q1_4x4", 3, 1, 4, 4, 1),
     ("f3s1_q4_4x4", 3, 1, 4, 4, 4),
@@ -653,6 +690,15 @@ def main(outdir):
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
         table.append((name, K, S, PH, PW, Q, mb, 3, 0, 0, 0))
+    for name, R, V in VARIANTS_1X1:
+        mb = 2 if R * V <= 64 else 1
+        sp = 1 if name.startswith("s1") else 0
+        src = TEMPLATE_1X1.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, R=R, V=V, MINB=mb, SP=sp,
+                                  kind="exact row lists" if sp else "row blocks")
+        path = os.path.join(outdir, "variant_%s.cu" % name)
+        if not os.path.exists(path) or open(path).read() != src:
+            open(path, "w").write(src)
+        table.append((name, 1, 1, 1, V, R, mb, 5 if sp else 4, 0, 0, 0))
     keep = set("variant_%s.cu" % t[0] for t in table)
     for f in os.listdir(outdir):
         if f.startswith("variant_") and f.endswith(".cu") and f not in keep:

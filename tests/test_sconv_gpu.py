@@ -90,6 +90,7 @@ GRID = [  # N, C, H, W, M, K, stride, pad, density
     (2, 4, 16, 16, 6, 1, 2, 0, 0.5), (1, 3, 11, 11, 4, 5, 2, 0, 0.6), (5, 2, 5, 6, 3, 3, 1, 0, 1.0),
     (2, 33, 14, 14, 31, 3, 1, 1, 0.1), (1, 4, 8, 8, 70, 3, 1, 2, 0.2), (2, 8, 32, 30, 10, 5, 1, 2, 0.1),
     (1, 1, 4, 4, 1, 3, 1, 1, 1.0), (3, 18, 6, 6, 29, 1, 1, 0, 0.25),
+    (3, 37, 7, 7, 26, 1, 1, 0, 0.2), (2, 70, 14, 14, 45, 1, 1, 0, 0.2), (1, 9, 5, 3, 7, 1, 1, 0, 0.5),
 ]
 
 
