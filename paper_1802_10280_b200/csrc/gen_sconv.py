@@ -79,6 +79,9 @@ VARIANTS = [
     ("t1s1_q6_4x4", 1, 1, 4, 4, 6),
     ("t1s1_q6_4x4_s", 1, 1, 4, 4, 6),
     ("t3s2_q4_2x4", 3, 2, 2, 4, 4),
+    ("t3s2_q4_2x4_nx", 3, 2, 2, 4, 4),
+    ("t3s2_q6_2x4_nx", 3, 2, 2, 4, 6),
+
 ]
 
 
