@@ -59,20 +59,37 @@ class LoweredConv:
 
 
 class CudnnConv:
-    """Dense cuDNN FP32 convolution (no TF32) — an extra reference point."""
+    """Dense cuDNN convolution — extra reference points (not the method):
+      precision "fp32": FP32 math, TF32 off (same precision as the sparse path);
+      precision "tf32": TF32 tensor cores (tcgen05 on B200; ~1e-3 relative error);
+      precision "bf16": BF16 tensor cores, channels-last, activations converted
+                        to BF16 once outside the timed region (a BF16 network
+                        would carry BF16 activations), output back to FP32.
+    """
 
-    def __init__(self, layer, w_dense: np.ndarray, bias: np.ndarray, device):
-        torch.backends.cudnn.allow_tf32 = False
+    def __init__(self, layer, w_dense: np.ndarray, bias: np.ndarray, device, precision: str = "fp32"):
+        self.precision = precision
         L = layer
         g = L.groups
         Mg, Cg = L.M // g, L.C // g
         wg = np.concatenate([w_dense[i * Mg:(i + 1) * Mg, i * Cg:(i + 1) * Cg] for i in range(g)], 0)
         self.w = torch.from_numpy(np.ascontiguousarray(wg)).to(device)
         self.b = torch.from_numpy(bias).to(device)
+        if precision == "bf16":
+            self.w = self.w.to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+            self.b = self.b.to(torch.bfloat16)
+        self.xc = None
         self.L = L
 
     def __call__(self, x, out):
         L = self.L
-        y = torch.nn.functional.conv2d(x, self.w, self.b, stride=L.stride, padding=L.pad, groups=L.groups)
+        torch.backends.cudnn.allow_tf32 = self.precision == "tf32"
+        xin = x
+        if self.precision == "bf16":
+            if self.xc is None or self.xc[0] is not x:
+                self.xc = (x, x.to(torch.bfloat16).contiguous(memory_format=torch.channels_last))
+            xin = self.xc[1]
+        y = torch.nn.functional.conv2d(xin, self.w, self.b, stride=L.stride, padding=L.pad, groups=L.groups)
         out.copy_(torch.relu_(y))
+        torch.backends.cudnn.allow_tf32 = False
         return out

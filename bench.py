@@ -438,25 +438,40 @@ def run_baselines(torch, escoin, runs, flush, stream, args, sconv_value):
         return float(np.median(tot))
 
     B = runs[0].x.shape[0]
-    for mode in ["cublas", "cusparse", "cudnn"]:
+    names = {"cublas": "im2col+cublas_sgemm", "cusparse": "im2col+cusparse_spmm", "cudnn": "cudnn_fp32_dense",
+             "cudnn_tf32": "cudnn_tf32_dense_tensorcore", "cudnn_bf16": "cudnn_bf16_dense_tensorcore"}
+    for mode in ["cublas", "cusparse", "cudnn", "cudnn_tf32", "cudnn_bf16"]:
         per = {}
         try:
             for r in runs:
-                if mode == "cudnn":
-                    op = bl.CudnnConv(r.L, r.w_dense, r.bias.cpu().numpy(), r.x.device)
+                if mode.startswith("cudnn"):
+                    op = bl.CudnnConv(r.L, r.w_dense, r.bias.cpu().numpy(), r.x.device,
+                                      {"cudnn": "fp32", "cudnn_tf32": "tf32", "cudnn_bf16": "bf16"}[mode])
                 else:
                     op = bl.LoweredConv(r.L, r.w_dense, r.bias.cpu().numpy(), r.x.device, mode)
                 y = torch.empty_like(r.out)
                 per[r.L.name] = time_fn(lambda: op(r.x, y))
                 del op, y
             tot = sum(per.values())
-            out[{"cublas": "im2col+cublas_sgemm", "cusparse": "im2col+cusparse_spmm",
-                 "cudnn": "cudnn_fp32_dense"}[mode]] = {
+            out[names[mode]] = {
                 "images_per_s": B / (tot / 1e3), "ms_per_layer": {k: round(v, 4) for k, v in per.items()},
                 "escoin_speedup": round(sconv_value / (B / (tot / 1e3)), 3)}
         except Exception as e:  # report, do not hide
             out[mode] = {"error": repr(e)[:300]}
         torch.cuda.empty_cache()
+    # our own dense tcgen05 implicit GEMM (the north_star comparison point), TF32 and 3xTF32
+    for nsplit, key in [(1, "dense_tcgen05_tf32"), (3, "dense_tcgen05_3xtf32")]:
+        per = {}
+        for r in runs:
+            L = r.L
+            wd = torch.from_numpy(np.ascontiguousarray(r.w_dense)).to(r.x.device)
+            y = torch.empty_like(r.out)
+            per[L.name] = time_fn(lambda: escoin.bench_dense_tc_forward(wd, r.x, r.bias, L.stride, L.pad, True,
+                                                                        nsplit, out=y, stream=s))
+            del wd, y
+        tot = sum(per.values())
+        out[key] = {"images_per_s": B / (tot / 1e3), "ms_per_layer": {k: round(v, 4) for k, v in per.items()},
+                    "escoin_speedup": round(sconv_value / (B / (tot / 1e3)), 3)}
     # the paper's Pascal-era mapping (variant 0) on B200, as an ablation
     per = {}
     for r in runs:

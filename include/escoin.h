@@ -160,8 +160,8 @@ int escoin_csr_get_kernel(const escoin_csr* csr, int* id);
 /* Measured kernel customization (§3.4 P:563-564 "the optimization space we
  * explore includes the grid shape and thread block size"): time every
  * compiled variant that accepts the handle's (K, stride) — including the
- * paper mapping — and, per variant, its best three modelled tilings (CTA
- * shape, channel chunk), on the caller's buffers (same meaning as
+ * paper mapping — and, per variant, its best four modelled tilings (CTA
+ * shape, mosaic width, channel chunk), on the caller's buffers (same meaning as
  * escoin_sconv_forward; `out` is overwritten), `reps` timed forwards each
  * after one warm-up, and keep the fastest.  Synchronous on cuda_stream.
  * *best_id (may be NULL) receives the chosen variant, *best_ms its mean time.
@@ -169,6 +169,19 @@ int escoin_csr_get_kernel(const escoin_csr* csr, int* id);
  * Errors: as escoin_sconv_forward, plus CUDA/ALLOC from the rebuilds. */
 int escoin_csr_autotune(escoin_csr* csr, int N, const float* in, float* out, const float* bias, int relu,
                         int reps, void* cuda_stream, int* best_id, float* best_ms);
+
+/* ---- Benchmark-only comparison point (NOT the method; SURVEY 8(b) "escoin_bench_*",
+ * north_star: "a dense tcgen05 implicit-GEMM is kept only as a measured comparison point").
+ * Dense convolution of the pruned weights INCLUDING their zeros on the 5th-generation
+ * tensor cores: out = act(conv(in, w) + bias), implicit im2col, virtual padding.
+ *   w     device fp32 [M][C][K][K] dense (block-diagonal expanded for grouped layers);
+ *   in    device fp32 [N][C][H][W]; out device fp32 [N][M][E][F]; bias device [M] or NULL.
+ *   nsplit 1: TF32 operands (~1e-3 relative error; NOT within the method's tolerance);
+ *          3: 3xTF32 split (hi*hi + hi*lo + lo*hi), FP32-level accuracy.
+ * Asynchronous on cuda_stream, no allocation.  Errors: NULL, SHAPE, UNSUPPORTED (nsplit), CUDA. */
+int escoin_bench_dense_tc_forward(int N, int C, int H, int W, int M, int K, int stride, int pad, const float* w,
+                                  const float* in, float* out, const float* bias, int relu, int nsplit,
+                                  void* cuda_stream);
 
 const char* escoin_status_string(int status);
 /* Library version string, e.g. "escoin-b200 0.1 sm_100a". */

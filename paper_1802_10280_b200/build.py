@@ -64,7 +64,7 @@ def build(jobs: int | None = None, verbose: bool = False) -> str:
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         glob.glob(os.path.join(INCLUDE, "*.h")) + [os.path.join(GEN, "variants_table.inc")]
     core = [os.path.join(CSRC, "escoin_host.cu"), os.path.join(CSRC, "sconv_paper.cu"),
-            os.path.join(CSRC, "stretch_device.cu")]
+            os.path.join(CSRC, "stretch_device.cu"), os.path.join(CSRC, "dense_tc.cu")]
     srcs = core + variants
     jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 4))
     with ThreadPoolExecutor(jobs) as ex:

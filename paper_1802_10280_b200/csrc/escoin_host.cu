@@ -1091,6 +1091,18 @@ const char* escoin_status_string(int status) {
   }
 }
 
+int escoin_bench_dense_tc_forward(int N, int C, int H, int W, int M, int K, int stride, int pad, const float* w,
+                                  const float* in, float* out, const float* bias, int relu, int nsplit,
+                                  void* cuda_stream) {
+  if (!w || !in || !out) return ESCOIN_ERR_NULL;
+  if (N < 1 || C < 1 || H < 1 || W < 1 || M < 1 || K < 1 || stride < 1 || pad < 0) return ESCOIN_ERR_SHAPE;
+  if (H + 2 * pad < K || W + 2 * pad < K) return ESCOIN_ERR_SHAPE;
+  if (nsplit != 1 && nsplit != 3) return ESCOIN_ERR_UNSUPPORTED;
+  const int rc = launch_dense_tc(in, w, bias, out, N, C, H, W, M, K, stride, pad, relu ? 1 : 0, nsplit,
+                                 static_cast<cudaStream_t>(cuda_stream));
+  return rc == 0 ? ESCOIN_OK : ESCOIN_ERR_CUDA;
+}
+
 const char* escoin_version(void) { return "escoin-b200 0.1 sm_100a"; }
 
 /* Internal (not in escoin.h): host-only plan of tiled variant `id` for tests.

@@ -64,6 +64,10 @@ int launch_paper(const int* rowptr, const int* colidx, const float* value, const
 
 const TiledVariant* tiled_variants(int* count);
 
+// Dense tcgen05 implicit-GEMM comparison point (dense_tc.cu); nsplit 1 = TF32, 3 = 3xTF32.
+int launch_dense_tc(const float* in, const float* w, const float* bias, float* out, int N, int C, int H, int W,
+                    int M, int K, int S, int pad, int relu, int nsplit, cudaStream_t s);
+
 // Device weight stretching (stretch_device.cu).
 int launch_stretch_count(const float* w, int M, int64_t crs, int* cnt, cudaStream_t s);
 int launch_stretch_scan(const int* cnt, int M, int32_t* rowptr, cudaStream_t s);

@@ -31,6 +31,7 @@ EXPORTS = [
     "escoin_csr_wrap_device", "escoin_csr_free", "escoin_sconv_forward", "escoin_sconv_forward_hostio",
     "escoin_kernel_count", "escoin_kernel_info", "escoin_csr_set_kernel", "escoin_csr_get_kernel",
     "escoin_status_string", "escoin_version", "escoin_csr_autotune", "escoin_csr_stretch_device",
+    "escoin_bench_dense_tc_forward",
 ]
 
 
@@ -73,6 +74,7 @@ def lib():
             L.escoin_csr_set_kernel.argtypes = [vp, ci]
             L.escoin_csr_get_kernel.argtypes = [vp, ip]
             L.escoin_csr_autotune.argtypes = [vp, ci, vp, vp, vp, ci, ci, vp, ip, ctypes.POINTER(ctypes.c_float)]
+            L.escoin_bench_dense_tc_forward.argtypes = [ci] * 8 + [vp, vp, vp, vp, ci, ci, vp]
             L.escoin_status_string.argtypes = [ci]
             L.escoin_status_string.restype = ctypes.c_char_p
             L.escoin_version.restype = ctypes.c_char_p
@@ -214,6 +216,21 @@ def sconv_forward_hostio(N, C, H, W, M, K, stride, pad, csr: Csr, h_in, h_out, d
     _check("escoin_sconv_forward_hostio", lib().escoin_sconv_forward_hostio(
         N, C, H, W, M, K, stride, pad, csr.handle, _ptr(h_in), _ptr(h_out), _ptr(d_in), _ptr(d_out), _ptr(bias),
         1 if relu else 0, stream))
+
+
+def bench_dense_tc_forward(w, x, bias=None, stride=1, pad=0, relu=False, nsplit=3, out=None, stream=None):
+    """escoin_bench_dense_tc_forward — the dense tcgen05 comparison point (NOT the method).
+    w: torch CUDA fp32 [M][C][K][K] dense pruned weights; x: [N][C][H][W]."""
+    import torch
+    M, C, K, _ = w.shape
+    N, _, H, W = x.shape
+    E, F = out_dims(H, W, K, stride, pad)
+    if out is None:
+        out = torch.empty((N, M, E, F), dtype=torch.float32, device=x.device)
+    s = (stream if stream is not None else torch.cuda.current_stream(x.device)).cuda_stream
+    _check("escoin_bench_dense_tc_forward", lib().escoin_bench_dense_tc_forward(
+        N, C, H, W, M, K, stride, pad, _ptr(w), _ptr(x), _ptr(out), _ptr(bias), 1 if relu else 0, nsplit, s))
+    return out
 
 
 def out_dims(H, W, K, stride, pad):
