@@ -73,6 +73,8 @@ VARIANTS = [
     ("t5s1_q2_4x4_x", 5, 1, 4, 4, 2),
     ("t5s1_q2_4x4_nx", 5, 1, 4, 4, 2),
     ("t5s1_q1_4x4_nx", 5, 1, 4, 4, 1),
+    ("t5s1_q1_6x4_nx", 5, 1, 6, 4, 1),
+    ("t5s1_q1_5x4_nx", 5, 1, 5, 4, 1),
     ("t5s1_q2_3x4_nx", 5, 1, 3, 4, 2),
     ("t5s1_q2_3x4_x", 5, 1, 3, 4, 2),
     ("t5s1_q3_2x4_nx", 5, 1, 2, 4, 3),

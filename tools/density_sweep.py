@@ -1,7 +1,8 @@
 """BASELINE configs[4]: density sweep 5-100% on the AlexNet conv3 shape, batch 128.
 
 Direct sparse (escoin, autotuned) vs im2col+cuBLAS SGEMM vs im2col+cuSPARSE SpMM
-vs cuDNN FP32 dense; reports ms per layer and the crossover densities.
+vs cuDNN FP32 dense, plus the dense tensor-core references (cuDNN TF32 and our
+tcgen05 3xTF32 kernel); reports ms per layer and the crossover densities.
 Writes gpurun_out/density_sweep.json and gpurun_out/density_sweep.md.
 """
 import json
@@ -58,6 +59,11 @@ def main(batch=128):
             del op
         op = bl.CudnnConv(L, w, b_np, dev)
         r["cudnn_ms"] = timeit(lambda: op(x, y), flush)
+        op = bl.CudnnConv(L, w, b_np, dev, "tf32")
+        r["cudnn_tf32_ms"] = timeit(lambda: op(x, y), flush)
+        wd = torch.from_numpy(w).to(dev)
+        r["tcgen05_3xtf32_ms"] = timeit(lambda: escoin.bench_dense_tc_forward(wd, x, bias, L.stride, L.pad, True, 3,
+                                                                             out=y), flush)
         rows.append(r)
         print(json.dumps(r), flush=True)
         csr.free()
@@ -69,18 +75,23 @@ def main(batch=128):
     res = {"layer": "AlexNet conv3 shape (C=256, 13x13, M=384, 3x3, pad 1), batch %d" % batch, "rows": rows,
            "escoin_slower_than_cublas_from_density": crossover("cublas_ms"),
            "escoin_slower_than_cusparse_from_density": crossover("cusparse_ms"),
-           "escoin_slower_than_cudnn_from_density": crossover("cudnn_ms")}
+           "escoin_slower_than_cudnn_from_density": crossover("cudnn_ms"),
+           "escoin_slower_than_cudnn_tf32_from_density": crossover("cudnn_tf32_ms"),
+           "escoin_slower_than_tcgen05_3xtf32_from_density": crossover("tcgen05_3xtf32_ms")}
     json.dump(res, open("gpurun_out/density_sweep.json", "w"), indent=1)
     md = ["# Density sweep — %s" % res["layer"], "",
-          "| density | nnz | escoin ms (kernel) | escoin TFLOP/s | im2col+cuBLAS ms | im2col+cuSPARSE ms | cuDNN FP32 ms |",
-          "|---|---|---|---|---|---|---|"]
+          "| density | nnz | escoin ms (kernel) | escoin TFLOP/s | im2col+cuBLAS ms | im2col+cuSPARSE ms | cuDNN FP32 ms "
+          "| cuDNN TF32 ms | tcgen05 3xTF32 ms |",
+          "|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
-        md.append("| %.2f | %d | %.3f (%s) | %.2f | %.3f | %.3f | %.3f |" % (
+        md.append("| %.2f | %d | %.3f (%s) | %.2f | %.3f | %.3f | %.3f | %.3f | %.3f |" % (
             r["density"], r["nnz"], r["escoin_ms"], r["escoin_kernel"], r["escoin_tflops"], r["cublas_ms"],
-            r["cusparse_ms"], r["cudnn_ms"]))
-    md += ["", "escoin slower than cuBLAS from density %s, than cuSPARSE from %s, than cuDNN from %s." % (
-        res["escoin_slower_than_cublas_from_density"], res["escoin_slower_than_cusparse_from_density"],
-        res["escoin_slower_than_cudnn_from_density"])]
+            r["cusparse_ms"], r["cudnn_ms"], r["cudnn_tf32_ms"], r["tcgen05_3xtf32_ms"]))
+    md += ["", "escoin slower than cuBLAS from density %s, than cuSPARSE from %s, than cuDNN FP32 from %s, "
+           "than cuDNN TF32 from %s, than the tcgen05 3xTF32 kernel from %s (None = never)." % (
+               res["escoin_slower_than_cublas_from_density"], res["escoin_slower_than_cusparse_from_density"],
+               res["escoin_slower_than_cudnn_from_density"], res["escoin_slower_than_cudnn_tf32_from_density"],
+               res["escoin_slower_than_tcgen05_3xtf32_from_density"])]
     open("gpurun_out/density_sweep.md", "w").write("\n".join(md) + "\n")
 
 
