@@ -40,12 +40,8 @@ REL_D = 12  # "_x" variants: successor window of the per-case jump tables
 
 VARIANTS_MASK = [
     ("m3s1_q4_4x4", 3, 1, 4, 4, 4),
-    ("m3s1_q8_4x4", 3, 1, 4, 4, 8),
-    ("m3s1_q6_4x4", 3, 1, 4, 4, 6),
     ("m3s1_q4_1x13", 3, 1, 1, 13, 4),
     ("m5s1_q2_4x4", 5, 1, 4, 4, 2),
-    ("m5s1_q4_4x4", 5, 1, 4, 4, 4),
-    ("m1s1_q12_2x4", 1, 1, 2, 4, 12),
 ]
 # "_s": one shared dispatch site (one small jump table; pays a direct branch
 # and an exposed jump-table load per record) — better when Q*K*K is large.
@@ -56,34 +52,15 @@ VARIANTS = [
     ("t3s1_q4_4x4_n", 3, 1, 4, 4, 4),
     ("t3s1_q4_4x4_nx", 3, 1, 4, 4, 4),
     ("t3s1_q3_4x4_nx", 3, 1, 4, 4, 3),
-
-    ("t3s1_q5_4x4_x", 3, 1, 4, 4, 5),
     ("t3s1_q3_4x4_x", 3, 1, 4, 4, 3),
     ("t3s1_q2_4x4", 3, 1, 4, 4, 2),
     ("t3s1_q3_4x4", 3, 1, 4, 4, 3),
-    ("t3s1_q3_4x4_s", 3, 1, 4, 4, 3),
-    ("t3s1_q4_2x7", 3, 1, 2, 7, 4),
-    ("t3s1_q4_1x13_r", 3, 1, 1, 13, 4),
-    ("t3s1_q3_1x13_r", 3, 1, 1, 13, 3),
     ("t3s1_q4_1x13_rx", 3, 1, 1, 13, 4),
-    ("t3s1_q3_1x13_rx", 3, 1, 1, 13, 3),
-    ("t3s1_q5_4x4_s", 3, 1, 4, 4, 5),
     ("t5s1_q1_4x4", 5, 1, 4, 4, 1),
     ("t5s1_q2_4x4_s", 5, 1, 4, 4, 2),
-    ("t5s1_q2_4x4_x", 5, 1, 4, 4, 2),
     ("t5s1_q2_4x4_nx", 5, 1, 4, 4, 2),
     ("t5s1_q1_4x4_nx", 5, 1, 4, 4, 1),
-    ("t5s1_q1_6x4_nx", 5, 1, 6, 4, 1),
     ("t5s1_q1_5x4_nx", 5, 1, 5, 4, 1),
-    ("t5s1_q2_3x4_nx", 5, 1, 3, 4, 2),
-    ("t5s1_q2_3x4_x", 5, 1, 3, 4, 2),
-    ("t5s1_q3_2x4_nx", 5, 1, 2, 4, 3),
-    ("t3s1_q4_3x4_nx", 3, 1, 3, 4, 4),
-
-    ("t5s1_q1_4x4_x", 5, 1, 4, 4, 1),
-    ("t5s1_q2_4x4", 5, 1, 4, 4, 2),
-    ("t1s1_q6_4x4", 1, 1, 4, 4, 6),
-    ("t1s1_q6_4x4_s", 1, 1, 4, 4, 6),
     ("t3s2_q4_2x4", 3, 2, 2, 4, 4),
     ("t3s2_q4_2x4_nx", 3, 2, 2, 4, 4),
     ("t3s2_q6_2x4_nx", 3, 2, 2, 4, 6),
@@ -481,9 +458,6 @@ int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
 
 VARIANTS_P3 = [
     ("p3s1_q4_2x4", 3, 1, 2, 4, 4),
-    ("p3s1_q3_2x4", 3, 1, 2, 4, 3),
-    ("p3s1_q2_4x4", 3, 1, 4, 4, 2),
-    ("p5s1_q1_2x4", 5, 1, 2, 4, 1),
 ]
 
 
@@ -523,7 +497,6 @@ VARIANTS_1X1 = [
     ("d1_r2_v8", 2, 8),
     ("d1_r6_v8", 6, 8),
     ("d1_r8_v4", 8, 4),
-    ("d1_r4_v16", 4, 16),
     ("s1_r4_v8", 4, 8),
     ("s1_r8_v8", 8, 8),
     ("s1_r4_v4", 4, 4),
@@ -531,7 +504,6 @@ VARIANTS_1X1 = [
     ("s1_r2_v16", 2, 16),
     ("s1_r4_v16", 4, 16),
     ("s1_r2_v4", 2, 4),
-    ("s1_r1_v4", 1, 4),
     ("s1_r1_v8", 1, 8),
     ("s1_r2_v2", 2, 2),
     ("s1_r4_v2", 4, 2),
@@ -554,11 +526,8 @@ int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
 
 VARIANTS_F2 = [
     ("f3s1_q1_4x4", 3, 1, 4, 4, 1),
-    ("f3s1_q4_4x4", 3, 1, 4, 4, 4),
     ("f3s1_q3_4x4", 3, 1, 4, 4, 3),
-    ("f3s1_q2_4x4", 3, 1, 4, 4, 2),
     ("f5s1_q2_4x4", 5, 1, 4, 4, 2),
-    ("f5s1_q1_4x4", 5, 1, 4, 4, 1),
 ]
 
 
