@@ -165,7 +165,8 @@ bool choose_tiling_1x1(const TiledVariant& v, const escoin_csr* h, int CC, std::
 }
 
 bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vector<Tiling>* cands) {
-  if (v.mode >= 4) return choose_tiling_1x1(v, h, CC, cands);
+  if (v.mode == 4 || v.mode == 5) return choose_tiling_1x1(v, h, CC, cands);
+  if (v.mode == 6 && (v.S != 1 || v.PW != 1)) return false;
   const double slab_budget = (v.min_blocks > 1 ? 110.0 : 220.0) * 1024 * 0.85;  // leave room for records
   const int E = h->E, F = h->F;
   const int PR = ceil_div(E, v.PH), PC = ceil_div(F, v.PW);
@@ -194,6 +195,7 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
     const int WM = 8 / WP;
     const int slots = 32 * WP;
     if (PCs > slots) continue;
+    if (v.mode == 6 && PCs > 32) continue;  // tap records: one 32-column slab row block per CTA
     Tiling t{};
     t.WM = WM;
     t.WP = WP;
@@ -221,8 +223,14 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
     const int SC4 = (t.SC + 3) & ~3;
     if (t.SR * h->W > kMaxStagePos * kTiledThreads) continue;  // interior floats per staged plane
     // pick row/plane padding that minimises LDS.128 bank-group conflicts
+    // (mode 6: fixed row stride 32 + K - 1, lanes read consecutive columns)
     int bestc = 1 << 30;
-    for (int sp = 0; sp < 8; ++sp) {
+    if (v.mode == 6) {
+      bestc = 1;
+      t.SCs = 32 + v.K - 1;
+      t.plane = (t.SR * t.SCs + 3) & ~3;
+    }
+    for (int sp = 0; sp < 8 && v.mode != 6; ++sp) {
       const int SCs = SC4 + 4 * sp;
       for (int pp = 0; pp < 8; ++pp) {
         Tiling u = t;
@@ -251,7 +259,11 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
     const bool vec = ((v.PW * v.S) % 4 == 0) || PC == 1;
     const double win = vec ? XH * ((XW + 3) / 4) * 4.0 * (bestc > 1 ? bestc : 1) : XH * XW;
     const double work = v.mode >= 2 ? P / 2.0 * IP + 10 : P + 9;  // issue slots per record
-    const double compute = (v.Q * dens * v.K * v.K * (work + lat) + win + 30) / IP;
+    // mode 6: a record per tap where any of the Q channels has a nonzero,
+    // Q*P FFMAs + P loads each, no dispatch, no window
+    const double u6 = 1.0 - std::pow(1.0 - dens, v.Q);
+    const double compute = v.mode == 6 ? v.K * v.K * u6 * (v.Q * P + P + 6) + 10
+                                       : (v.Q * dens * v.K * v.K * (work + lat) + win + 30) / IP;
     const double staging = mos ? 5.0 * t.SR * mos * h->W / kTiledThreads
                                : 5.0 * t.NB * IP * std::min(t.SR, h->H) * h->W / kTiledThreads / IP;
     // wave quantisation of the grid at the benchmark batch (128 images)
@@ -371,8 +383,81 @@ void build_ds_1x1(const escoin_csr* h, const TiledVariant& v, int WM, int CC, in
   }
 }
 
+// Mode 6 streams (tap records): per (m-block, chunk, warp) a 16-byte header
+// {count} and one record per tap (c, kh, kw) — ascending, i.e. CSR order —
+// where any of the warp's Q rows has a nonzero: {byte offset (c_local*plane +
+// kh*SCs + kw)*4 from the lane's window origin, w[0..Q-1]} (absent: +0.0f),
+// padded to 16-byte units.
+void build_ds_tap(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int plane, DS6* out) {
+  const int Q = v.Q, M = h->M, C = h->C, K = h->K, KK = K * K;
+  const int SCs = 32 + K - 1;
+  const int G = ceil_div(M, Q), B = ceil_div(G, WM), NK = ceil_div(C, CC);
+  const int RS2 = 2 * ((1 + Q + 3) / 4);
+  const int64_t HpWp = int64_t(h->H + 2 * h->pad) * (h->W + 2 * h->pad);
+  const int Wp = h->W + 2 * h->pad;
+  const size_t CKK = size_t(C) * KK;
+  std::vector<float> wd(size_t(M) * CKK, 0.0f);
+  std::vector<unsigned char> nz(size_t(M) * CKK, 0);
+  for (int m = 0; m < M; ++m)
+    for (int64_t j = h->rowptr[m]; j < h->rowptr[m + 1]; ++j) {
+      const int64_t off = h->colidx[j];
+      const int c = int(off / HpWp), rem = int(off - c * HpWp);
+      const size_t col = size_t(c) * KK + size_t(rem / Wp) * K + rem % Wp;
+      wd[size_t(m) * CKK + col] = h->value[j];
+      nz[size_t(m) * CKK + col] = 1;
+    }
+  out->recs.clear();
+  out->sched.clear();
+  out->sched_off.assign(1, 0);
+  out->max_block = 0;
+  std::vector<int> woff(WM), rec(RS2 * 2);
+  for (int b = 0; b < B; ++b) {
+    for (int k = 0; k < NK; ++k) {
+      const int start = int(out->recs.size());
+      int total = 0;
+      for (int wm = 0; wm < WM; ++wm) {
+        woff[wm] = int(out->recs.size()) - start;
+        const size_t hdr = out->recs.size();
+        out->recs.push_back(make_int2(0, 0));
+        out->recs.push_back(make_int2(0, 0));
+        const int g = b * WM + wm;
+        int cnt = 0;
+        for (int cl = 0; cl < CC && g < G; ++cl) {
+          const int c = k * CC + cl;
+          if (c >= C) break;
+          for (int tap = 0; tap < KK; ++tap) {
+            const size_t col = size_t(c) * KK + tap;
+            bool any = false;
+            for (int r = 0; r < Q && g * Q + r < M; ++r) any |= nz[size_t(g * Q + r) * CKK + col] != 0;
+            if (!any) continue;
+            std::fill(rec.begin(), rec.end(), 0);
+            rec[0] = (cl * plane + (tap / K) * SCs + tap % K) * 4;
+            for (int r = 0; r < Q && g * Q + r < M; ++r) std::memcpy(&rec[1 + r], &wd[size_t(g * Q + r) * CKK + col], 4);
+            for (int i = 0; i < RS2; ++i) out->recs.push_back(make_int2(rec[2 * i], rec[2 * i + 1]));
+            ++cnt;
+          }
+        }
+        out->recs[hdr].x = cnt;
+        total += cnt;
+      }
+      if (total == 0) {
+        out->recs.resize(start);
+        continue;
+      }
+      const int count = int(out->recs.size()) - start;
+      out->max_block = std::max(out->max_block, count);
+      out->sched.push_back(k);
+      out->sched.push_back(start);
+      out->sched.push_back(count);
+      for (int wm = 0; wm < WM; ++wm) out->sched.push_back(woff[wm]);
+    }
+    out->sched_off.push_back(int(out->sched.size() / (3 + WM)));
+  }
+}
+
 void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int plane, DS6* out) {
-  if (v.mode >= 4) return build_ds_1x1(h, v, WM, CC, plane, out);
+  if (v.mode == 4 || v.mode == 5) return build_ds_1x1(h, v, WM, CC, plane, out);
+  if (v.mode == 6) return build_ds_tap(h, v, WM, CC, plane, out);
   const int Q = v.Q, K = h->K;
   const int G = ceil_div(h->M, Q), B = ceil_div(G, WM), NK = ceil_div(h->C, CC);
   const int64_t HpWp = int64_t(h->H + 2 * h->pad) * (h->W + 2 * h->pad);
@@ -659,7 +744,7 @@ int prepare_tiled(escoin_csr* h, int vi, int rank, cudaStream_t s) {
   a.SCs = t.SCs;
   a.plane = t.plane;
   a.CC = CC;
-  a.tiles_r = v.mode >= 4 ? 1 : ceil_div(t.PR, t.TR);
+  a.tiles_r = (v.mode == 4 || v.mode == 5) ? 1 : ceil_div(t.PR, t.TR);
   a.TP = t.plane;
   a.vec16 = (h->H * h->W) % 4 == 0 ? 1 : 0;
   a.B = int(ds.sched_off.size()) - 1;
@@ -960,7 +1045,7 @@ int escoin_sconv_forward(int N, int C, int H, int W, int M, int K, int stride, i
       a.PR = ceil_div(mosaic_rows(h, a.mos, N), tv[h->kernel - 1].PH);
       a.tiles_r = ceil_div(a.PR, a.TR);
     }
-    if (tv[h->kernel - 1].mode >= 4)
+    if (tv[h->kernel - 1].mode == 4 || tv[h->kernel - 1].mode == 5)
       a.ntiles = int((int64_t(N) * H * W + a.TP - 1) / a.TP);
     else
       a.ntiles = a.mos ? a.tiles_r : a.flat ? ceil_div(N * a.PR, a.WP * 32) : ceil_div(N, a.NB * a.IP) * a.tiles_r;

@@ -524,6 +524,30 @@ int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
 }}  // namespace escoin
 """
 
+# Tap-record variants (mode 6, no dispatch): name, K, PH (rows per lane), Q
+VARIANTS_TAP = [
+    ("b3_q4_8x1", 3, 8, 4),
+    ("b3_q3_8x1", 3, 8, 3),
+    ("b3_q4_12x1", 3, 12, 4),
+    ("b3_q2_16x1", 3, 16, 2),
+    ("b3_q6_8x1", 3, 8, 6),
+    ("b5_q4_8x1", 5, 8, 4),
+    ("b5_q3_8x1", 5, 8, 3),
+]
+
+TEMPLATE_TAP = """// GENERATED by gen_sconv.py — do not edit.
+// Variant {name}: K={K} tap records (mode 6), column patches {PH}x1, Q={Q}.
+#include "sconv_tiled.cuh"
+
+namespace escoin {{
+
+int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
+  return launch_tiled<{K}, 1, {PH}, 1, {Q}, 2, 6, {TAG}>(a, s);
+}}
+
+}}  // namespace escoin
+"""
+
 VARIANTS_F2 = [
     ("f3s1_q1_4x4", 3, 1, 4, 4, 1),
     ("f3s1_q3_4x4", 3, 1, 4, 4, 3),
@@ -677,6 +701,12 @@ def main(outdir):
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
         table.append((name, 1, 1, 1, V, R, mb, 5 if sp else 4, 0, 0, 0))
+    for name, K, PH, Q in VARIANTS_TAP:
+        src = TEMPLATE_TAP.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, PH=PH, Q=Q)
+        path = os.path.join(outdir, "variant_%s.cu" % name)
+        if not os.path.exists(path) or open(path).read() != src:
+            open(path, "w").write(src)
+        table.append((name, K, 1, PH, 1, Q, 2, 6, 0, 0, 0))
     keep = set("variant_%s.cu" % t[0] for t in table)
     for f in os.listdir(outdir):
         if f.startswith("variant_") and f.endswith(".cu") and f not in keep:

@@ -291,6 +291,42 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
     } else if constexpr (MODE == 3) {
       unsigned p = smem_addr(ws);
       chunk_loop3<K, S, PH, PW, Q, TAG>(acc3, xw3, p, smem_addr(slab), 4u * a.SCs);
+    } else if constexpr (MODE == 6) {
+      // Tap records (no dispatch): {byte offset of tap (c, kh, kw) from the
+      // lane's window origin, w[0..Q-1]} for every tap where any of the warp's
+      // Q output channels has a nonzero (absent weights +0.0f: adds exact
+      // zeros, so each channel still accumulates exactly its CSR terms in
+      // ascending (c, kh, kw)).  Lanes own 32 consecutive output columns,
+      // each PH rows of one column: per tap, PH conflict-free scalar LDS
+      // (immediate row offsets, slab row stride SCS6) and Q*PH FFMAs.
+      static_assert(PW == 1 && S == 1, "tap-record mode: column patches, stride 1");
+      constexpr int SCS6 = 32 + K - 1;
+      constexpr int RS4 = (1 + Q + 3) / 4;
+      const int4* rp = reinterpret_cast<const int4*>(ws);
+      const int cnt = rp[0].x;
+      rp += 1;
+      const char* sb = reinterpret_cast<const char*>(slab);
+#pragma unroll 2
+      for (int i = 0; i < cnt; ++i) {
+        float w[RS4 * 4];
+#pragma unroll
+        for (int k = 0; k < RS4; ++k) {
+          const int4 t = rp[k];
+          w[4 * k + 0] = __int_as_float(t.x);
+          w[4 * k + 1] = __int_as_float(t.y);
+          w[4 * k + 2] = __int_as_float(t.z);
+          w[4 * k + 3] = __int_as_float(t.w);
+        }
+        rp += RS4;
+        const float* b = reinterpret_cast<const float*>(sb + __float_as_int(w[0]));
+        float xv[PH];
+#pragma unroll
+        for (int v = 0; v < PH; ++v) xv[v] = b[v * SCS6];
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+          for (int v = 0; v < PH; ++v) acc[q * P + v] = fmaf(w[1 + q], xv[v], acc[q * P + v]);
+      }
     } else {
       // warp stream: per bucket {c, 0, 0, 0} + Q*K*K weights (16-byte padded); c < 0 ends
       constexpr int NW4 = (Q * K * K + 3) / 4;
