@@ -166,7 +166,7 @@ bool choose_tiling_1x1(const TiledVariant& v, const escoin_csr* h, int CC, std::
 
 bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vector<Tiling>* cands) {
   if (v.mode == 4 || v.mode == 5) return choose_tiling_1x1(v, h, CC, cands);
-  if (v.mode == 6 && (v.S != 1 || v.PW != 1)) return false;
+  if (v.mode == 6 && v.PW != 1) return false;
   const double slab_budget = (v.min_blocks > 1 ? 110.0 : 220.0) * 1024 * 0.85;  // leave room for records
   const int E = h->E, F = h->F;
   const int PR = ceil_div(E, v.PH), PC = ceil_div(F, v.PW);
@@ -223,11 +223,11 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
     const int SC4 = (t.SC + 3) & ~3;
     if (t.SR * h->W > kMaxStagePos * kTiledThreads) continue;  // interior floats per staged plane
     // pick row/plane padding that minimises LDS.128 bank-group conflicts
-    // (mode 6: fixed row stride 32 + K - 1, lanes read consecutive columns)
+    // (mode 6: fixed row stride 31*S + K, lanes read consecutive columns)
     int bestc = 1 << 30;
     if (v.mode == 6) {
       bestc = 1;
-      t.SCs = 32 + v.K - 1;
+      t.SCs = 31 * v.S + v.K;
       t.plane = (t.SR * t.SCs + 3) & ~3;
     }
     for (int sp = 0; sp < 8 && v.mode != 6; ++sp) {
@@ -390,7 +390,7 @@ void build_ds_1x1(const escoin_csr* h, const TiledVariant& v, int WM, int CC, in
 // padded to 16-byte units.
 void build_ds_tap(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int plane, DS6* out) {
   const int Q = v.Q, M = h->M, C = h->C, K = h->K, KK = K * K;
-  const int SCs = 32 + K - 1;
+  const int SCs = 31 * h->stride + K;  // the kernel's slab row stride (sconv_tiled.cuh, MODE 6)
   const int G = ceil_div(M, Q), B = ceil_div(G, WM), NK = ceil_div(C, CC);
   const int RS2 = 2 * ((1 + Q + 3) / 4);
   const int64_t HpWp = int64_t(h->H + 2 * h->pad) * (h->W + 2 * h->pad);

@@ -525,24 +525,43 @@ int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
 """
 
 # Tap-record variants (mode 6, no dispatch): name, K, PH (rows per lane), Q
+# (stride 1; the "s2" entries below are stride 2)
 VARIANTS_TAP = [
     ("b3_q4_8x1", 3, 8, 4),
     ("b3_q3_8x1", 3, 8, 3),
     ("b3_q4_12x1", 3, 12, 4),
     ("b3_q2_16x1", 3, 16, 2),
     ("b3_q6_8x1", 3, 8, 6),
+    ("b3_q1_32x1", 3, 32, 1),
+    ("b3_q1_16x1", 3, 16, 1),
+    ("b3_q2_24x1", 3, 24, 2),
+    ("b5_q1_32x1", 5, 32, 1),
+    ("b5_q2_16x1", 5, 16, 2),
+    ("b5_q3_16x1", 5, 16, 3),
+    ("b5_q2_20x1", 5, 20, 2),
+    ("b5_q2_12x1", 5, 12, 2),
+    ("b3_q3_16x1", 3, 16, 3),
+    ("b3_q2_12x1", 3, 12, 2),
     ("b5_q4_8x1", 5, 8, 4),
     ("b5_q3_8x1", 5, 8, 3),
+    ("b3s2_q2_16x1", 3, 16, 2),
+    ("b3s2_q2_8x1", 3, 8, 2),
+    ("b3s2_q3_8x1", 3, 8, 3),
+    ("b3s2_q4_8x1", 3, 8, 4),
+    ("b3s2_q6_8x1", 3, 8, 6),
+    ("b3s2_q8_8x1", 3, 8, 8),
+    ("b3s2_q4_12x1", 3, 12, 4),
+    ("b3s2_q8_4x1", 3, 4, 8),
 ]
 
 TEMPLATE_TAP = """// GENERATED by gen_sconv.py — do not edit.
-// Variant {name}: K={K} tap records (mode 6), column patches {PH}x1, Q={Q}.
+// Variant {name}: K={K} stride={S} tap records (mode 6), column patches {PH}x1, Q={Q}.
 #include "sconv_tiled.cuh"
 
 namespace escoin {{
 
 int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
-  return launch_tiled<{K}, 1, {PH}, 1, {Q}, 2, 6, {TAG}>(a, s);
+  return launch_tiled<{K}, {S}, {PH}, 1, {Q}, 2, 6, {TAG}>(a, s);
 }}
 
 }}  // namespace escoin
@@ -702,11 +721,12 @@ def main(outdir):
             open(path, "w").write(src)
         table.append((name, 1, 1, 1, V, R, mb, 5 if sp else 4, 0, 0, 0))
     for name, K, PH, Q in VARIANTS_TAP:
-        src = TEMPLATE_TAP.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, PH=PH, Q=Q)
+        S = 2 if "s2" in name else 1
+        src = TEMPLATE_TAP.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, S=S, PH=PH, Q=Q)
         path = os.path.join(outdir, "variant_%s.cu" % name)
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
-        table.append((name, K, 1, PH, 1, Q, 2, 6, 0, 0, 0))
+        table.append((name, K, S, PH, 1, Q, 2, 6, 0, 0, 0))
     keep = set("variant_%s.cu" % t[0] for t in table)
     for f in os.listdir(outdir):
         if f.startswith("variant_") and f.endswith(".cu") and f not in keep:

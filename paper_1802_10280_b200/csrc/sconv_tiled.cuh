@@ -297,10 +297,11 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
       // Q output channels has a nonzero (absent weights +0.0f: adds exact
       // zeros, so each channel still accumulates exactly its CSR terms in
       // ascending (c, kh, kw)).  Lanes own 32 consecutive output columns,
-      // each PH rows of one column: per tap, PH conflict-free scalar LDS
-      // (immediate row offsets, slab row stride SCS6) and Q*PH FFMAs.
-      static_assert(PW == 1 && S == 1, "tap-record mode: column patches, stride 1");
-      constexpr int SCS6 = 32 + K - 1;
+      // each PH rows of one column: per tap, PH scalar LDS (conflict-free at
+      // stride 1, 2-way at stride 2; immediate row offsets, slab row stride
+      // SCS6) and Q*PH FFMAs.
+      static_assert(PW == 1, "tap-record mode: column patches");
+      constexpr int SCS6 = 31 * S + K;  // slab row stride: 32 output columns at stride S
       constexpr int RS4 = (1 + Q + 3) / 4;
       const int4* rp = reinterpret_cast<const int4*>(ws);
       const int cnt = rp[0].x;
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
         const float* b = reinterpret_cast<const float*>(sb + __float_as_int(w[0]));
         float xv[PH];
 #pragma unroll
-        for (int v = 0; v < PH; ++v) xv[v] = b[v * SCS6];
+        for (int v = 0; v < PH; ++v) xv[v] = b[v * S * SCS6];
 #pragma unroll
         for (int q = 0; q < Q; ++q)
 #pragma unroll
