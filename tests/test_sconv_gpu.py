@@ -286,6 +286,31 @@ def test_full_batch_sampled(wl, name):
     assert np.all(np.isfinite(out))
 
 
+@pytest.mark.parametrize("wl,name", [("alexnet", "conv2"), ("alexnet", "conv3"), ("resnet50_v15", "res4a_branch2b"),
+                                     ("googlenet_1x1", "inception_4e/1x1")])
+def test_full_batch_autotuned_sampled(wl, name):
+    # exactly the launch configuration bench.py times: N=128, the variant and
+    # tiling escoin_csr_autotune picks on these buffers; sampled outputs vs oracle
+    L = [l for l in workloads.workload(wl).layers if l.name == name][0]
+    x, w, b = layer_case(wl, L, 0, 128)
+    csr = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad).to_device(0)
+    dx, db = torch.from_numpy(x).cuda(), torch.from_numpy(b).cuda()
+    out = torch.empty((128, L.M, L.E, L.F), device="cuda")
+    csr.autotune(128, dx, out, db, True, 2, torch.cuda.current_stream().cuda_stream)
+    out = escoin.forward(csr, dx, bias=db, relu=True)
+    torch.cuda.synchronize()
+    got_all = out.cpu().numpy()
+    rng = np.random.default_rng(9)
+    npts = 3000
+    coords = np.stack([rng.integers(0, 128, npts), rng.integers(0, L.M, npts), rng.integers(0, L.E, npts),
+                       rng.integers(0, L.F, npts)], 1)
+    rp, ci, v = oracle.csr_stretch(w, L.H, L.W, L.stride, L.pad)
+    ref, scale = oracle.sconv_points(x, rp, ci, v, L.M, L.K, L.stride, L.pad, coords, bias=b, relu=True)
+    got = got_all[coords[:, 0], coords[:, 1], coords[:, 2], coords[:, 3]].astype(np.float64)
+    assert np.all(np.abs(got - ref) <= TOL * (scale + np.abs(b[coords[:, 1]]))), escoin.kernels()[csr.kernel()][1]
+    assert np.all(np.isfinite(got_all))
+
+
 # ------------------------------------------------------------------ ABI paths
 def test_wrap_device_and_hostio_match():
     L = workloads.TINY
