@@ -326,6 +326,7 @@ def main():
     step_ms = shard.max_over_ranks(step_ms_local, device)
     value = B * world / (step_ms / 1e3)
     layer_ms = per_layer.mean(0)
+    layer_ms_min, layer_ms_med = per_layer.min(0), np.median(per_layer, 0)
 
     # ---------------- e2e through the C-ABI with host buffers
     # Every step copies each layer's input from pinned host memory, runs the
@@ -381,8 +382,9 @@ def main():
     achieved = rd.flops / (layer_ms[dom] / 1e3) / 1e12
     traffic = load_traffic(args.workload).get(rd.L.name)
     layers_out = []
-    for r, ms in zip(runs, layer_ms):
-        layers_out.append({"layer": r.L.name, "ms": round(float(ms), 5), "kernel": r.kernel, "nnz": r.nnz,
+    for r, ms, mn, md in zip(runs, layer_ms, layer_ms_min, layer_ms_med):
+        layers_out.append({"layer": r.L.name, "ms": round(float(ms), 5), "ms_min": round(float(mn), 5),
+                           "ms_median": round(float(md), 5), "kernel": r.kernel, "nnz": r.nnz,
                            "gflop": round(r.flops / 1e9, 4),
                            "tflops": round(r.flops / (ms / 1e3) / 1e12, 3),
                            "frac_fp32": round(r.flops / (ms / 1e3) / 1e12 / peak_tf, 4),
