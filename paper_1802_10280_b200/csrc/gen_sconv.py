@@ -36,7 +36,7 @@ import zlib
 # mode "brx": per-record indirect dispatch; mode "mask": dense per-bucket
 # weight block swept in fixed (tap, q) order with warp-uniform forward
 # branches over the absent (zero) slots — no indirect branches at all.
-REL_D = 12  # "_x" variants: successor window of the per-case jump tables
+REL_D = 8  # "_x" variants: successor window of the per-case jump tables (measured: 8 > 6, 12, 18)
 
 VARIANTS_MASK = [
     ("m3s1_q4_4x4", 3, 1, 4, 4, 4),
@@ -670,12 +670,14 @@ def main(outdir):
         last = name.split("_")[-1]
         sfx = "" if re.match(r"^\d+x\d+$", last) else last
         full_row, rel, link = "r" in sfx, "x" in sfx, "n" in sfx
+        dm = re.search(r"x(\d+)$", sfx)  # "_nx8": relative tables with D = 8 successors
+        rel_d = int(dm.group(1)) if dm else REL_D
         vec = (PW * S) % 4 == 0 or full_row
         if link:
-            body, outs, ins = chunk_loop_link(K, S, PH, PW, Q, vec=vec, D=REL_D if rel else 0,
+            body, outs, ins = chunk_loop_link(K, S, PH, PW, Q, vec=vec, D=rel_d if rel else 0,
                                               depth=2 if "2" in sfx else 1)
         elif rel:
-            body, outs, ins = chunk_loop_rel(K, S, PH, PW, Q, vec=vec, D=REL_D)
+            body, outs, ins = chunk_loop_rel(K, S, PH, PW, Q, vec=vec, D=rel_d)
         else:
             body, outs, ins = chunk_loop(K, S, PH, PW, Q, vec=vec, single="s" in sfx)
         src = TEMPLATE.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NC=Q * K * K, body=body, outs=outs, ins=ins,
@@ -684,7 +686,7 @@ def main(outdir):
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
         table.append((name, K, S, PH, PW, Q, min_blocks(K, S, PH, PW, Q), 0, 1 if full_row else 0,
-                      REL_D if rel else 0, 1 if link else 0))
+                      rel_d if rel else 0, 1 if link else 0))
     for name, K, S, PH, PW, Q in VARIANTS_MASK:
         body, outs, ins = bucket_mask(K, S, PH, PW, Q)
         src = TEMPLATE_MASK.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, S=S, PH=PH, PW=PW, Q=Q, NS=Q * K * K, body=body, outs=outs,
