@@ -185,6 +185,9 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
   for (int pcs_opt = 0; pcs_opt < 3; ++pcs_opt) {
     if (v.full_row && pcs_opt > 0) continue;
     if (mos_force >= 0 && mos != mos_force && mos_ok) continue;
+    // mode 7 (row records): lanes over consecutive rows of the mosaic
+    // super-image — one row segment per lane, so the patch must span it
+    if (v.mode == 7 && (mos == 0 || pcs_opt > 0 || ceil_div(mosaic_cols(h, mos), v.PW) != 1)) continue;
     // mosaic: one tall super-image of the whole (benchmark-size) batch
     const int PRm = mos ? ceil_div(mosaic_rows(h, mos, 128), v.PH) : PR;
     const int PCm = mos ? ceil_div(mosaic_cols(h, mos), v.PW) : PC;
@@ -262,8 +265,13 @@ bool choose_tiling(const TiledVariant& v, const escoin_csr* h, int CC, std::vect
     // mode 6: a record per tap where any of the Q channels has a nonzero,
     // Q*P FFMAs + P loads each, no dispatch, no window
     const double u6 = 1.0 - std::pow(1.0 - dens, v.Q);
+    // mode 7: a record per (c, kh) where any of K*Q weights is nonzero; per
+    // record vector loads of the row + per-kw branch + Q*PW FFMAs per active kw
+    const double u7 = 1.0 - std::pow(1.0 - dens, v.K * v.Q);
     const double compute = v.mode == 6 ? v.K * v.K * u6 * (v.Q * P + P + 6) + 10
-                                       : (v.Q * dens * v.K * v.K * (work + lat) + win + 30) / IP;
+                           : v.mode == 7 ? v.K * u7 * ((v.PW + v.K + 2) / 4 + 2 + (v.K * v.Q + 3) / 4 + 2 * v.K +
+                                                      v.K * u6 * v.Q * P) + 10
+                                         : (v.Q * dens * v.K * v.K * (work + lat) + win + 30) / IP;
     const double staging = mos ? 5.0 * t.SR * mos * h->W / kTiledThreads
                                : 5.0 * t.NB * IP * std::min(t.SR, h->H) * h->W / kTiledThreads / IP;
     // wave quantisation of the grid at the benchmark batch (128 images)
@@ -455,7 +463,83 @@ void build_ds_tap(const escoin_csr* h, const TiledVariant& v, int WM, int CC, in
   }
 }
 
-void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int plane, DS6* out) {
+// Mode 7 streams (row records): per (m-block, chunk, warp) a 16-byte header
+// {count} and one record per (c, kh) — ascending — where any of the warp's Q
+// rows has a nonzero: {byte offset (c_local*plane + kh*SCs)*4 from the lane's
+// window origin, kw-mask (bit kw: some q has a nonzero), 0, 0} followed by the
+// K*Q weights w[kw*Q + q] (absent: +0.0f), padded to 16 bytes.
+void build_ds_row(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int plane, int SCs, DS6* out) {
+  const int Q = v.Q, M = h->M, C = h->C, K = h->K, KK = K * K;
+  const int G = ceil_div(M, Q), B = ceil_div(G, WM), NK = ceil_div(C, CC);
+  const int RS2 = 2 * (1 + (K * Q + 3) / 4);
+  const int64_t HpWp = int64_t(h->H + 2 * h->pad) * (h->W + 2 * h->pad);
+  const int Wp = h->W + 2 * h->pad;
+  const size_t CKK = size_t(C) * KK;
+  std::vector<float> wd(size_t(M) * CKK, 0.0f);
+  std::vector<unsigned char> nz(size_t(M) * CKK, 0);
+  for (int m = 0; m < M; ++m)
+    for (int64_t j = h->rowptr[m]; j < h->rowptr[m + 1]; ++j) {
+      const int64_t off = h->colidx[j];
+      const int c = int(off / HpWp), rem = int(off - c * HpWp);
+      const size_t col = size_t(c) * KK + size_t(rem / Wp) * K + rem % Wp;
+      wd[size_t(m) * CKK + col] = h->value[j];
+      nz[size_t(m) * CKK + col] = 1;
+    }
+  out->recs.clear();
+  out->sched.clear();
+  out->sched_off.assign(1, 0);
+  out->max_block = 0;
+  std::vector<int> woff(WM), rec(RS2 * 2);
+  for (int b = 0; b < B; ++b) {
+    for (int k = 0; k < NK; ++k) {
+      const int start = int(out->recs.size());
+      int total = 0;
+      for (int wm = 0; wm < WM; ++wm) {
+        woff[wm] = int(out->recs.size()) - start;
+        const size_t hdr = out->recs.size();
+        out->recs.push_back(make_int2(0, 0));
+        out->recs.push_back(make_int2(0, 0));
+        const int g = b * WM + wm;
+        int cnt = 0;
+        for (int cl = 0; cl < CC && g < G; ++cl) {
+          const int c = k * CC + cl;
+          if (c >= C) break;
+          for (int kh = 0; kh < K; ++kh) {
+            unsigned mask = 0;
+            std::fill(rec.begin(), rec.end(), 0);
+            for (int kw = 0; kw < K; ++kw)
+              for (int r = 0; r < Q && g * Q + r < M; ++r) {
+                const size_t idx = size_t(g * Q + r) * CKK + size_t(c) * KK + kh * K + kw;
+                if (nz[idx]) mask |= 1u << kw;
+                std::memcpy(&rec[4 + kw * Q + r], &wd[idx], 4);
+              }
+            if (!mask) continue;
+            rec[0] = (cl * plane + kh * SCs) * 4;
+            rec[1] = int(mask);
+            for (int i = 0; i < RS2; ++i) out->recs.push_back(make_int2(rec[2 * i], rec[2 * i + 1]));
+            ++cnt;
+          }
+        }
+        out->recs[hdr].x = cnt;
+        total += cnt;
+      }
+      if (total == 0) {
+        out->recs.resize(start);
+        continue;
+      }
+      const int count = int(out->recs.size()) - start;
+      out->max_block = std::max(out->max_block, count);
+      out->sched.push_back(k);
+      out->sched.push_back(start);
+      out->sched.push_back(count);
+      for (int wm = 0; wm < WM; ++wm) out->sched.push_back(woff[wm]);
+    }
+    out->sched_off.push_back(int(out->sched.size() / (3 + WM)));
+  }
+}
+
+void build_ds6(const escoin_csr* h, const TiledVariant& v, int WM, int CC, int plane, int SCs, DS6* out) {
+  if (v.mode == 7) return build_ds_row(h, v, WM, CC, plane, SCs, out);
   if (v.mode == 4 || v.mode == 5) return build_ds_1x1(h, v, WM, CC, plane, out);
   if (v.mode == 6) return build_ds_tap(h, v, WM, CC, plane, out);
   const int Q = v.Q, K = h->K;
@@ -670,7 +754,7 @@ int plan_tiled(const escoin_csr* h, const TiledVariant& v, int rank, Tiling* t, 
     }
     if (dup) continue;
     DS6 dd;
-    build_ds6(h, v, c.t.WM, c.CC, c.t.plane, &dd);
+    build_ds6(h, v, c.t.WM, c.CC, c.t.plane, c.t.SCs, &dd);
     const size_t stage_f = (size_t(c.t.NB) * c.CC * c.t.plane + 3) & ~size_t(3);
     // slack: the dispatch loop prefetches up to two records (16 B each for
     // rel_d variants) past a warp's DONE

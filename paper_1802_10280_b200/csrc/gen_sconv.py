@@ -567,6 +567,37 @@ int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
 }}  // namespace escoin
 """
 
+# Row-record variants (mode 7, no dispatch; mosaic tiling, lanes over super-image rows,
+# PW >= the (super-)row width): name, K, PW (row pixels), Q
+VARIANTS_ROW = [
+    ("c3_q2_1x13", 3, 13, 2),
+    ("c3_q4_1x13", 3, 13, 4),
+    ("c3_q3_1x13", 3, 13, 3),
+    ("c3_q2_1x14", 3, 14, 2),
+    ("c3_q4_1x14", 3, 14, 4),
+    ("c3_q4_1x7", 3, 7, 4),
+    ("c3_q8_1x7", 3, 7, 8),
+    ("c3_q2_1x28", 3, 28, 2),
+    ("c5_q2_1x27", 5, 27, 2),
+    ("c5_q1_1x27", 5, 27, 1),
+    ("c5_q2_1x28", 5, 28, 2),
+    ("c5_q4_1x14", 5, 14, 4),
+    ("c5_q4_1x7", 5, 7, 4),
+]
+
+TEMPLATE_ROW = """// GENERATED by gen_sconv.py — do not edit.
+// Variant {name}: K={K} row records (mode 7), full-row patches 1x{PW}, Q={Q}.
+#include "sconv_tiled.cuh"
+
+namespace escoin {{
+
+int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
+  return launch_tiled<{K}, 1, 1, {PW}, {Q}, 2, 7, {TAG}>(a, s);
+}}
+
+}}  // namespace escoin
+"""
+
 VARIANTS_F2 = [
     ("f3s1_q1_4x4", 3, 1, 4, 4, 1),
     ("f3s1_q3_4x4", 3, 1, 4, 4, 3),
@@ -729,6 +760,12 @@ def main(outdir):
         if not os.path.exists(path) or open(path).read() != src:
             open(path, "w").write(src)
         table.append((name, K, S, PH, 1, Q, 2, 6, 0, 0, 0))
+    for name, K, PW, Q in VARIANTS_ROW:
+        src = TEMPLATE_ROW.format(TAG=zlib.crc32(name.encode()) & 0x7fffffff, name=name, K=K, PW=PW, Q=Q)
+        path = os.path.join(outdir, "variant_%s.cu" % name)
+        if not os.path.exists(path) or open(path).read() != src:
+            open(path, "w").write(src)
+        table.append((name, K, 1, 1, PW, Q, 2, 7, 0, 0, 0))
     keep = set("variant_%s.cu" % t[0] for t in table)
     for f in os.listdir(outdir):
         if f.startswith("variant_") and f.endswith(".cu") and f not in keep:

@@ -328,6 +328,57 @@ __global__ void __launch_bounds__(kTiledThreads, MINB) sconv_tiled_kernel(const 
 #pragma unroll
           for (int v = 0; v < PH; ++v) acc[q * P + v] = fmaf(w[1 + q], xv[v], acc[q * P + v]);
       }
+    } else if constexpr (MODE == 7) {
+      // Row records (no dispatch, CSR order kept): lanes own one output row
+      // segment of PW pixels each (flat (image, row) slots).  One record per
+      // (c, kh) where any of the warp's Q channels has a nonzero: {byte offset
+      // of input row kh of channel c from the lane's window origin, kw-mask,
+      // then w[kw][q]} — the lane loads its PW+K-1 input values of that row
+      // once (vector LDS) and, for every kw with a nonzero (warp-uniform
+      // branch), does Q*PW FFMAs; kw ascends inside the record, records ascend
+      // in (c, kh), so each channel accumulates exactly in CSR order.
+      static_assert(PH == 1 && S == 1, "row-record mode: full-row patches, stride 1");
+      constexpr int XR = PW + K - 1;
+      constexpr int XV = (XR + 3) / 4;
+      constexpr int RS4 = 1 + (K * Q + 3) / 4;
+      const int4* rp = reinterpret_cast<const int4*>(ws);
+      const int cnt = rp[0].x;
+      rp += 1;
+      const char* sb = reinterpret_cast<const char*>(slab);
+#pragma unroll 1
+      for (int i = 0; i < cnt; ++i) {
+        const int4 hd = rp[0];
+        float w[(RS4 - 1) * 4];
+#pragma unroll
+        for (int k = 0; k < RS4 - 1; ++k) {
+          const int4 t = rp[1 + k];
+          w[4 * k + 0] = __int_as_float(t.x);
+          w[4 * k + 1] = __int_as_float(t.y);
+          w[4 * k + 2] = __int_as_float(t.z);
+          w[4 * k + 3] = __int_as_float(t.w);
+        }
+        rp += RS4;
+        const float4* b = reinterpret_cast<const float4*>(sb + hd.x);
+        float xr[XV * 4];
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+          const float4 t = b[v];
+          xr[4 * v + 0] = t.x;
+          xr[4 * v + 1] = t.y;
+          xr[4 * v + 2] = t.z;
+          xr[4 * v + 3] = t.w;
+        }
+        const unsigned mask = static_cast<unsigned>(hd.y);
+#pragma unroll
+        for (int kw = 0; kw < K; ++kw) {
+          if (mask & (1u << kw)) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+              for (int px = 0; px < PW; ++px) acc[q * P + px] = fmaf(w[kw * Q + q], xr[px + kw], acc[q * P + px]);
+          }
+        }
+      }
     } else {
       // warp stream: per bucket {c, 0, 0, 0} + Q*K*K weights (16-byte padded); c < 0 ends
       constexpr int NW4 = (Q * K * K + 3) / 4;
