@@ -580,6 +580,9 @@ VARIANTS_ROW = [
     ("c3_q2_1x28", 3, 28, 2),
     ("c5_q2_1x27", 5, 27, 2),
     ("c5_q1_1x27", 5, 27, 1),
+    ("c5_q1_1x28", 5, 28, 1),
+    ("c5_q1_1x14", 5, 14, 1),
+    ("c5_q2_1x14", 5, 14, 2),
     ("c5_q2_1x28", 5, 28, 2),
     ("c5_q4_1x14", 5, 14, 4),
     ("c5_q4_1x7", 5, 7, 4),
