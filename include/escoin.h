@@ -170,6 +170,32 @@ int escoin_csr_get_kernel(const escoin_csr* csr, int* id);
 int escoin_csr_autotune(escoin_csr* csr, int N, const float* in, float* out, const float* bias, int relu,
                         int reps, void* cuda_stream, int* best_id, float* best_ms);
 
+/* ---------------------------------------------------------------- pattern-specialised kernel
+ * Kernel customisation (§3.4) taken to the layer's weights: the
+ * paper specialises its kernel per filter size / ofmap size / batch / stride
+ * with C++ templates; weights are fixed once stretched ("only run once",
+ * P:437-442), so this call compiles the handle's nonzero PATTERN and VALUES
+ * into a kernel (generated PTX, one `fma.rn.f32 acc, x, <weight>, acc` per
+ * nonzero and output pixel, compiled in-process for sm_100a and loaded into
+ * the current context).  Results are bitwise identical to every other variant
+ * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
+ *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
+ *              forwards accept any N.
+ *   tunables   NULL or ntunables (<= 6) ints {Q output channels per CTA,
+ *              P pixels per lane, CC channels per stage, NS stages, warps per
+ *              CTA, CTAs per SM}; <= 0 entries take the defaults.
+ * On success the handle's kernel becomes ESCOIN_KERNEL_JIT.  Synchronous
+ * (device-wide sync first); compile time grows with nnz (about 25 s for
+ * 180k nonzeros on one host core).  Only stride 1 with "same" padding
+ * (2*pad == K-1) has a specialised form.
+ * Errors: NULL, NOT_ON_DEVICE, UNSUPPORTED (shape, tunables, compile), CUDA (load). */
+#define ESCOIN_KERNEL_JIT 1000
+int escoin_csr_jit(escoin_csr* csr, int n_hint, const int* tunables, int ntunables);
+/* Parameters of the handle's specialised kernel: tunables6 (6 ints, as above,
+ * defaults resolved), mosaic width, registers per thread, cubin bytes.  Any
+ * output pointer may be NULL.  Errors: NULL, UNSUPPORTED (no specialised kernel). */
+int escoin_csr_jit_info(const escoin_csr* csr, int* tunables6, int* mos, int* regs, int64_t* code_bytes);
+
 /* ---- Benchmark-only comparison point (NOT the method; SURVEY 8(b) "escoin_bench_*",
  * north_star: "a dense tcgen05 implicit-GEMM is kept only as a measured comparison point").
  * Dense convolution of the pruned weights INCLUDING their zeros on the 5th-generation

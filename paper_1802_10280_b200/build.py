@@ -21,6 +21,9 @@ GEN = os.path.join(CSRC, "generated")
 OBJ = os.path.join(ROOT, "build", "obj")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libescoin.so")
+# in-process PTX compiler for the pattern-specialised kernels (jit_sconv.cpp)
+PTXC = os.path.join(os.path.dirname(os.path.dirname(os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc"))),
+                    "lib64", "libnvptxcompiler_static.a")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -64,12 +67,13 @@ def build(jobs: int | None = None, verbose: bool = False) -> str:
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         glob.glob(os.path.join(INCLUDE, "*.h")) + [os.path.join(GEN, "variants_table.inc")]
     core = [os.path.join(CSRC, "escoin_host.cu"), os.path.join(CSRC, "sconv_paper.cu"),
-            os.path.join(CSRC, "stretch_device.cu"), os.path.join(CSRC, "dense_tc.cu")]
+            os.path.join(CSRC, "stretch_device.cu"), os.path.join(CSRC, "dense_tc.cu"),
+            os.path.join(CSRC, "jit_sconv.cpp")]
     srcs = core + variants
     jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 4))
     with ThreadPoolExecutor(jobs) as ex:
         objs = dict(zip(srcs, ex.map(lambda s: _compile(s, headers), srcs)))
-    _link(LIB, [objs[s] for s in core + variants], [])
+    _link(LIB, [objs[s] for s in core + variants], [PTXC])
     if verbose:
         for s in srcs:
             log = os.path.join(OBJ, os.path.basename(s) + ".o.log")

@@ -11,6 +11,7 @@
 
 #include "escoin.h"
 #include "escoin_internal.h"
+#include "jit_sconv.h"
 
 using namespace escoin;
 
@@ -32,6 +33,7 @@ struct escoin_csr {
   int* d_sched = nullptr;
   int* d_sched_off = nullptr;
   TiledArgs targs{};  // pointers/tiling filled at DS-6 build; tensors per forward
+  JitModule* jit = nullptr;  // pattern-specialised kernel (escoin_csr_jit), kept until free
 };
 
 namespace {
@@ -859,9 +861,44 @@ int auto_kernel(const escoin_csr* h) {
   return best;
 }
 
+// Pattern-specialised kernel (jit_sconv.cpp): plan, generate, compile, load.
+// tun = {Q, P, CC, NS, warps, minb} (<= 0: default) or NULL.
+int build_jit(escoin_csr* h, int n_hint, const int* tun) {
+  JitPlan p;
+  if (tun) {
+    p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5];
+  }
+  if (p.P > 8 || p.Q > 256 || p.CC > 64 || p.NS > 6 || p.warps > 32 || p.minb > 8) return ESCOIN_ERR_UNSUPPORTED;
+  if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint) != 0) return ESCOIN_ERR_UNSUPPORTED;
+  if (int64_t(p.warps) * 32 * p.minb > 2048) return ESCOIN_ERR_UNSUPPORTED;
+  if (h->rowptr.size() != size_t(h->M) + 1) return ESCOIN_ERR_UNSUPPORTED;
+  JitModule* jm = new (std::nothrow) JitModule();
+  if (!jm) return ESCOIN_ERR_ALLOC;
+  const int rc = jit_build(*jm, p, h->rowptr.data(), h->colidx.data(), h->value.data(), nullptr);
+  if (rc != 0) {
+    delete jm;
+    return rc == -2 ? ESCOIN_ERR_UNSUPPORTED : ESCOIN_ERR_CUDA;
+  }
+  if (h->jit) {
+    jit_free(*h->jit);
+    delete h->jit;
+  }
+  h->jit = jm;
+  return ESCOIN_OK;
+}
+
 int set_kernel(escoin_csr* h, int id, cudaStream_t s, int rank = 0) {
   int nv = 0;
   const TiledVariant* tv = tiled_variants(&nv);
+  if (id == ESCOIN_KERNEL_JIT) {
+    if (!h->jit) {
+      const int rc = build_jit(h, 128, nullptr);
+      if (rc != ESCOIN_OK) return rc;
+    }
+    free_ds6(h);
+    h->kernel = id;
+    return ESCOIN_OK;
+  }
   if (id == ESCOIN_KERNEL_AUTO) id = auto_kernel(h);
   if (id < 0 || id > nv) return ESCOIN_ERR_UNSUPPORTED;
   if (id > 0 && (tv[id - 1].K != h->K || tv[id - 1].S != h->stride)) return ESCOIN_ERR_UNSUPPORTED;
@@ -1090,6 +1127,10 @@ void escoin_csr_free(escoin_csr* h) {
     DeviceGuard g(h->device);
     cudaDeviceSynchronize();
     free_ds6(h);
+    if (h->jit) {
+      jit_free(*h->jit);
+      delete h->jit;
+    }
     if (!h->borrowed) {
       if (h->d_rowptr) cudaFree(h->d_rowptr);
       if (h->d_colidx) cudaFree(h->d_colidx);
@@ -1113,7 +1154,10 @@ int escoin_sconv_forward(int N, int C, int H, int W, int M, int K, int stride, i
   if (int64_t(N) * C * H * W > (int64_t(1) << 40)) return ESCOIN_ERR_OVERFLOW;
   cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
   int rc;
-  if (h->kernel == 0) {
+  if (h->kernel == ESCOIN_KERNEL_JIT) {
+    if (int64_t(N) * C * H * W > kInt32Max) return ESCOIN_ERR_OVERFLOW;
+    rc = jit_launch(*h->jit, in, out, bias, relu, N, s);
+  } else if (h->kernel == 0) {
     rc = launch_paper(h->d_rowptr, h->d_colidx, h->d_value, in, out, bias, relu ? 1 : 0, N, C, H, W, M, K, stride,
                       pad, h->E, h->F, s);
   } else {
@@ -1184,7 +1228,7 @@ int escoin_csr_set_kernel(escoin_csr* h, int id) {
   if (!h->on_device) {
     int nv = 0;
     tiled_variants(&nv);
-    if (id != ESCOIN_KERNEL_AUTO && (id < 0 || id > nv)) return ESCOIN_ERR_UNSUPPORTED;
+    if (id != ESCOIN_KERNEL_AUTO && id != ESCOIN_KERNEL_JIT && (id < 0 || id > nv)) return ESCOIN_ERR_UNSUPPORTED;
     h->kernel = id;  // resolved at escoin_csr_to_device
     return ESCOIN_OK;
   }
@@ -1228,6 +1272,19 @@ int escoin_csr_autotune(escoin_csr* h, int N, const float* in, float* out, const
     ms /= reps;
     if (best < 0 || ms < best_t) { best = id; best_rank = rank; best_t = ms; }
   }
+  if (rc == ESCOIN_OK && h->jit) {  // the pattern-specialised kernel, when one was built (escoin_csr_jit)
+    h->kernel = ESCOIN_KERNEL_JIT;
+    rc = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < reps && rc == ESCOIN_OK; ++r)
+      rc = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
+    cudaEventRecord(e1, s);
+    if (rc == ESCOIN_OK && cudaEventSynchronize(e1) != cudaSuccess) rc = ESCOIN_ERR_CUDA;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+    if (rc == ESCOIN_OK && (best < 0 || ms < best_t)) { best = ESCOIN_KERNEL_JIT; best_t = ms; }
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (rc != ESCOIN_OK) return rc;
@@ -1236,6 +1293,36 @@ int escoin_csr_autotune(escoin_csr* h, int N, const float* in, float* out, const
   if (cudaStreamSynchronize(s) != cudaSuccess) return ESCOIN_ERR_CUDA;
   if (best_id) *best_id = best;
   if (best_ms) *best_ms = best_t;
+  return ESCOIN_OK;
+}
+
+int escoin_csr_jit(escoin_csr* h, int n_hint, const int* tunables, int ntunables) {
+  if (!h) return ESCOIN_ERR_NULL;
+  if (!h->on_device) return ESCOIN_ERR_NOT_ON_DEVICE;
+  if (ntunables < 0 || ntunables > 6 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
+  int tun[6] = {0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
+  DeviceGuard g(h->device);
+  if (!g.ok) return ESCOIN_ERR_CUDA;
+  cudaDeviceSynchronize();  // no forward may be running the kernel being replaced
+  const int rc = build_jit(h, n_hint > 0 ? n_hint : 128, tun);
+  if (rc != ESCOIN_OK) return rc;
+  free_ds6(h);
+  h->kernel = ESCOIN_KERNEL_JIT;
+  return ESCOIN_OK;
+}
+
+int escoin_csr_jit_info(const escoin_csr* h, int* tunables6, int* mos, int* regs, int64_t* code_bytes) {
+  if (!h) return ESCOIN_ERR_NULL;
+  if (!h->jit) return ESCOIN_ERR_UNSUPPORTED;
+  const JitPlan& p = h->jit->plan;
+  if (tunables6) {
+    tunables6[0] = p.Q; tunables6[1] = p.P; tunables6[2] = p.CC;
+    tunables6[3] = p.NS; tunables6[4] = p.warps; tunables6[5] = p.minb;
+  }
+  if (mos) *mos = p.mos;
+  if (regs) *regs = h->jit->regs;
+  if (code_bytes) *code_bytes = int64_t(h->jit->cubin_bytes);
   return ESCOIN_OK;
 }
 

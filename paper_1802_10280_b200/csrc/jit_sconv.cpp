@@ -1,0 +1,464 @@
+// jit_sconv.cpp — pattern-specialised direct sparse convolution (kernel
+// customisation, §3.4, carried to its limit).
+//
+// The paper customises its kernel per (filter size, ofmap size, batch,
+// stride) with C++ templates.  Weights are fixed once a layer is pruned and
+// stretched ("only run once"), so this file goes one step further
+// and compiles the layer's nonzero PATTERN and VALUES into the instruction
+// stream: for every (output-channel group, input channel) the generated PTX
+// loads the input taps the group uses from the shared-memory slab and issues
+// one `fma.rn.f32 acc, x, <weight immediate>, acc` per (nonzero, pixel).
+// There is no per-nonzero dispatch, no record stream and no weight load at
+// all (the weight is an FFMA immediate), which is what the register-tiled
+// interpreter kernels (sconv_tiled.cuh) spend most of their issue slots on.
+//
+// Semantics are exactly escoin_sconv_forward's (Alg.2 P:389-410 with the
+// stride/pad generalisation R#1, R#9, R#10): each accumulator starts at 0.0f
+// and receives its CSR terms in ascending (c, kh, kw) = colidx order with
+// fma.rn.f32, then acc + bias[m] and ReLU — bit-identical to every other
+// variant (tested).
+//
+// Geometry (stride 1, "same" padding 2*pad == K-1): the batch is one mosaic
+// super-image (images on a grid of `mos` columns separated by `pad` zero
+// rows/columns, shared by neighbours); an output SLOT q = R*SWs + X of the
+// super-image reads the staged input at q + kh*SWs + kw, i.e. the stretched
+// offset f(0, kh, kw) of P:428 with the super-image row stride.  A CTA owns
+// T consecutive slots (lane l of warp w: slots q0 + (w*P + j)*32 + l), stages
+// [q0, q0 + T + (K-1)*(SWs+1)) of CC channels per pipeline stage with
+// 4-byte cp.async (zero-fill = the virtual padding, R#9), and blockIdx.y
+// selects the output-channel group of Q rows whose code it runs.
+//
+// Compilation: PTX text -> nvPTXCompiler (static, in-process) -> cubin ->
+// driver module (entry points via cudaGetDriverEntryPoint, so the library
+// has no link-time dependency on libcuda).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nvPTXCompiler.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "jit_sconv.h"
+
+namespace escoin {
+namespace {
+
+typedef CUresult (*PFN_ModuleLoadData)(CUmodule*, const void*);
+typedef CUresult (*PFN_ModuleGetFunction)(CUfunction*, CUmodule, const char*);
+typedef CUresult (*PFN_ModuleUnload)(CUmodule);
+typedef CUresult (*PFN_FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
+typedef CUresult (*PFN_FuncGetAttribute)(int*, CUfunction_attribute, CUfunction);
+typedef CUresult (*PFN_LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                     unsigned, CUstream, void**, void**);
+
+struct Driver {
+  PFN_ModuleLoadData load = nullptr;
+  PFN_ModuleGetFunction get = nullptr;
+  PFN_ModuleUnload unload = nullptr;
+  PFN_FuncSetAttribute setattr = nullptr;
+  PFN_FuncGetAttribute getattr = nullptr;
+  PFN_LaunchKernel launch = nullptr;
+  bool ok = false;
+};
+
+template <typename T>
+bool entry(const char* name, T* fn) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+      !p)
+    return false;
+  *fn = reinterpret_cast<T>(p);
+  return true;
+}
+
+const Driver& driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    d.ok = entry("cuModuleLoadData", &d.load) && entry("cuModuleGetFunction", &d.get) &&
+           entry("cuModuleUnload", &d.unload) && entry("cuFuncSetAttribute", &d.setattr) &&
+           entry("cuFuncGetAttribute", &d.getattr) && entry("cuLaunchKernel", &d.launch);
+  });
+  return d;
+}
+
+int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- geometry
+void plan_geometry(JitPlan& p, int n_hint) {
+  const int hp = p.H + p.pad, wp = p.W + p.pad;
+  const int nmg = cdiv(p.M, p.Q);
+  const int T = p.warps * 32 * p.P;
+  double best = 0;
+  p.mos = 1;
+  for (int mos = 1; mos <= n_hint; ++mos) {
+    const int NR = cdiv(n_hint, mos);
+    const int64_t SWs = int64_t(mos) * wp + p.pad;
+    if (SWs * (p.K - 1) > 4 * T) break;  // halo larger than 4 tiles: wider is only worse
+    const int64_t slots = (int64_t(NR - 1) * hp + p.H) * SWs;
+    const int64_t tiles = (slots + T - 1) / T;
+    const int64_t L = T + int64_t(p.K - 1) * (SWs + 1);
+    const int64_t ctas = tiles * nmg, per_wave = int64_t(148) * p.minb;
+    const double waves = double((ctas + per_wave - 1) / per_wave) / double(ctas) * per_wave;  // quantisation
+    const double cost = double(tiles) * (T + 0.15 * double(L - T)) * waves / double(per_wave);
+    if (mos == 1 || cost < best) { best = cost; p.mos = mos; }
+  }
+  p.T = T;
+  p.SWs = p.mos * wp + p.pad;
+  p.L = T + (p.K - 1) * (p.SWs + 1);
+  p.Ls = (p.L + 3) & ~3;
+  p.nmg = nmg;
+  p.nch = cdiv(p.C, p.CC);
+  p.KS = cdiv(p.L, p.warps * 32);
+  p.smem_bytes = p.NS * p.CC * p.Ls * 4;
+}
+
+// ---------------------------------------------------------------- PTX text
+struct Out {
+  std::string s;
+  char buf[256];
+  void operator()(const char* fmt, ...) __attribute__((format(printf, 2, 3))) {
+    va_list ap;
+    va_start(ap, fmt);
+    va_list ap2;
+    va_copy(ap2, ap);
+    const int n = vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (n < int(sizeof buf)) {
+      s.append(buf, n);
+    } else {  // long line (branch-target lists)
+      std::string big(size_t(n) + 1, '\0');
+      vsnprintf(&big[0], big.size(), fmt, ap2);
+      s.append(big.data(), n);
+    }
+    va_end(ap2);
+    s.push_back('\n');
+  }
+};
+
+struct Nz {
+  int t, q;
+  uint32_t bits;
+};
+
+std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value) {
+  const int KK = p.K * p.K, Q = p.Q, P = p.P, NT = p.warps * 32;
+  const int Hpd = p.H + 2 * p.pad, Wpd = p.W + 2 * p.pad;  // stretched geometry (R#3)
+  const int hp = p.H + p.pad, wp = p.W + p.pad;
+  const int HW = p.H * p.W, EF = p.E * p.F;
+  // nonzeros per (m-group, channel), ascending tap then row
+  std::vector<std::vector<Nz>> lists(size_t(p.nmg) * p.C);
+  for (int m = 0; m < p.M; ++m) {
+    const int g = m / Q, q = m % Q;
+    for (int j = rowptr[m]; j < rowptr[m + 1]; ++j) {
+      const int col = colidx[j];
+      const int c = col / (Hpd * Wpd), r = col % (Hpd * Wpd);
+      const int kh = r / Wpd, kw = r % Wpd;
+      uint32_t bits;
+      std::memcpy(&bits, &value[j], 4);
+      lists[size_t(g) * p.C + c].push_back({kh * p.K + kw, q, bits});
+    }
+  }
+  for (auto& l : lists)
+    std::stable_sort(l.begin(), l.end(), [](const Nz& a, const Nz& b) { return a.t < b.t; });
+
+  Out o;
+  o(".version 8.7");
+  o(".target sm_100a");
+  o(".address_size 64");
+  o(".extern .shared .align 16 .b8 smem[];");
+  o(".visible .entry escoin_jit_sconv(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
+    ".param .u32 p_relu, .param .u32 p_N)");
+  o(".maxntid %d, 1, 1", NT);
+  o(".minnctapersm %d", p.minb);
+  o("{");
+  o(".reg .pred %%p<%d>;", 16 + 2 * p.KS + P);
+  o(".reg .b32 %%r<%d>;", 64 + 4 * p.KS + 8 * P);
+  o(".reg .b64 %%rd<%d>;", 32 + 2 * p.KS + 2 * P);
+  o(".reg .f32 %%a<%d>;", Q * P);
+  o(".reg .f32 %%x<%d>;", KK * P);
+  o(".reg .f32 %%v<8>;");
+  // params, ids
+  o("ld.param.u64 %%rd0, [p_in];");
+  o("cvta.to.global.u64 %%rd0, %%rd0;");
+  o("ld.param.u64 %%rd1, [p_out];");
+  o("cvta.to.global.u64 %%rd1, %%rd1;");
+  o("ld.param.u64 %%rd2, [p_bias];");
+  o("ld.param.u32 %%r0, [p_relu];");
+  o("ld.param.u32 %%r1, [p_N];");
+  o("mov.u32 %%r2, %%tid.x;");
+  o("mov.u32 %%r3, %%ctaid.x;");
+  o("mov.u32 %%r4, %%ctaid.y;");
+  o("mul.lo.u32 %%r5, %%r3, %d;", p.T);  // q0
+  o("mov.u32 %%r6, smem;");
+  o("and.b32 %%r7, %%r2, 31;");           // lane
+  o("shr.u32 %%r8, %%r2, 5;");            // warp
+  o("mul.lo.u32 %%r9, %%r8, %d;", 32 * P);
+  o("add.u32 %%r9, %%r9, %%r7;");         // lane slot (j = 0)
+  o("shl.b32 %%r10, %%r9, 2;");
+  o("add.u32 %%r10, %%r10, %%r6;");       // lane smem base
+  // staging slots: k < KS; regs: rd(32+k) src ptr, r(64+k) dst, r(64+KS+k) size, p(16+k) in range
+  for (int k = 0; k < p.KS; ++k) {
+    const int rs = 64 + k, rz = 64 + p.KS + k, t0 = 64 + 2 * p.KS;  // t0.. scratch
+    o("add.u32 %%r%d, %%r2, %d;", t0, k * NT);                // i
+    o("setp.lt.u32 %%p%d, %%r%d, %d;", 16 + k, t0, p.L);
+    o("shl.b32 %%r%d, %%r%d, 2;", rs, t0);
+    o("add.u32 %%r%d, %%r%d, %%r6;", rs, rs);                 // dst
+    o("add.u32 %%r%d, %%r%d, %%r5;", t0 + 1, t0);             // flat
+    o("div.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, p.SWs);    // R'
+    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 2, p.SWs);
+    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 3, t0 + 1, t0 + 3);  // X'
+    o("sub.s32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 2, p.pad);    // rr
+    o("sub.s32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 3, p.pad);    // cc
+    o("setp.ge.s32 %%p0, %%r%d, 0;", t0 + 2);
+    o("setp.ge.and.s32 %%p0, %%r%d, 0, %%p0;", t0 + 3);
+    o("max.s32 %%r%d, %%r%d, 0;", t0 + 2, t0 + 2);
+    o("max.s32 %%r%d, %%r%d, 0;", t0 + 3, t0 + 3);
+    o("div.u32 %%r%d, %%r%d, %d;", t0 + 4, t0 + 2, hp);       // nr
+    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 5, t0 + 4, hp);
+    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 5, t0 + 2, t0 + 5);  // y
+    o("div.u32 %%r%d, %%r%d, %d;", t0 + 6, t0 + 3, wp);       // nc
+    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 7, t0 + 6, wp);
+    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 7, t0 + 3, t0 + 7);  // x
+    o("setp.lt.and.u32 %%p0, %%r%d, %d, %%p0;", t0 + 5, p.H);
+    o("setp.lt.and.u32 %%p0, %%r%d, %d, %%p0;", t0 + 7, p.W);
+    o("setp.lt.and.u32 %%p0, %%r%d, %d, %%p0;", t0 + 6, p.mos);
+    o("mad.lo.u32 %%r%d, %%r%d, %d, %%r%d;", t0 + 4, t0 + 4, p.mos, t0 + 6);  // n
+    o("setp.lt.and.u32 %%p0, %%r%d, %%r1, %%p0;", t0 + 4);
+    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 4, t0 + 4, p.C * HW);
+    o("mad.lo.u32 %%r%d, %%r%d, %d, %%r%d;", t0 + 4, t0 + 5, p.W, t0 + 4);
+    o("add.u32 %%r%d, %%r%d, %%r%d;", t0 + 4, t0 + 4, t0 + 7);  // src element
+    o("selp.u32 %%r%d, %%r%d, 0, %%p0;", t0 + 4, t0 + 4);
+    o("selp.u32 %%r%d, 4, 0, %%p0;", rz);
+    o("mul.wide.u32 %%rd%d, %%r%d, 4;", 32 + k, t0 + 4);
+    o("add.s64 %%rd%d, %%rd%d, %%rd0;", 32 + k, 32 + k);
+  }
+  // stage(chunk register rc, buffer byte offset register rb): r11 = chunk, r12 = buffer offset
+  auto stage = [&](const char* rc, const char* rb) {
+    o("mul.wide.u32 %%rd3, %s, %d;", rc, p.CC * HW * 4);
+    o("mul.lo.u32 %%r13, %s, %d;", rc, p.CC);
+    o("sub.s32 %%r13, %d, %%r13;", p.C);  // channels left
+    for (int cc = 0; cc < p.CC; ++cc) {
+      o("setp.gt.s32 %%p1, %%r13, %d;", cc);
+      for (int k = 0; k < p.KS; ++k) {
+        o("and.pred %%p2, %%p1, %%p%d;", 16 + k);
+        o("add.u32 %%r14, %%r%d, %s;", 64 + k, rb);
+        o("add.s64 %%rd4, %%rd%d, %%rd3;", 32 + k);
+        o("@%%p2 cp.async.ca.shared.global [%%r14+%d], [%%rd4+%d], 4, %%r%d;", cc * p.Ls * 4, cc * HW * 4,
+          64 + p.KS + k);
+      }
+    }
+  };
+  for (int q = 0; q < Q * P; ++q) o("mov.f32 %%a%d, 0f00000000;", q);
+  for (int s = 0; s < p.NS - 1; ++s) {
+    if (s < p.nch) {
+      o("mov.u32 %%r11, %d;", s);
+      o("mov.u32 %%r12, %d;", s * p.CC * p.Ls * 4);
+      stage("%r11", "%r12");
+    }
+    o("cp.async.commit_group;");
+  }
+  o("mov.u32 %%r15, 0;");  // k
+  o("mov.u32 %%r16, %d;", (p.NS - 1) * p.CC * p.Ls * 4);  // buffer offset of chunk k + NS - 1
+  // branch targets
+  std::string tg = "ts: .branchtargets ";
+  for (int g = 0; g < p.nmg; ++g)
+    for (int k = 0; k < p.nch; ++k) {
+      char b[32];
+      snprintf(b, sizeof b, "%sB%d_%d", (g || k) ? ", " : "", g, k);
+      tg += b;
+    }
+  tg += ";";
+  o("LOOP:");
+  o("cp.async.wait_group %d;", p.NS - 2);
+  o("bar.sync 0;");
+  o("add.u32 %%r11, %%r15, %d;", p.NS - 1);
+  o("setp.ge.u32 %%p3, %%r11, %d;", p.nch);
+  o("@%%p3 bra.uni NOSTAGE;");
+  stage("%r11", "%r16");
+  o("NOSTAGE:");
+  o("cp.async.commit_group;");
+  o("add.u32 %%r16, %%r16, %d;", p.CC * p.Ls * 4);
+  o("setp.ge.u32 %%p4, %%r16, %d;", p.NS * p.CC * p.Ls * 4);
+  o("@%%p4 mov.u32 %%r16, 0;");
+  o("mad.lo.u32 %%r17, %%r4, %d, %%r15;", p.nch);
+  o("%s", tg.c_str());
+  o("brx.idx.uni %%r17, ts;");
+  for (int g = 0; g < p.nmg; ++g)
+    for (int k = 0; k < p.nch; ++k) {
+      o("B%d_%d:", g, k);
+      const int buf = k % p.NS;
+      for (int cc = 0; cc < p.CC; ++cc) {
+        const int c = k * p.CC + cc;
+        if (c >= p.C) break;
+        const auto& l = lists[size_t(g) * p.C + c];
+        if (l.empty()) continue;
+        bool used[64] = {};
+        for (const Nz& z : l) used[z.t] = true;
+        for (int t = 0; t < KK; ++t) {
+          if (!used[t]) continue;
+          const int kh = t / p.K, kw = t % p.K;
+          for (int j = 0; j < P; ++j)
+            o("ld.shared.f32 %%x%d, [%%r10+%d];", t * P + j,
+              ((buf * p.CC + cc) * p.Ls + j * 32 + kh * p.SWs + kw) * 4);
+        }
+        for (const Nz& z : l)
+          for (int j = 0; j < P; ++j)
+            o("fma.rn.f32 %%a%d, %%x%d, 0f%08X, %%a%d;", z.q * P + j, z.t * P + j, z.bits, z.q * P + j);
+      }
+      o("bra.uni NEXT;");
+    }
+  o("NEXT:");
+  o("add.u32 %%r15, %%r15, 1;");
+  o("setp.lt.u32 %%p5, %%r15, %d;", p.nch);
+  o("@%%p5 bra.uni LOOP;");
+  // epilogue
+  o("setp.ne.u64 %%p6, %%rd2, 0;");
+  o("setp.ne.u32 %%p7, %%r0, 0;");
+  o("mul.lo.u32 %%r18, %%r4, %d;", Q);           // m0
+  o("mul.wide.u32 %%rd5, %%r18, 4;");
+  o("add.s64 %%rd5, %%rd5, %%rd2;");             // bias + m0
+  o("mul.wide.u32 %%rd6, %%r18, %d;", EF * 4);   // m0 * EF bytes
+  o("sub.s32 %%r19, %d, %%r18;", p.M);           // rows left
+  for (int j = 0; j < P; ++j) {
+    const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j, t0 = 64 + 4 * p.KS + 8 * j;
+    o("add.u32 %%r%d, %%r9, %%r5;", t0);
+    if (j) o("add.u32 %%r%d, %%r%d, %d;", t0, t0, 32 * j);
+    o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, p.SWs);      // R
+    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, p.SWs);
+    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 2, t0, t0 + 2);  // X
+    o("div.u32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 1, hp);     // nr
+    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 4, t0 + 3, hp);
+    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 4, t0 + 1, t0 + 4);  // oh
+    o("div.u32 %%r%d, %%r%d, %d;", t0 + 5, t0 + 2, wp);     // nc
+    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 6, t0 + 5, wp);
+    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 6, t0 + 2, t0 + 6);  // ow
+    o("setp.lt.u32 %%p%d, %%r%d, %d;", pv, t0 + 4, p.E);
+    o("setp.lt.and.u32 %%p%d, %%r%d, %d, %%p%d;", pv, t0 + 6, p.F, pv);
+    o("setp.lt.and.u32 %%p%d, %%r%d, %d, %%p%d;", pv, t0 + 5, p.mos, pv);
+    o("mad.lo.u32 %%r%d, %%r%d, %d, %%r%d;", t0 + 3, t0 + 3, p.mos, t0 + 5);  // n
+    o("setp.lt.and.u32 %%p%d, %%r%d, %%r1, %%p%d;", pv, t0 + 3, pv);
+    o("mul.wide.u32 %%rd%d, %%r%d, %d;", rdo, t0 + 3, p.M * EF);  // n*M*EF (elements)
+    o("mad.lo.u32 %%r%d, %%r%d, %d, %%r%d;", t0 + 4, t0 + 4, p.F, t0 + 6);  // oh*F + ow
+    o("cvt.u64.u32 %%rd7, %%r%d;", t0 + 4);
+    o("add.s64 %%rd%d, %%rd%d, %%rd7;", rdo, rdo);
+    o("shl.b64 %%rd%d, %%rd%d, 2;", rdo, rdo);
+    o("add.s64 %%rd%d, %%rd%d, %%rd1;", rdo, rdo);
+    o("add.s64 %%rd%d, %%rd%d, %%rd6;", rdo, rdo);
+  }
+  for (int q = 0; q < Q; ++q) {
+    o("setp.gt.s32 %%p8, %%r19, %d;", q);
+    o("mov.f32 %%v0, 0f00000000;");
+    o("and.pred %%p9, %%p8, %%p6;");
+    o("@%%p9 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
+    for (int j = 0; j < P; ++j) {
+      const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j;
+      o("add.rn.f32 %%v1, %%a%d, %%v0;", q * P + j);
+      o("setp.gt.f32 %%p10, %%v1, 0f00000000;");
+      o("selp.f32 %%v2, %%v1, 0f00000000, %%p10;");
+      o("selp.f32 %%v1, %%v2, %%v1, %%p7;");
+      o("and.pred %%p11, %%p8, %%p%d;", pv);
+      o("@%%p11 st.global.f32 [%%rd%d+%d], %%v1;", rdo, q * EF * 4);
+    }
+  }
+  o("ret;");
+  o("}");
+  return o.s;
+}
+
+}  // namespace
+
+int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad, int n_hint) {
+  if (stride != 1 || 2 * pad != K - 1 || K > 7) return -1;
+  p.C = C; p.H = H; p.W = W; p.M = M; p.K = K; p.pad = pad;
+  p.E = H; p.F = W;
+  if (p.Q <= 0) p.Q = 64;
+  if (p.P <= 0) p.P = 1;
+  if (p.CC <= 0) p.CC = 8;
+  if (p.NS <= 1) p.NS = 3;
+  if (p.warps <= 0) p.warps = 8;
+  if (p.minb <= 0) p.minb = 2;
+  p.Q = std::min(p.Q, M);
+  plan_geometry(p, std::max(1, n_hint));
+  if (p.smem_bytes > 227 * 1024 / p.minb) return -1;
+  if (int64_t(p.SWs) * (p.H + p.pad) * ((n_hint + p.mos - 1) / p.mos + 1) > (int64_t(1) << 30)) return -1;
+  return 0;
+}
+
+int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
+              std::string* log) {
+  const Driver& d = driver();
+  if (!d.ok) return -1;
+  jm.plan = p;
+  const std::string ptx = gen_ptx(p, rowptr, colidx, value);
+  jm.ptx_bytes = ptx.size();
+  nvPTXCompilerHandle c = nullptr;
+  if (nvPTXCompilerCreate(&c, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) return -1;
+  const char* opts[] = {"--gpu-name=sm_100a", "-O3"};
+  const nvPTXCompileResult r = nvPTXCompilerCompile(c, 2, opts);
+  if (r != NVPTXCOMPILE_SUCCESS) {
+    if (log) {
+      size_t n = 0;
+      nvPTXCompilerGetErrorLogSize(c, &n);
+      std::string e(n, '\0');
+      if (n) nvPTXCompilerGetErrorLog(c, &e[0]);
+      *log = e;
+    }
+    nvPTXCompilerDestroy(&c);
+    return -2;
+  }
+  size_t n = 0;
+  nvPTXCompilerGetCompiledProgramSize(c, &n);
+  std::vector<char> cubin(n);
+  nvPTXCompilerGetCompiledProgram(c, cubin.data());
+  nvPTXCompilerDestroy(&c);
+  jm.cubin_bytes = n;
+  CUmodule mod = nullptr;
+  if (d.load(&mod, cubin.data()) != CUDA_SUCCESS) return -3;
+  CUfunction f = nullptr;
+  if (d.get(&f, mod, "escoin_jit_sconv") != CUDA_SUCCESS) { d.unload(mod); return -3; }
+  if (d.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, p.smem_bytes) != CUDA_SUCCESS) {
+    d.unload(mod);
+    return -3;
+  }
+  d.getattr(&jm.regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f);
+  jm.module = mod;
+  jm.func = f;
+  return 0;
+}
+
+std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value) {
+  return gen_ptx(p, rowptr, colidx, value);
+}
+
+void jit_free(JitModule& jm) {
+  if (jm.module && driver().ok) driver().unload(static_cast<CUmodule>(jm.module));
+  jm.module = nullptr;
+  jm.func = nullptr;
+}
+
+int jit_launch(const JitModule& jm, const float* in, float* out, const float* bias, int relu, int N,
+               cudaStream_t s) {
+  const JitPlan& p = jm.plan;
+  const int NR = cdiv(N, p.mos);
+  const int64_t slots = (int64_t(NR - 1) * (p.H + p.pad) + p.H) * p.SWs;
+  const int64_t tiles = (slots + p.T - 1) / p.T;
+  if (tiles > 0x7fffffff || slots + p.L > 0x7fffffff) return -1;
+  unsigned relu_u = relu ? 1u : 0u, n_u = unsigned(N);
+  const void* a_in = in;
+  void* a_out = out;
+  const void* a_bias = bias;
+  void* args[] = {&a_in, &a_out, &a_bias, &relu_u, &n_u};
+  const CUresult r = driver().launch(static_cast<CUfunction>(jm.func), unsigned(tiles), unsigned(p.nmg), 1,
+                                     unsigned(p.warps * 32), 1, 1, unsigned(p.smem_bytes), (CUstream)s, args,
+                                     nullptr);
+  return r == CUDA_SUCCESS ? 0 : -1;
+}
+
+}  // namespace escoin

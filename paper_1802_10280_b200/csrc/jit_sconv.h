@@ -1,0 +1,48 @@
+// jit_sconv.h — pattern-specialised sconv kernels (jit_sconv.cpp). Internal, not ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace escoin {
+
+struct JitPlan {
+  // tunables (<= 0: default)
+  int Q = 0;      // output channels per CTA (rows of one m-group)
+  int P = 0;      // pixels per lane (slots 32 apart)
+  int CC = 0;     // input channels per pipeline stage
+  int NS = 0;     // pipeline stages
+  int warps = 0;  // warps per CTA
+  int minb = 0;   // CTAs per SM the register budget is compiled for
+  // layer
+  int C = 0, H = 0, W = 0, M = 0, K = 0, pad = 0, E = 0, F = 0;
+  // derived
+  int mos = 1;    // images per mosaic super-row
+  int SWs = 0;    // super-image row stride (words)
+  int T = 0;      // slots per CTA
+  int L = 0, Ls = 0;  // staged words per channel (and padded stride)
+  int KS = 0;     // staging slots per thread
+  int nmg = 0, nch = 0;
+  int smem_bytes = 0;
+};
+
+struct JitModule {
+  JitPlan plan;
+  void* module = nullptr;  // CUmodule
+  void* func = nullptr;    // CUfunction
+  int regs = 0;
+  size_t ptx_bytes = 0, cubin_bytes = 0;
+};
+
+// 0 = supported (plan filled), < 0 = this layer has no JIT form (stride != 1, 2*pad != K-1, smem).
+int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad, int n_hint);
+// Generate, compile and load; 0 = OK. log receives the compiler error log on failure.
+int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
+              std::string* log);
+std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value);
+void jit_free(JitModule& jm);
+int jit_launch(const JitModule& jm, const float* in, float* out, const float* bias, int relu, int N,
+               cudaStream_t s);
+
+}  // namespace escoin

@@ -24,6 +24,7 @@ OK = 0
 ERR_NULL, ERR_SHAPE, ERR_CSR_MISMATCH, ERR_NOT_ON_DEVICE = -1, -2, -3, -4
 ERR_OVERFLOW, ERR_UNSUPPORTED, ERR_ALLOC, ERR_CUDA = -5, -6, -7, -8
 KERNEL_AUTO = -1
+KERNEL_JIT = 1000  # the handle's pattern-specialised kernel (escoin_csr_jit)
 
 # Every symbol include/escoin.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -31,7 +32,7 @@ EXPORTS = [
     "escoin_csr_wrap_device", "escoin_csr_free", "escoin_sconv_forward", "escoin_sconv_forward_hostio",
     "escoin_kernel_count", "escoin_kernel_info", "escoin_csr_set_kernel", "escoin_csr_get_kernel",
     "escoin_status_string", "escoin_version", "escoin_csr_autotune", "escoin_csr_stretch_device",
-    "escoin_bench_dense_tc_forward",
+    "escoin_bench_dense_tc_forward", "escoin_csr_jit", "escoin_csr_jit_info",
 ]
 
 
@@ -75,6 +76,8 @@ def lib():
             L.escoin_csr_get_kernel.argtypes = [vp, ip]
             L.escoin_csr_autotune.argtypes = [vp, ci, vp, vp, vp, ci, ci, vp, ip, ctypes.POINTER(ctypes.c_float)]
             L.escoin_bench_dense_tc_forward.argtypes = [ci] * 8 + [vp, vp, vp, vp, ci, ci, vp]
+            L.escoin_csr_jit.argtypes = [vp, ci, ip, ci]
+            L.escoin_csr_jit_info.argtypes = [vp, ip, ip, ip, ctypes.POINTER(cl)]
             L.escoin_status_string.argtypes = [ci]
             L.escoin_status_string.restype = ctypes.c_char_p
             L.escoin_version.restype = ctypes.c_char_p
@@ -183,6 +186,22 @@ class Csr:
                                                                 1 if relu else 0, reps, stream, ctypes.byref(bid),
                                                                 ctypes.byref(bms)))
         return bid.value, bms.value
+
+    def jit(self, n_hint=128, Q=0, P=0, CC=0, NS=0, warps=0, minb=0) -> "Csr":
+        """escoin_csr_jit: compile this layer's pattern-specialised kernel and select it."""
+        tun = (ctypes.c_int * 6)(Q, P, CC, NS, warps, minb)
+        _check("escoin_csr_jit", lib().escoin_csr_jit(self._h, n_hint, tun, 6))
+        return self
+
+    def jit_info(self):
+        """dict(Q, P, CC, NS, warps, minb, mos, regs, code_bytes) of the specialised kernel."""
+        tun = (ctypes.c_int * 6)()
+        mos, regs, code = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+        _check("escoin_csr_jit_info", lib().escoin_csr_jit_info(self._h, tun, ctypes.byref(mos), ctypes.byref(regs),
+                                                                ctypes.byref(code)))
+        d = dict(zip(["Q", "P", "CC", "NS", "warps", "minb"], list(tun)))
+        d.update(mos=mos.value, regs=regs.value, code_bytes=code.value)
+        return d
 
     def free(self):
         if self._h.value:

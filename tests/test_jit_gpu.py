@@ -1,0 +1,166 @@
+"""GPU parity of the pattern-specialised kernel (escoin_csr_jit, jit_sconv.cpp).
+
+Same tolerance as tests/test_sconv_gpu.py (reading R#11) against the fp64
+oracle, plus bitwise identity with the paper-mapping kernel (variant 0): the
+specialised kernel performs the same fp32 FMAs in the same ascending
+(c, kh, kw) order from 0.0f (R#10), so it must produce the same bits.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1802_10280_b200 import escoin, inputs, workloads
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def oracle_ref(w, x, bias, stride, pad, relu):
+    M, C, K, _ = w.shape
+    rp, ci, v = oracle.csr_stretch(w, x.shape[2], x.shape[3], stride, pad)
+    return oracle.sconv(x, rp, ci, v, M, K, stride, pad, bias=bias, relu=relu)
+
+
+def check(out, ref, scale, bias):
+    b = 0.0 if bias is None else np.abs(bias.astype(np.float64))[None, :, None, None]
+    err = np.abs(out.astype(np.float64) - ref)
+    bound = TOL * (scale + b)
+    assert not (err > bound).any(), "max err ratio %.3g" % np.max(err / np.maximum(bound, 1e-300))
+
+
+def fwd(csr, x, b, relu):
+    dx = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    db = None if b is None else torch.from_numpy(b).cuda()
+    out = escoin.forward(csr, dx, bias=db, relu=relu)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def jit_and_paper(w, x, b, pad, relu, n_hint=0, **tun):
+    N, C, H, W = x.shape
+    csr = escoin.Csr.stretch(w, H, W, 1, pad).to_device(0)
+    csr.jit(n_hint=n_hint or N, **tun)
+    assert csr.kernel() == escoin.KERNEL_JIT
+    out = fwd(csr, x, b, relu)
+    csr.set_kernel(0)
+    paper = fwd(csr, x, b, relu)
+    return out, paper, csr
+
+
+@pytest.mark.parametrize("relu", [False, True])
+@pytest.mark.parametrize("with_bias", [False, True])
+def test_tiny(relu, with_bias):
+    L = workloads.TINY
+    x = inputs.activations("tiny", "tiny", 0, 1, L.C, L.H, L.W)
+    w = inputs.layer_weights("tiny", L, 800)
+    b = inputs.bias("tiny", "tiny", L.M) if with_bias else None
+    ref, scale = oracle_ref(w, x, b, L.stride, L.pad, relu)
+    out, paper, _ = jit_and_paper(w, x, b, L.pad, relu)
+    check(out, ref, scale, b)
+    assert out.tobytes() == paper.tobytes()
+
+
+GRID = [  # N, C, H, W, M, K, pad, density — stride 1, "same" padding
+    (2, 5, 14, 14, 9, 3, 1, 0.3), (3, 16, 13, 13, 40, 3, 1, 0.2), (1, 7, 27, 27, 33, 5, 2, 0.2),
+    (2, 3, 9, 17, 5, 5, 2, 0.5), (4, 20, 7, 7, 17, 3, 1, 0.2), (2, 9, 28, 28, 12, 3, 1, 0.2),
+    (1, 12, 56, 56, 8, 3, 1, 0.15), (3, 11, 10, 12, 13, 1, 0, 0.3), (5, 2, 5, 6, 3, 3, 1, 1.0),
+    (2, 33, 14, 14, 131, 3, 1, 0.1), (1, 1, 4, 4, 1, 3, 1, 1.0), (7, 9, 6, 9, 70, 3, 1, 0.25),
+    (3, 37, 7, 7, 26, 1, 0, 0.2), (9, 13, 13, 13, 65, 3, 1, 0.2),
+]
+TUNINGS = [dict(), dict(Q=16, P=2, CC=3, NS=2), dict(Q=32, P=3, CC=5, NS=4, warps=4, minb=3),
+           dict(Q=8, P=1, CC=1, NS=2, warps=2, minb=1)]
+
+
+@pytest.mark.parametrize("tun", range(len(TUNINGS)))
+@pytest.mark.parametrize("case", GRID)
+def test_parity_grid(case, tun):
+    N, C, H, W, M, K, p, d = case
+    rng = np.random.default_rng(abs(hash(case)) % 2**32)
+    x = rng.random((N, C, H, W)).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= d] = 0.0
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    ref, scale = oracle_ref(w, x, b, 1, p, True)
+    out, paper, _ = jit_and_paper(w, x, b, p, True, **TUNINGS[tun])
+    check(out, ref, scale, b)
+    assert out.tobytes() == paper.tobytes()
+
+
+def test_batch_other_than_hint_and_empty_rows():
+    rng = np.random.default_rng(3)
+    N, C, H, M = 11, 10, 13, 30
+    x = rng.random((N, C, H, H)).astype(np.float32)
+    w = rng.standard_normal((M, C, 3, 3)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.2] = 0.0
+    w[[0, 7, 29]] = 0.0  # empty rows: output = bias
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    csr = escoin.Csr.stretch(w, H, H, 1, 1).to_device(0)
+    csr.jit(n_hint=128, Q=16)
+    ref, scale = oracle_ref(w, x, b, 1, 1, False)
+    for n0, n1 in [(0, 11), (3, 4), (2, 9)]:
+        out = fwd(csr, x[n0:n1], b, False)
+        check(out, ref[n0:n1], scale[n0:n1], b)
+
+
+def test_exact_integer_regime():
+    rng = np.random.default_rng(11)
+    N, C, H, M = 3, 12, 14, 24
+    x = rng.integers(0, 4, (N, C, H, H)).astype(np.float32)
+    w = rng.integers(-3, 4, (M, C, 3, 3)).astype(np.float32)
+    b = rng.integers(-3, 4, M).astype(np.float32)
+    ref, _ = oracle_ref(w, x, b, 1, 1, True)
+    out, _, _ = jit_and_paper(w, x, b, 1, True)
+    assert np.array_equal(out.astype(np.float64), ref)
+
+
+def test_unsupported_shapes_rejected():
+    w = np.ones((4, 3, 3, 3), np.float32)
+    for stride, pad in [(2, 1), (1, 0), (1, 2)]:
+        csr = escoin.Csr.stretch(w, 9, 9, stride, pad).to_device(0)
+        with pytest.raises(escoin.EscoinError) as e:
+            csr.jit()
+        assert e.value.status == escoin.ERR_UNSUPPORTED
+        assert csr.kernel() != escoin.KERNEL_JIT  # the previous kernel stays selected
+
+
+@pytest.mark.parametrize("wl,name", [("alexnet", "conv3"), ("alexnet", "conv2"), ("resnet50", "res2a_branch2b"),
+                                     ("googlenet", "inception_4a/5x5")])
+def test_full_batch_sampled(wl, name):
+    # BASELINE full size (N=128) with the default plan bench.py uses; sampled outputs vs oracle,
+    # and bitwise identity with the autotuned interpreter kernel on the whole tensor.
+    W = workloads.workload(wl)
+    L = [l for l in W.layers if l.name == name][0]
+    x = inputs.activations(W.net, L.name, 0, 128, L.C, L.H, L.W)
+    w = inputs.layer_weights(W.net, L, W.sparsity_permille)
+    b = inputs.bias(W.net, L.name, L.M)
+    csr = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad).to_device(0)
+    auto = fwd(csr, x, b, True)
+    csr.jit(n_hint=128)
+    out = fwd(csr, x, b, True)
+    assert out.tobytes() == auto.tobytes()
+    rng = np.random.default_rng(5)
+    npts = 3000
+    coords = np.stack([rng.integers(0, 128, npts), rng.integers(0, L.M, npts), rng.integers(0, L.E, npts),
+                       rng.integers(0, L.F, npts)], 1)
+    rp, ci, v = oracle.csr_stretch(w, L.H, L.W, L.stride, L.pad)
+    ref, scale = oracle.sconv_points(x, rp, ci, v, L.M, L.K, L.stride, L.pad, coords, bias=b, relu=True)
+    got = out[coords[:, 0], coords[:, 1], coords[:, 2], coords[:, 3]].astype(np.float64)
+    assert np.all(np.abs(got - ref) <= TOL * (scale + np.abs(b[coords[:, 1]])))
+
+
+def test_autotune_considers_jit():
+    L = workloads.TINY
+    x = inputs.activations("tiny", "tiny", 0, 4, L.C, L.H, L.W)
+    w = inputs.layer_weights("tiny", L, 800)
+    csr = escoin.Csr.stretch(w, L.H, L.W, 1, 1).to_device(0)
+    ref = fwd(csr, x, None, True)
+    csr.jit(n_hint=4)
+    dx = torch.from_numpy(x).cuda()
+    out = torch.empty((4, L.M, L.E, L.F), device="cuda")
+    kid, ms = csr.autotune(4, dx, out, None, True, 2, torch.cuda.current_stream().cuda_stream)
+    assert ms > 0 and csr.kernel() == kid
+    assert fwd(csr, x, None, True).tobytes() == ref.tobytes()
+    info = csr.jit_info()
+    assert info["regs"] > 0 and info["code_bytes"] > 0 and info["Q"] > 0
