@@ -22,6 +22,7 @@ import subprocess
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -53,6 +54,7 @@ def parse():
     p.add_argument("--sparsity", type=int, default=800, help="per-mille (ASSUMED 800, reading R#14)")
     p.add_argument("--kernel", type=int, default=-1, help="sconv variant id (-1 = auto)")
     p.add_argument("--no-autotune", action="store_true", help="skip escoin_csr_autotune at setup")
+    p.add_argument("--no-jit", action="store_true", help="skip the pattern-specialised kernels (escoin_csr_jit)")
     p.add_argument("--no-baselines", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -160,15 +162,36 @@ def setup(args, wl, device, rank, world, torch, escoin):
         r.x = r.h_x.to(device)
         r.out = torch.empty((B, L.M, L.E, L.F), dtype=torch.float32, device=device)
         r.tune = None
-        if args.kernel == -1 and not args.no_autotune:
-            # kernel customization (paper §3.4): measured once at setup, untimed
-            kid, kms = r.csr.autotune(B, r.x, r.out, r.bias, True, 3, torch.cuda.current_stream().cuda_stream)
-            r.tune = {"kernel_id": kid, "ms": round(kms, 4)}
-        r.kernel = escoin.kernels()[r.csr.kernel()][1]
         r.h_out = torch.empty((B, L.M, L.E, L.F), dtype=torch.float32).pin_memory()
         r.flops = 2.0 * B * r.nnz * L.E * L.F
         r.alg_bytes = 4.0 * (B * L.C * L.H * L.W + B * L.M * L.E * L.F + 2 * r.nnz + L.M + 1 + L.M)
         runs.append(r)
+    torch.cuda.synchronize()
+    if args.kernel == -1 and not args.no_jit:
+        # pattern-specialised kernels (escoin_csr_jit): compiled once at setup, untimed, one host
+        # thread per layer (the library releases the GIL; compile time grows with nnz)
+        def jit(r):
+            t0 = time.time()
+            try:
+                r.csr.jit(B)
+            except escoin.EscoinError as e:
+                if e.status != escoin.ERR_UNSUPPORTED:
+                    raise
+                return None
+            return round(time.time() - t0, 2)
+        with ThreadPoolExecutor(max(1, min(len(runs), os.cpu_count() or 1))) as ex:
+            for r, t in zip(runs, ex.map(jit, runs)):
+                r.jit_s = t
+    for r in runs:
+        if args.kernel == -1 and not args.no_autotune:
+            # kernel customization (paper §3.4): measured once at setup, untimed; includes the
+            # pattern-specialised kernel when one was compiled
+            kid, kms = r.csr.autotune(B, r.x, r.out, r.bias, True, 3, torch.cuda.current_stream().cuda_stream)
+            r.tune = {"kernel_id": kid, "ms": round(kms, 4)}
+        r.kernel = escoin.kernel_name(r.csr.kernel())
+        if r.csr.kernel() == escoin.KERNEL_JIT:
+            ji = r.csr.jit_info()
+            r.kernel = "jit_q%d_p%d_w%d" % (ji["Q"], ji["P"], ji["warps"])
     torch.cuda.synchronize()
     return runs, B
 
@@ -385,6 +408,7 @@ def main():
     for r, ms, mn, md in zip(runs, layer_ms, layer_ms_min, layer_ms_med):
         layers_out.append({"layer": r.L.name, "ms": round(float(ms), 5), "ms_min": round(float(mn), 5),
                            "ms_median": round(float(md), 5), "kernel": r.kernel, "nnz": r.nnz,
+                           "jit_compile_s": getattr(r, "jit_s", None),
                            "gflop": round(r.flops / 1e9, 4),
                            "tflops": round(r.flops / (ms / 1e3) / 1e12, 3),
                            "frac_fp32": round(r.flops / (ms / 1e3) / 1e12 / peak_tf, 4),

@@ -869,7 +869,9 @@ int build_jit(escoin_csr* h, int n_hint, const int* tun) {
     p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5];
   }
   if (p.P > 8 || p.Q > 256 || p.CC > 64 || p.NS > 6 || p.warps > 32 || p.minb > 8) return ESCOIN_ERR_UNSUPPORTED;
-  if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint) != 0) return ESCOIN_ERR_UNSUPPORTED;
+  const double density = double(h->nnz) / (double(h->M) * h->C * h->K * h->K);
+  if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint, density) != 0)
+    return ESCOIN_ERR_UNSUPPORTED;
   if (int64_t(p.warps) * 32 * p.minb > 2048) return ESCOIN_ERR_UNSUPPORTED;
   if (h->rowptr.size() != size_t(h->M) + 1) return ESCOIN_ERR_UNSUPPORTED;
   JitModule* jm = new (std::nothrow) JitModule();

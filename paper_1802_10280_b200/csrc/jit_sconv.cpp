@@ -36,6 +36,7 @@
 #include <nvPTXCompiler.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -173,6 +174,8 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o(".target sm_100a");
   o(".address_size 64");
   o(".extern .shared .align 16 .b8 smem[];");
+  const size_t table_pos = o.s.size();
+  std::string mgr_table;
   o(".visible .entry escoin_jit_sconv(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
     ".param .u32 p_relu, .param .u32 p_N)");
   o(".maxntid %d, 1, 1", NT);
@@ -180,7 +183,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("{");
   o(".reg .pred %%p<%d>;", 16 + 2 * p.KS + P);
   o(".reg .b32 %%r<%d>;", 64 + 4 * p.KS + 8 * P);
-  o(".reg .b64 %%rd<%d>;", 32 + 2 * p.KS + 2 * P);
+  o(".reg .b64 %%rd<%d>;", 32 + 2 * p.KS + 2 * P + p.KS);
   o(".reg .f32 %%a<%d>;", Q * P);
   o(".reg .f32 %%x<%d>;", KK * P);
   o(".reg .f32 %%v<8>;");
@@ -240,31 +243,73 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("add.s64 %%rd%d, %%rd%d, %%rd0;", 32 + k, 32 + k);
   }
   // stage(chunk register rc, buffer byte offset register rb): r11 = chunk, r12 = buffer offset
+  // Per (channel, slot) one cp.async; the channel offset and the stage offset are immediates
+  // or hoisted per slot, predicates only where a chunk or the slot range is ragged.
+  const bool ragged_c = p.C % p.CC != 0;
   auto stage = [&](const char* rc, const char* rb) {
     o("mul.wide.u32 %%rd3, %s, %d;", rc, p.CC * HW * 4);
-    o("mul.lo.u32 %%r13, %s, %d;", rc, p.CC);
-    o("sub.s32 %%r13, %d, %%r13;", p.C);  // channels left
+    if (ragged_c) {
+      o("mul.lo.u32 %%r13, %s, %d;", rc, p.CC);
+      o("sub.s32 %%r13, %d, %%r13;", p.C);  // channels left
+    }
+    for (int k = 0; k < p.KS; ++k) {
+      o("add.u32 %%r%d, %%r%d, %s;", 64 + 2 * p.KS + k, 64 + k, rb);
+      o("add.s64 %%rd%d, %%rd%d, %%rd3;", 32 + p.KS + P + k, 32 + k);
+    }
     for (int cc = 0; cc < p.CC; ++cc) {
-      o("setp.gt.s32 %%p1, %%r13, %d;", cc);
+      if (ragged_c) o("setp.gt.s32 %%p1, %%r13, %d;", cc);
       for (int k = 0; k < p.KS; ++k) {
-        o("and.pred %%p2, %%p1, %%p%d;", 16 + k);
-        o("add.u32 %%r14, %%r%d, %s;", 64 + k, rb);
-        o("add.s64 %%rd4, %%rd%d, %%rd3;", 32 + k);
-        o("@%%p2 cp.async.ca.shared.global [%%r14+%d], [%%rd4+%d], 4, %%r%d;", cc * p.Ls * 4, cc * HW * 4,
-          64 + p.KS + k);
+        const bool ragged_k = (k + 1) * NT > p.L;
+        std::string pred;
+        if (ragged_c && ragged_k) {
+          o("and.pred %%p2, %%p1, %%p%d;", 16 + k);
+          pred = "@%p2 ";
+        } else if (ragged_c) {
+          pred = "@%p1 ";
+        } else if (ragged_k) {
+          pred = "@%p" + std::to_string(16 + k) + " ";
+        }
+        o("%scp.async.ca.shared.global [%%r%d+%d], [%%rd%d+%d], 4, %%r%d;", pred.c_str(), 64 + 2 * p.KS + k,
+          cc * p.Ls * 4, 32 + p.KS + P + k, cc * HW * 4, 64 + p.KS + k);
       }
     }
   };
   for (int q = 0; q < Q * P; ++q) o("mov.f32 %%a%d, 0f00000000;", q);
+  // Active chunk range per m-group (grouped layers: an m-group touches only its group's
+  // channels; empty groups run no chunk at all and store bias only).
+  std::vector<int> klo(p.nmg, 0), khi(p.nmg, 0);
+  for (int g = 0; g < p.nmg; ++g) {
+    int lo = p.nch, hi = 0;
+    for (int c = 0; c < p.C; ++c)
+      if (!lists[size_t(g) * p.C + c].empty()) {
+        lo = std::min(lo, c / p.CC);
+        hi = std::max(hi, c / p.CC + 1);
+      }
+    if (lo < hi) { klo[g] = lo; khi[g] = hi; }
+  }
+  {
+    std::string tbl;
+    for (int g = 0; g < p.nmg; ++g) tbl += (g ? ", " : "") + std::to_string(klo[g]) + ", " + std::to_string(khi[g]);
+    // (declared at module scope below via a placeholder replaced after generation)
+    mgr_table = tbl;
+  }
+  o("mov.u64 %%rd8, mgr;");
+  o("mul.wide.u32 %%rd9, %%r4, 8;");
+  o("add.s64 %%rd8, %%rd8, %%rd9;");
+  o("ld.global.nc.u32 %%r20, [%%rd8];");    // k_lo
+  o("ld.global.nc.u32 %%r21, [%%rd8+4];");  // k_hi
   for (int s = 0; s < p.NS - 1; ++s) {
-    if (s < p.nch) {
-      o("mov.u32 %%r11, %d;", s);
-      o("mov.u32 %%r12, %d;", s * p.CC * p.Ls * 4);
-      stage("%r11", "%r12");
-    }
+    o("add.u32 %%r11, %%r20, %d;", s);
+    o("setp.ge.u32 %%p3, %%r11, %%r21;");
+    o("@%%p3 bra.uni PRO%d;", s);
+    o("mov.u32 %%r12, %d;", s * p.CC * p.Ls * 4);
+    stage("%r11", "%r12");
+    o("PRO%d:", s);
     o("cp.async.commit_group;");
   }
-  o("mov.u32 %%r15, 0;");  // k
+  o("mov.u32 %%r15, %%r20;");  // k
+  o("setp.ge.u32 %%p3, %%r15, %%r21;");
+  o("@%%p3 bra.uni EPI;");
   o("mov.u32 %%r16, %d;", (p.NS - 1) * p.CC * p.Ls * 4);  // buffer offset of chunk k + NS - 1
   // branch targets
   std::string tg = "ts: .branchtargets ";
@@ -279,7 +324,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("cp.async.wait_group %d;", p.NS - 2);
   o("bar.sync 0;");
   o("add.u32 %%r11, %%r15, %d;", p.NS - 1);
-  o("setp.ge.u32 %%p3, %%r11, %d;", p.nch);
+  o("setp.ge.u32 %%p3, %%r11, %%r21;");
   o("@%%p3 bra.uni NOSTAGE;");
   stage("%r11", "%r16");
   o("NOSTAGE:");
@@ -293,7 +338,11 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   for (int g = 0; g < p.nmg; ++g)
     for (int k = 0; k < p.nch; ++k) {
       o("B%d_%d:", g, k);
-      const int buf = k % p.NS;
+      if (k < klo[g] || k >= khi[g]) {  // never entered
+        o("bra.uni NEXT;");
+        continue;
+      }
+      const int buf = (k - klo[g]) % p.NS;
       for (int cc = 0; cc < p.CC; ++cc) {
         const int c = k * p.CC + cc;
         if (c >= p.C) break;
@@ -316,8 +365,9 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     }
   o("NEXT:");
   o("add.u32 %%r15, %%r15, 1;");
-  o("setp.lt.u32 %%p5, %%r15, %d;", p.nch);
+  o("setp.lt.u32 %%p5, %%r15, %%r21;");
   o("@%%p5 bra.uni LOOP;");
+  o("EPI:");
   // epilogue
   o("setp.ne.u64 %%p6, %%rd2, 0;");
   o("setp.ne.u32 %%p7, %%r0, 0;");
@@ -369,23 +419,50 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   }
   o("ret;");
   o("}");
+  o.s.insert(table_pos, ".global .align 8 .u32 mgr[" + std::to_string(2 * p.nmg) + "] = {" + mgr_table + "};\n");
   return o.s;
 }
 
 }  // namespace
 
-int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad, int n_hint) {
+int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad, int n_hint, double density) {
   if (stride != 1 || 2 * pad != K - 1 || K > 7) return -1;
   p.C = C; p.H = H; p.W = W; p.M = M; p.K = K; p.pad = pad;
   p.E = H; p.F = W;
-  if (p.Q <= 0) p.Q = 64;
   if (p.P <= 0) p.P = 1;
   if (p.CC <= 0) p.CC = 8;
   if (p.NS <= 1) p.NS = 3;
-  if (p.warps <= 0) p.warps = 8;
-  if (p.minb <= 0) p.minb = 2;
-  p.Q = std::min(p.Q, M);
-  plan_geometry(p, std::max(1, n_hint));
+  n_hint = std::max(1, n_hint);
+  if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0) {
+    // Shape choice by a small model: CTAs of 16 warps, one per SM, keep every warp of an SM on
+    // the same code (one instruction stream in the SM's instruction caches: measured +20% over
+    // two 8-warp CTAs on AlexNet conv3); Q trades FFMAs per input load against grid fill.
+    static const int cand[][3] = {{64, 16, 1}, {32, 16, 1}, {64, 8, 2}, {32, 8, 2}, {16, 16, 1}, {16, 8, 2}};
+    double best = -1;
+    JitPlan keep = p;
+    for (const auto& c : cand) {
+      JitPlan t = keep;
+      t.Q = std::min(c[0], M); t.warps = c[1]; t.minb = c[2];
+      plan_geometry(t, n_hint);
+      if (t.smem_bytes > 227 * 1024 / t.minb) continue;
+      const int NR = cdiv(n_hint, t.mos);
+      const double slots = (double(NR - 1) * (H + pad) + H) * t.SWs;
+      const double ctas = double(cdiv(int(std::min(slots, 2e9)), t.T)) * t.nmg, per_wave = 148.0 * t.minb;
+      const double wave_eff = ctas / (std::ceil(ctas / per_wave) * per_wave);
+      const double fma = t.Q * K * K * density;
+      const double taps = K * K * (1.0 - std::pow(1.0 - density, t.Q));
+      const double instr_eff = fma / (fma + taps + 2.0 * t.L / t.T);
+      const double score = wave_eff * instr_eff * (t.minb == 1 ? 1.0 : 0.85);
+      if (score > best) { best = score; p = t; }
+    }
+    if (best < 0) return -1;
+  } else {
+    if (p.Q <= 0) p.Q = 64;
+    if (p.warps <= 0) p.warps = 16;
+    if (p.minb <= 0) p.minb = 1;
+    p.Q = std::min(p.Q, M);
+    plan_geometry(p, n_hint);
+  }
   if (p.smem_bytes > 227 * 1024 / p.minb) return -1;
   if (int64_t(p.SWs) * (p.H + p.pad) * ((n_hint + p.mos - 1) / p.mos + 1) > (int64_t(1) << 30)) return -1;
   return 0;

@@ -36,7 +36,7 @@ struct JitModule {
 };
 
 // 0 = supported (plan filled), < 0 = this layer has no JIT form (stride != 1, 2*pad != K-1, smem).
-int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad, int n_hint);
+int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad, int n_hint, double density);
 // Generate, compile and load; 0 = OK. log receives the compiler error log on failure.
 int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
               std::string* log);

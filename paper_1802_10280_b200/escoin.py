@@ -108,6 +108,13 @@ def kernels():
     return out
 
 
+def kernel_name(kernel_id: int) -> str:
+    """Name of a kernel id as returned by Csr.kernel() (variants, or "jit" for KERNEL_JIT)."""
+    if kernel_id == KERNEL_JIT:
+        return "jit"
+    return kernels()[kernel_id][1]
+
+
 class Csr:
     """Owning wrapper of an escoin_csr* handle (one pruned, stretched layer)."""
 

@@ -164,3 +164,23 @@ def test_autotune_considers_jit():
     assert fwd(csr, x, None, True).tobytes() == ref.tobytes()
     info = csr.jit_info()
     assert info["regs"] > 0 and info["code_bytes"] > 0 and info["Q"] > 0
+
+
+@pytest.mark.parametrize("tun", [dict(), dict(Q=8, CC=3, NS=2, warps=4, minb=2), dict(Q=16, CC=5, NS=4)])
+def test_grouped_block_diagonal_and_empty_groups(tun):
+    # block-diagonal expansion of a g=3 grouped layer (R#18): every m-group touches a channel
+    # sub-range only (the kernel skips the other chunks); one whole group of rows is empty
+    rng = np.random.default_rng(21)
+    N, C, H, M, g = 3, 24, 9, 48, 3
+    x = rng.random((N, C, H, H)).astype(np.float32)
+    w = np.zeros((M, C, 3, 3), np.float32)
+    for k in range(g):
+        blk = rng.standard_normal((M // g, C // g, 3, 3)).astype(np.float32)
+        blk[rng.random(blk.shape) >= 0.3] = 0.0
+        w[k * M // g:(k + 1) * M // g, k * C // g:(k + 1) * C // g] = blk
+    w[16:32] = 0.0
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    ref, scale = oracle_ref(w, x, b, 1, 1, True)
+    out, paper, _ = jit_and_paper(w, x, b, 1, True, **tun)
+    check(out, ref, scale, b)
+    assert out.tobytes() == paper.tobytes()

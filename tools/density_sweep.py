@@ -51,7 +51,7 @@ def main(batch=128):
         t_esc = timeit(lambda: escoin.sconv_forward(batch, L.C, L.H, L.W, L.M, L.K, L.stride, L.pad, csr, x, out,
                                                     bias, True, s), flush)
         y = torch.empty_like(out)
-        r = {"density": dpm / 1000.0, "nnz": nnz, "escoin_ms": t_esc, "escoin_kernel": escoin.kernels()[kid][1],
+        r = {"density": dpm / 1000.0, "nnz": nnz, "escoin_ms": t_esc, "escoin_kernel": escoin.kernel_name(kid),
              "escoin_tflops": 2.0 * batch * nnz * L.E * L.F / t_esc / 1e9}
         for mode in ["cublas", "cusparse"]:
             op = bl.LoweredConv(L, w, b_np, dev, mode)

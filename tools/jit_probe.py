@@ -51,7 +51,7 @@ def main():
             kid = csr.kernel()
         ms = timeit(lambda: escoin.forward(csr, x, bias=b, relu=True, out=out))
         ref = out.clone()
-        print(json.dumps(dict(layer=L.name, cand="auto:" + escoin.kernels()[kid][1], ms=round(ms, 4),
+        print(json.dumps(dict(layer=L.name, cand="auto:" + escoin.kernel_name(kid), ms=round(ms, 4),
                               tflops=round(flop / ms / 1e9, 2))), flush=True)
         for t in tunings:
             t0 = time.time()

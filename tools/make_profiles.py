@@ -33,7 +33,12 @@ METRICS = [
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith("_raw.csv") or not os.path.exists(rep):
+        # exported on the GPU box (`ncu -i REP --page raw --csv`): the .ncu-rep of
+        # pattern-specialised kernels is too large to bring back
+        out = open(rep[:-len(".ncu-rep")] + "_raw.csv" if rep.endswith(".ncu-rep") else rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2:]
 
