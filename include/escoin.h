@@ -181,9 +181,10 @@ int escoin_csr_autotune(escoin_csr* csr, int N, const float* in, float* out, con
  * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
  *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
  *              forwards accept any N.
- *   tunables   NULL or ntunables (<= 6) ints {Q output channels per CTA,
+ *   tunables   NULL or ntunables (<= 7) ints {Q output channels per CTA,
  *              P pixels per lane, CC channels per stage, NS stages, warps per
- *              CTA, CTAs per SM}; <= 0 entries take the defaults.
+ *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off)};
+ *              <= 0 entries take the defaults.
  * On success the handle's kernel becomes ESCOIN_KERNEL_JIT.  Synchronous
  * (device-wide sync first); compile time grows with nnz (about 25 s for
  * 180k nonzeros on one host core).  Only stride 1 with "same" padding

@@ -320,6 +320,33 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
       tg += b;
     }
   tg += ";";
+  // Instruction prefetch pass (p.pf): the code of one m-group is hundreds of KB and, after
+  // an L2 flush, every CTA running that group would stall on the same sequential i-cache
+  // misses (ncu: no_instructions dominates). Before the main loop, warp w of each CTA runs
+  // ONE chunk block of its group (chunk ps + w, slices of `warps` chunks chosen by
+  // blockIdx.x) on whatever the stage buffers hold, then the accumulators are reset: the
+  // group's code streams into L2 from many warps and SMs in parallel, nothing is kept.
+  // (Guard predicates instead would make ptxas if-convert every FFMA into FFMA + FSEL.)
+  if (p.pf) {
+    std::string tp = tg;
+    tp[1] = 'p';  // "tp: .branchtargets ..."
+    o("setp.eq.u32 %%p12, %%r1, 0;");              // false at run time (N >= 1), opaque to ptxas
+    o("sub.u32 %%r23, %%r21, %%r20;");             // active chunks
+    o("add.u32 %%r25, %%r23, %d;", p.warps - 1);
+    o("div.u32 %%r25, %%r25, %d;", p.warps);       // slices
+    o("max.u32 %%r25, %%r25, 1;");
+    o("rem.u32 %%r26, %%r3, %%r25;");
+    o("mad.lo.u32 %%r26, %%r26, %d, %%r20;", p.warps);
+    o("add.u32 %%r26, %%r26, %%r8;");              // this warp's chunk
+    o("setp.ge.u32 %%p14, %%r26, %%r21;");
+    o("@%%p14 bra.uni PF_DONE;");
+    o("mad.lo.u32 %%r17, %%r4, %d, %%r26;", p.nch);
+    o("%s", tp.c_str());
+    o("brx.idx.uni %%r17, tp;");
+    o("PF_DONE:");
+    o("setp.ne.u32 %%p12, %%r1, 0;");              // true from here on
+    for (int q = 0; q < Q * P; ++q) o("mov.f32 %%a%d, 0f00000000;", q);
+  }
   o("LOOP:");
   o("cp.async.wait_group %d;", p.NS - 2);
   o("bar.sync 0;");
@@ -335,6 +362,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("mad.lo.u32 %%r17, %%r4, %d, %%r15;", p.nch);
   o("%s", tg.c_str());
   o("brx.idx.uni %%r17, ts;");
+  const char* pg = "";
   for (int g = 0; g < p.nmg; ++g)
     for (int k = 0; k < p.nch; ++k) {
       o("B%d_%d:", g, k);
@@ -354,16 +382,17 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
           if (!used[t]) continue;
           const int kh = t / p.K, kw = t % p.K;
           for (int j = 0; j < P; ++j)
-            o("ld.shared.f32 %%x%d, [%%r10+%d];", t * P + j,
+            o("%sld.shared.f32 %%x%d, [%%r10+%d];", pg, t * P + j,
               ((buf * p.CC + cc) * p.Ls + j * 32 + kh * p.SWs + kw) * 4);
         }
         for (const Nz& z : l)
           for (int j = 0; j < P; ++j)
-            o("fma.rn.f32 %%a%d, %%x%d, 0f%08X, %%a%d;", z.q * P + j, z.t * P + j, z.bits, z.q * P + j);
+            o("%sfma.rn.f32 %%a%d, %%x%d, 0f%08X, %%a%d;", pg, z.q * P + j, z.t * P + j, z.bits, z.q * P + j);
       }
       o("bra.uni NEXT;");
     }
   o("NEXT:");
+  if (p.pf) o("@!%%p12 bra.uni PF_DONE;");
   o("add.u32 %%r15, %%r15, 1;");
   o("setp.lt.u32 %%p5, %%r15, %%r21;");
   o("@%%p5 bra.uni LOOP;");
@@ -432,6 +461,7 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   if (p.P <= 0) p.P = 1;
   if (p.CC <= 0) p.CC = 8;
   if (p.NS <= 1) p.NS = 3;
+  p.pf = p.pf < 0 ? 0 : 1;
   n_hint = std::max(1, n_hint);
   if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0) {
     // Shape choice by a small model: CTAs of 16 warps, one per SM, keep every warp of an SM on

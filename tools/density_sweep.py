@@ -6,7 +6,9 @@ tcgen05 3xTF32 kernel); reports ms per layer and the crossover densities.
 Writes gpurun_out/density_sweep.json and gpurun_out/density_sweep.md.
 """
 import json
+import os
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import torch
@@ -43,16 +45,26 @@ def main(batch=128):
     out = torch.empty((batch, L.M, L.E, L.F), device=dev)
     s = torch.cuda.current_stream().cuda_stream
     rows = []
+    # pattern-specialised kernels: compiled for every density up front, in parallel host threads
+    ws = {dpm: inputs.layer_weights("alexnet", L, 1000 - dpm) for dpm in workloads.SWEEP_DENSITIES_PERMILLE}
+    jits = {dpm: escoin.Csr.stretch(ws[dpm], L.H, L.W, L.stride, L.pad).to_device(0) for dpm in ws}
+    with ThreadPoolExecutor(os.cpu_count() or 4) as ex:
+        list(ex.map(lambda c: c.jit(batch), jits.values()))
     for dpm in workloads.SWEEP_DENSITIES_PERMILLE:
-        w = inputs.layer_weights("alexnet", L, 1000 - dpm)
+        w = ws[dpm]
         csr = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad).to_device(0)
         nnz = csr.info()["nnz"]
         kid, _ = csr.autotune(batch, x, out, bias, True, 3, s)
-        t_esc = timeit(lambda: escoin.sconv_forward(batch, L.C, L.H, L.W, L.M, L.K, L.stride, L.pad, csr, x, out,
-                                                    bias, True, s), flush)
+        run = lambda c: escoin.sconv_forward(batch, L.C, L.H, L.W, L.M, L.K, L.stride, L.pad, c, x, out, bias,
+                                             True, s)
+        t_int = timeit(lambda: run(csr), flush)
+        t_jit = timeit(lambda: run(jits[dpm]), flush)
+        t_esc = min(t_int, t_jit)
         y = torch.empty_like(out)
-        r = {"density": dpm / 1000.0, "nnz": nnz, "escoin_ms": t_esc, "escoin_kernel": escoin.kernel_name(kid),
-             "escoin_tflops": 2.0 * batch * nnz * L.E * L.F / t_esc / 1e9}
+        r = {"density": dpm / 1000.0, "nnz": nnz, "escoin_ms": t_esc,
+             "escoin_kernel": "jit" if t_jit <= t_int else escoin.kernel_name(kid),
+             "escoin_tflops": 2.0 * batch * nnz * L.E * L.F / t_esc / 1e9,
+             "interpreter_ms": t_int, "interpreter_kernel": escoin.kernel_name(kid), "jit_ms": t_jit}
         for mode in ["cublas", "cusparse"]:
             op = bl.LoweredConv(L, w, b_np, dev, mode)
             r[mode + "_ms"] = timeit(lambda: op(x, y), flush)
@@ -67,6 +79,7 @@ def main(batch=128):
         rows.append(r)
         print(json.dumps(r), flush=True)
         csr.free()
+        jits[dpm].free()
     def crossover(key):
         for r in rows:
             if r["escoin_ms"] > r[key]:
@@ -80,12 +93,13 @@ def main(batch=128):
            "escoin_slower_than_tcgen05_3xtf32_from_density": crossover("tcgen05_3xtf32_ms")}
     json.dump(res, open("gpurun_out/density_sweep.json", "w"), indent=1)
     md = ["# Density sweep — %s" % res["layer"], "",
-          "| density | nnz | escoin ms (kernel) | escoin TFLOP/s | im2col+cuBLAS ms | im2col+cuSPARSE ms | cuDNN FP32 ms "
+          "| density | nnz | escoin ms (kernel) | escoin TFLOP/s | JIT ms | best interpreter ms (kernel) | im2col+cuBLAS ms | im2col+cuSPARSE ms | cuDNN FP32 ms "
           "| cuDNN TF32 ms | tcgen05 3xTF32 ms |",
-          "|---|---|---|---|---|---|---|---|---|"]
+          "|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
-        md.append("| %.2f | %d | %.3f (%s) | %.2f | %.3f | %.3f | %.3f | %.3f | %.3f |" % (
-            r["density"], r["nnz"], r["escoin_ms"], r["escoin_kernel"], r["escoin_tflops"], r["cublas_ms"],
+        md.append("| %.2f | %d | %.3f (%s) | %.2f | %.3f | %.3f (%s) | %.3f | %.3f | %.3f | %.3f | %.3f |" % (
+            r["density"], r["nnz"], r["escoin_ms"], r["escoin_kernel"], r["escoin_tflops"], r["jit_ms"],
+            r["interpreter_ms"], r["interpreter_kernel"], r["cublas_ms"],
             r["cusparse_ms"], r["cudnn_ms"], r["cudnn_tf32_ms"], r["tcgen05_3xtf32_ms"]))
     md += ["", "escoin slower than cuBLAS from density %s, than cuSPARSE from %s, than cuDNN FP32 from %s, "
            "than cuDNN TF32 from %s, than the tcgen05 3xTF32 kernel from %s (None = never)." % (

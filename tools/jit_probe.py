@@ -1,6 +1,6 @@
 """Per-layer timing of the pattern-specialised kernel against the autotuned interpreter kernels.
 
-python tools/jit_probe.py WORKLOAD [tuning ...]   tuning = Q,P,CC,NS,warps,minb (0 = default)
+python tools/jit_probe.py WORKLOAD [tuning ...]   tuning = Q,P,CC,NS,warps,minb,prefetch (0 = default)
 Prints one JSON line per (layer, candidate): ms, TFLOP/s, compile seconds, registers.
 """
 import json
@@ -15,10 +15,28 @@ import torch  # noqa: E402
 from paper_1802_10280_b200 import escoin, inputs, workloads  # noqa: E402
 
 
+_flush = None
+
+
 def timeit(fn, reps=10):
+    """Mean ms over reps; FLUSH=1: a 256 MB write before every rep (outside the events), as bench.py."""
+    global _flush
     s = torch.cuda.current_stream()
     fn()
     torch.cuda.synchronize()
+    if os.environ.get("FLUSH") == "1":
+        if _flush is None:
+            _flush = torch.empty(64 * 1024 * 1024, device="cuda")
+        tot = 0.0
+        for _ in range(reps):
+            _flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            fn()
+            e1.record(s)
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        return tot / reps
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
     for _ in range(reps):
@@ -30,7 +48,7 @@ def timeit(fn, reps=10):
 
 def main():
     wl = sys.argv[1]
-    tunings = [tuple(int(v) for v in a.split(",")) for a in sys.argv[2:]] or [(0,) * 6]
+    tunings = [tuple(int(v) for v in a.split(",")) for a in sys.argv[2:]] or [(0,) * 7]
     W = workloads.workload(wl)
     N = 128
     only = os.environ.get("LAYERS")
