@@ -160,7 +160,8 @@ int escoin_csr_get_kernel(const escoin_csr* csr, int* id);
 /* Measured kernel customization (§3.4 P:563-564 "the optimization space we
  * explore includes the grid shape and thread block size"): time every
  * compiled variant that accepts the handle's (K, stride) — including the
- * paper mapping — and, per variant, its best four modelled tilings (CTA
+ * paper mapping and every specialised kernel compiled by escoin_csr_jit —
+ * and, per variant, its best four modelled tilings (CTA
  * shape, mosaic width, channel chunk), on the caller's buffers (same meaning as
  * escoin_sconv_forward; `out` is overwritten), `reps` timed forwards each
  * after one warm-up, and keep the fastest.  Synchronous on cuda_stream.
@@ -185,10 +186,13 @@ int escoin_csr_autotune(escoin_csr* csr, int N, const float* in, float* out, con
  *              P pixels per lane, CC channels per stage, NS stages, warps per
  *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off)};
  *              <= 0 entries take the defaults.
- * On success the handle's kernel becomes ESCOIN_KERNEL_JIT.  Synchronous
- * (device-wide sync first); compile time grows with nnz (about 25 s for
- * 180k nonzeros on one host core).  Only stride 1 with "same" padding
- * (2*pad == K-1) has a specialised form.
+ * On success the new kernel is added to the handle's specialised kernels
+ * and selected (the handle's kernel becomes ESCOIN_KERNEL_JIT); earlier ones
+ * stay compiled until escoin_csr_free, and escoin_csr_autotune times all of
+ * them.  Thread-safe per handle (several tunings may compile concurrently);
+ * not concurrent with forwards on the same handle.  Compile time grows with
+ * nnz (about 20 s for 180k nonzeros on one host core).  Only stride 1 with
+ * "same" padding (2*pad == K-1) has a specialised form.
  * Errors: NULL, NOT_ON_DEVICE, UNSUPPORTED (shape, tunables, compile), CUDA (load). */
 #define ESCOIN_KERNEL_JIT 1000
 int escoin_csr_jit(escoin_csr* csr, int n_hint, const int* tunables, int ntunables);

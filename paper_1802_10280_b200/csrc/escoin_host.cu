@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -33,7 +34,9 @@ struct escoin_csr {
   int* d_sched = nullptr;
   int* d_sched_off = nullptr;
   TiledArgs targs{};  // pointers/tiling filled at DS-6 build; tensors per forward
-  JitModule* jit = nullptr;  // pattern-specialised kernel (escoin_csr_jit), kept until free
+  std::vector<JitModule*> jits;  // pattern-specialised kernels compiled for this handle (escoin_csr_jit)
+  JitModule* jit = nullptr;      // the selected one
+  std::mutex jit_mu;             // escoin_csr_jit may be called from several host threads
 };
 
 namespace {
@@ -881,10 +884,8 @@ int build_jit(escoin_csr* h, int n_hint, const int* tun) {
     delete jm;
     return rc == -2 ? ESCOIN_ERR_UNSUPPORTED : ESCOIN_ERR_CUDA;
   }
-  if (h->jit) {
-    jit_free(*h->jit);
-    delete h->jit;
-  }
+  std::lock_guard<std::mutex> lk(h->jit_mu);
+  h->jits.push_back(jm);
   h->jit = jm;
   return ESCOIN_OK;
 }
@@ -1129,9 +1130,9 @@ void escoin_csr_free(escoin_csr* h) {
     DeviceGuard g(h->device);
     cudaDeviceSynchronize();
     free_ds6(h);
-    if (h->jit) {
-      jit_free(*h->jit);
-      delete h->jit;
+    for (JitModule* jm : h->jits) {
+      jit_free(*jm);
+      delete jm;
     }
     if (!h->borrowed) {
       if (h->d_rowptr) cudaFree(h->d_rowptr);
@@ -1274,7 +1275,9 @@ int escoin_csr_autotune(escoin_csr* h, int N, const float* in, float* out, const
     ms /= reps;
     if (best < 0 || ms < best_t) { best = id; best_rank = rank; best_t = ms; }
   }
-  if (rc == ESCOIN_OK && h->jit) {  // the pattern-specialised kernel, when one was built (escoin_csr_jit)
+  JitModule* best_jit = h->jit;
+  for (size_t ji = 0; ji < h->jits.size() && rc == ESCOIN_OK; ++ji) {  // every compiled specialised kernel
+    h->jit = h->jits[ji];
     h->kernel = ESCOIN_KERNEL_JIT;
     rc = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
     cudaEventRecord(e0, s);
@@ -1285,8 +1288,9 @@ int escoin_csr_autotune(escoin_csr* h, int N, const float* in, float* out, const
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     ms /= reps;
-    if (rc == ESCOIN_OK && (best < 0 || ms < best_t)) { best = ESCOIN_KERNEL_JIT; best_t = ms; }
+    if (rc == ESCOIN_OK && (best < 0 || ms < best_t)) { best = ESCOIN_KERNEL_JIT; best_t = ms; best_jit = h->jit; }
   }
+  h->jit = best_jit;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (rc != ESCOIN_OK) return rc;
@@ -1306,10 +1310,8 @@ int escoin_csr_jit(escoin_csr* h, int n_hint, const int* tunables, int ntunables
   for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
   DeviceGuard g(h->device);
   if (!g.ok) return ESCOIN_ERR_CUDA;
-  cudaDeviceSynchronize();  // no forward may be running the kernel being replaced
-  const int rc = build_jit(h, n_hint > 0 ? n_hint : 128, tun);
+  const int rc = build_jit(h, n_hint > 0 ? n_hint : 128, tun);  // adds a module, frees none
   if (rc != ESCOIN_OK) return rc;
-  free_ds6(h);
   h->kernel = ESCOIN_KERNEL_JIT;
   return ESCOIN_OK;
 }

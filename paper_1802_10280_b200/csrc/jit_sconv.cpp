@@ -18,15 +18,17 @@
 // fma.rn.f32, then acc + bias[m] and ReLU — bit-identical to every other
 // variant (tested).
 //
-// Geometry (stride 1, "same" padding 2*pad == K-1): the batch is one mosaic
-// super-image (images on a grid of `mos` columns separated by `pad` zero
-// rows/columns, shared by neighbours); an output SLOT q = R*SWs + X of the
-// super-image reads the staged input at q + kh*SWs + kw, i.e. the stretched
-// offset f(0, kh, kw) of P:428 with the super-image row stride.  A CTA owns
-// T consecutive slots (lane l of warp w: slots q0 + (w*P + j)*32 + l), stages
-// [q0, q0 + T + (K-1)*(SWs+1)) of CC channels per pipeline stage with
-// 4-byte cp.async (zero-fill = the virtual padding, R#9), and blockIdx.y
-// selects the output-channel group of Q rows whose code it runs.
+// Geometry (stride 1, "same" padding 2*pad == K-1): a CTA owns T consecutive
+// output pixels g = (n*E + oh)*F + ow (lane l of warp w: g0 + (w*P + j)*32 + l,
+// no idle lanes) and blockIdx.y selects the output-channel group of Q rows whose
+// code it runs.  The input is staged in a stacked layout — images one above
+// the other, separated by `pad` zero rows shared by neighbours, row stride
+// SWs = W + 2*pad — where pixel g sits at pos(g) = (n*(H+pad) + oh)*SWs + ow and
+// reads tap (kh, kw) at pos(g) + kh*SWs + kw: the stretched offset f(0, kh, kw)
+// of P:428 with the stacked row stride, an immediate offset from the lane's
+// base register.  Per pipeline stage CC channels of the window
+// [pos(g0), pos(g0) + L) are copied with 4-byte cp.async (zero-fill = the
+// virtual padding, R#9).
 //
 // Compilation: PTX text -> nvPTXCompiler (static, in-process) -> cubin ->
 // driver module (entry points via cudaGetDriverEntryPoint, so the library
@@ -92,29 +94,25 @@ const Driver& driver() {
 int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 // ---------------------------------------------------------------- geometry
-void plan_geometry(JitPlan& p, int n_hint) {
-  const int hp = p.H + p.pad, wp = p.W + p.pad;
-  const int nmg = cdiv(p.M, p.Q);
+void plan_geometry(JitPlan& p, int /*n_hint*/) {
+  // Dense pixel mapping: a CTA owns T consecutive output pixels g = (n*E + oh)*F + ow (no
+  // idle lanes); the input is staged in the stacked layout (images one above the other,
+  // separated by `pad` shared zero rows, row stride SWs = W + 2*pad), where pixel g sits at
+  // pos(g) = (n*(H+pad) + oh)*SWs + ow and reads tap (kh, kw) at pos(g) + kh*SWs + kw.
   const int T = p.warps * 32 * p.P;
-  double best = 0;
+  const int EF = p.E * p.F;
   p.mos = 1;
-  for (int mos = 1; mos <= n_hint; ++mos) {
-    const int NR = cdiv(n_hint, mos);
-    const int64_t SWs = int64_t(mos) * wp + p.pad;
-    if (SWs * (p.K - 1) > 4 * T) break;  // halo larger than 4 tiles: wider is only worse
-    const int64_t slots = (int64_t(NR - 1) * hp + p.H) * SWs;
-    const int64_t tiles = (slots + T - 1) / T;
-    const int64_t L = T + int64_t(p.K - 1) * (SWs + 1);
-    const int64_t ctas = tiles * nmg, per_wave = int64_t(148) * p.minb;
-    const double waves = double((ctas + per_wave - 1) / per_wave) / double(ctas) * per_wave;  // quantisation
-    const double cost = double(tiles) * (T + 0.15 * double(L - T)) * waves / double(per_wave);
-    if (mos == 1 || cost < best) { best = cost; p.mos = mos; }
-  }
   p.T = T;
-  p.SWs = p.mos * wp + p.pad;
-  p.L = T + (p.K - 1) * (p.SWs + 1);
+  p.SWs = p.W + 2 * p.pad;
+  auto pos = [&](int64_t g) {
+    const int64_t n = g / EF, r = g % EF;
+    return (n * (p.H + p.pad) + r / p.F) * p.SWs + r % p.F;
+  };
+  int64_t span = 0;  // max pos(g0 + T - 1) - pos(g0); periodic in g0 with period EF
+  for (int64_t g0 = 0; g0 < EF; ++g0) span = std::max(span, pos(g0 + T - 1) - pos(g0));
+  p.L = int(span + int64_t(p.K - 1) * (p.SWs + 1) + 1);
   p.Ls = (p.L + 3) & ~3;
-  p.nmg = nmg;
+  p.nmg = cdiv(p.M, p.Q);
   p.nch = cdiv(p.C, p.CC);
   p.KS = cdiv(p.L, p.warps * 32);
   p.smem_bytes = p.NS * p.CC * p.Ls * 4;
@@ -198,14 +196,39 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("mov.u32 %%r2, %%tid.x;");
   o("mov.u32 %%r3, %%ctaid.x;");
   o("mov.u32 %%r4, %%ctaid.y;");
-  o("mul.lo.u32 %%r5, %%r3, %d;", p.T);  // q0
+  o("mul.lo.u32 %%r28, %%r3, %d;", p.T);  // g0: first output pixel of the tile
+  o("mul.lo.u32 %%r29, %%r1, %d;", EF);
+  o("sub.u32 %%r29, %%r29, 1;");           // last pixel N*E*F - 1
+  // q0 = pos(g0): staged window start
+  o("div.u32 %%r30, %%r28, %d;", EF);
+  o("mul.lo.u32 %%r31, %%r30, %d;", EF);
+  o("sub.u32 %%r31, %%r28, %%r31;");
+  o("div.u32 %%r32, %%r31, %d;", p.F);
+  o("mul.lo.u32 %%r33, %%r32, %d;", p.F);
+  o("sub.u32 %%r33, %%r31, %%r33;");
+  o("mad.lo.u32 %%r34, %%r30, %d, %%r32;", hp);
+  o("mad.lo.u32 %%r5, %%r34, %d, %%r33;", p.SWs);
   o("mov.u32 %%r6, smem;");
   o("and.b32 %%r7, %%r2, 31;");           // lane
   o("shr.u32 %%r8, %%r2, 5;");            // warp
   o("mul.lo.u32 %%r9, %%r8, %d;", 32 * P);
-  o("add.u32 %%r9, %%r9, %%r7;");         // lane slot (j = 0)
-  o("shl.b32 %%r10, %%r9, 2;");
-  o("add.u32 %%r10, %%r10, %%r6;");       // lane smem base
+  o("add.u32 %%r9, %%r9, %%r7;");
+  o("add.u32 %%r9, %%r9, %%r28;");        // pixel g of j = 0 (j adds 32 j)
+  for (int j = 0; j < P; ++j) {          // lane smem base of pixel j: smem + 4 (pos(g) - q0)
+    o("add.u32 %%r35, %%r9, %d;", 32 * j);
+    o("min.u32 %%r35, %%r35, %%r29;");     // tail lanes read in range, never store
+    o("div.u32 %%r30, %%r35, %d;", EF);
+    o("mul.lo.u32 %%r31, %%r30, %d;", EF);
+    o("sub.u32 %%r31, %%r35, %%r31;");
+    o("div.u32 %%r32, %%r31, %d;", p.F);
+    o("mul.lo.u32 %%r33, %%r32, %d;", p.F);
+    o("sub.u32 %%r33, %%r31, %%r33;");
+    o("mad.lo.u32 %%r34, %%r30, %d, %%r32;", hp);
+    o("mad.lo.u32 %%r34, %%r34, %d, %%r33;", p.SWs);
+    o("sub.u32 %%r34, %%r34, %%r5;");
+    o("shl.b32 %%r34, %%r34, 2;");
+    o("add.u32 %%r%d, %%r34, %%r6;", 40 + j);
+  }
   // staging slots: k < KS; regs: rd(32+k) src ptr, r(64+k) dst, r(64+KS+k) size, p(16+k) in range
   for (int k = 0; k < p.KS; ++k) {
     const int rs = 64 + k, rz = 64 + p.KS + k, t0 = 64 + 2 * p.KS;  // t0.. scratch
@@ -322,24 +345,21 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   tg += ";";
   // Instruction prefetch pass (p.pf): the code of one m-group is hundreds of KB and, after
   // an L2 flush, every CTA running that group would stall on the same sequential i-cache
-  // misses (ncu: no_instructions dominates). Before the main loop, warp w of each CTA runs
-  // ONE chunk block of its group (chunk ps + w, slices of `warps` chunks chosen by
-  // blockIdx.x) on whatever the stage buffers hold, then the accumulators are reset: the
-  // group's code streams into L2 from many warps and SMs in parallel, nothing is kept.
-  // (Guard predicates instead would make ptxas if-convert every FFMA into FFMA + FSEL.)
+  // misses (ncu: no_instructions dominates). Before the main loop, warp 0 of each CTA runs
+  // ONE chunk block of its group — chunk k_lo + blockIdx.x mod (active chunks) — on whatever
+  // the stage buffers hold, then the accumulators are reset: the CTAs of a group pull
+  // different parts of its code into L2 in parallel, nothing computed is kept. (Guard
+  // predicates instead would make ptxas if-convert every FFMA into FFMA + FSEL; one chunk
+  // per warp instead of per CTA measured slower when L2 is warm: 16 streams per SM.)
   if (p.pf) {
     std::string tp = tg;
     tp[1] = 'p';  // "tp: .branchtargets ..."
     o("setp.eq.u32 %%p12, %%r1, 0;");              // false at run time (N >= 1), opaque to ptxas
-    o("sub.u32 %%r23, %%r21, %%r20;");             // active chunks
-    o("add.u32 %%r25, %%r23, %d;", p.warps - 1);
-    o("div.u32 %%r25, %%r25, %d;", p.warps);       // slices
-    o("max.u32 %%r25, %%r25, 1;");
-    o("rem.u32 %%r26, %%r3, %%r25;");
-    o("mad.lo.u32 %%r26, %%r26, %d, %%r20;", p.warps);
-    o("add.u32 %%r26, %%r26, %%r8;");              // this warp's chunk
-    o("setp.ge.u32 %%p14, %%r26, %%r21;");
+    o("setp.ne.u32 %%p14, %%r8, 0;");
     o("@%%p14 bra.uni PF_DONE;");
+    o("sub.u32 %%r23, %%r21, %%r20;");             // active chunks (>= 1 here)
+    o("rem.u32 %%r26, %%r3, %%r23;");
+    o("add.u32 %%r26, %%r26, %%r20;");
     o("mad.lo.u32 %%r17, %%r4, %d, %%r26;", p.nch);
     o("%s", tp.c_str());
     o("brx.idx.uni %%r17, tp;");
@@ -382,8 +402,8 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
           if (!used[t]) continue;
           const int kh = t / p.K, kw = t % p.K;
           for (int j = 0; j < P; ++j)
-            o("%sld.shared.f32 %%x%d, [%%r10+%d];", pg, t * P + j,
-              ((buf * p.CC + cc) * p.Ls + j * 32 + kh * p.SWs + kw) * 4);
+            o("%sld.shared.f32 %%x%d, [%%r%d+%d];", pg, t * P + j, 40 + j,
+              ((buf * p.CC + cc) * p.Ls + kh * p.SWs + kw) * 4);
         }
         for (const Nz& z : l)
           for (int j = 0; j < P; ++j)
@@ -407,25 +427,13 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("sub.s32 %%r19, %d, %%r18;", p.M);           // rows left
   for (int j = 0; j < P; ++j) {
     const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j, t0 = 64 + 4 * p.KS + 8 * j;
-    o("add.u32 %%r%d, %%r9, %%r5;", t0);
-    if (j) o("add.u32 %%r%d, %%r%d, %d;", t0, t0, 32 * j);
-    o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, p.SWs);      // R
-    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, p.SWs);
-    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 2, t0, t0 + 2);  // X
-    o("div.u32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 1, hp);     // nr
-    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 4, t0 + 3, hp);
-    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 4, t0 + 1, t0 + 4);  // oh
-    o("div.u32 %%r%d, %%r%d, %d;", t0 + 5, t0 + 2, wp);     // nc
-    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 6, t0 + 5, wp);
-    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 6, t0 + 2, t0 + 6);  // ow
-    o("setp.lt.u32 %%p%d, %%r%d, %d;", pv, t0 + 4, p.E);
-    o("setp.lt.and.u32 %%p%d, %%r%d, %d, %%p%d;", pv, t0 + 6, p.F, pv);
-    o("setp.lt.and.u32 %%p%d, %%r%d, %d, %%p%d;", pv, t0 + 5, p.mos, pv);
-    o("mad.lo.u32 %%r%d, %%r%d, %d, %%r%d;", t0 + 3, t0 + 3, p.mos, t0 + 5);  // n
-    o("setp.lt.and.u32 %%p%d, %%r%d, %%r1, %%p%d;", pv, t0 + 3, pv);
-    o("mul.wide.u32 %%rd%d, %%r%d, %d;", rdo, t0 + 3, p.M * EF);  // n*M*EF (elements)
-    o("mad.lo.u32 %%r%d, %%r%d, %d, %%r%d;", t0 + 4, t0 + 4, p.F, t0 + 6);  // oh*F + ow
-    o("cvt.u64.u32 %%rd7, %%r%d;", t0 + 4);
+    o("add.u32 %%r%d, %%r9, %d;", t0, 32 * j);                // g
+    o("setp.le.u32 %%p%d, %%r%d, %%r29;", pv, t0);
+    o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, EF);           // n
+    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, EF);
+    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 2, t0, t0 + 2);    // oh*F + ow
+    o("mul.wide.u32 %%rd%d, %%r%d, %d;", rdo, t0 + 1, p.M * EF);
+    o("cvt.u64.u32 %%rd7, %%r%d;", t0 + 2);
     o("add.s64 %%rd%d, %%rd%d, %%rd7;", rdo, rdo);
     o("shl.b64 %%rd%d, %%rd%d, 2;", rdo, rdo);
     o("add.s64 %%rd%d, %%rd%d, %%rd1;", rdo, rdo);
@@ -464,10 +472,10 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   p.pf = p.pf < 0 ? 0 : 1;
   n_hint = std::max(1, n_hint);
   if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0) {
-    // Shape choice by a small model: CTAs of 16 warps, one per SM, keep every warp of an SM on
-    // the same code (one instruction stream in the SM's instruction caches: measured +20% over
-    // two 8-warp CTAs on AlexNet conv3); Q trades FFMAs per input load against grid fill.
-    static const int cand[][3] = {{64, 16, 1}, {32, 16, 1}, {64, 8, 2}, {32, 8, 2}, {16, 16, 1}, {16, 8, 2}};
+    // Shape choice by a small model: one CTA per SM with as many warps as the registers allow
+    // (all warps of an SM stream the same code: measured +20% for one 16-warp CTA over two
+    // 8-warp CTAs on AlexNet conv3); Q trades FFMAs per input load against grid fill.
+    static const int cand[][3] = {{32, 32, 1}, {16, 32, 1}, {64, 16, 1}, {32, 16, 1}, {16, 16, 1}, {8, 32, 1}};
     double best = -1;
     JitPlan keep = p;
     for (const auto& c : cand) {
@@ -475,14 +483,17 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
       t.Q = std::min(c[0], M); t.warps = c[1]; t.minb = c[2];
       plan_geometry(t, n_hint);
       if (t.smem_bytes > 227 * 1024 / t.minb) continue;
-      const int NR = cdiv(n_hint, t.mos);
-      const double slots = (double(NR - 1) * (H + pad) + H) * t.SWs;
-      const double ctas = double(cdiv(int(std::min(slots, 2e9)), t.T)) * t.nmg, per_wave = 148.0 * t.minb;
+      const double pixels = double(n_hint) * H * W;
+      const double ctas = std::ceil(pixels / t.T) * t.nmg, per_wave = 148.0 * t.minb;
       const double wave_eff = ctas / (std::ceil(ctas / per_wave) * per_wave);
       const double fma = t.Q * K * K * density;
       const double taps = K * K * (1.0 - std::pow(1.0 - density, t.Q));
       const double instr_eff = fma / (fma + taps + 2.0 * t.L / t.T);
-      const double score = wave_eff * instr_eff * (t.minb == 1 ? 1.0 : 0.85);
+      // instruction fetch beyond the i-caches sustains ~1 instruction per 8 cycles per SM
+      // (measured: 16 warps in lockstep reach ~2 IPC), so throughput scales with the warps
+      // that share each fetched instruction, up to the 4-IPC issue limit at 32 warps
+      const double fetch = std::min(1.0, t.warps * t.minb / 32.0);
+      const double score = wave_eff * instr_eff * fetch;
       if (score > best) { best = score; p = t; }
     }
     if (best < 0) return -1;
@@ -494,7 +505,6 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
     plan_geometry(p, n_hint);
   }
   if (p.smem_bytes > 227 * 1024 / p.minb) return -1;
-  if (int64_t(p.SWs) * (p.H + p.pad) * ((n_hint + p.mos - 1) / p.mos + 1) > (int64_t(1) << 30)) return -1;
   return 0;
 }
 
@@ -553,10 +563,10 @@ void jit_free(JitModule& jm) {
 int jit_launch(const JitModule& jm, const float* in, float* out, const float* bias, int relu, int N,
                cudaStream_t s) {
   const JitPlan& p = jm.plan;
-  const int NR = cdiv(N, p.mos);
-  const int64_t slots = (int64_t(NR - 1) * (p.H + p.pad) + p.H) * p.SWs;
-  const int64_t tiles = (slots + p.T - 1) / p.T;
-  if (tiles > 0x7fffffff || slots + p.L > 0x7fffffff) return -1;
+  const int64_t pixels = int64_t(N) * p.E * p.F;
+  const int64_t tiles = (pixels + p.T - 1) / p.T;
+  const int64_t last_pos = (int64_t(N) * (p.H + p.pad) + p.pad) * p.SWs + p.L;  // staged positions stay int32
+  if (pixels > 0x7fffffff || last_pos > 0x7fffffff) return -1;
   unsigned relu_u = relu ? 1u : 0u, n_u = unsigned(N);
   const void* a_in = in;
   void* a_out = out;

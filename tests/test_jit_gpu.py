@@ -157,6 +157,8 @@ def test_autotune_considers_jit():
     csr = escoin.Csr.stretch(w, L.H, L.W, 1, 1).to_device(0)
     ref = fwd(csr, x, None, True)
     csr.jit(n_hint=4)
+    csr.jit(n_hint=4, Q=8, warps=4)  # a second specialised kernel on the same handle
+    csr.jit(n_hint=4, Q=16, CC=2, prefetch=-1)
     dx = torch.from_numpy(x).cuda()
     out = torch.empty((4, L.M, L.E, L.F), device="cuda")
     kid, ms = csr.autotune(4, dx, out, None, True, 2, torch.cuda.current_stream().cuda_stream)
