@@ -475,7 +475,7 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
     // Shape choice by a small model: one CTA per SM with as many warps as the registers allow
     // (all warps of an SM stream the same code: measured +20% for one 16-warp CTA over two
     // 8-warp CTAs on AlexNet conv3); Q trades FFMAs per input load against grid fill.
-    static const int cand[][3] = {{32, 32, 1}, {16, 32, 1}, {64, 16, 1}, {32, 16, 1}, {16, 16, 1}, {8, 32, 1}};
+    static const int cand[][3] = {{32, 32, 1}, {32, 16, 1}, {64, 16, 1}};
     double best = -1;
     JitPlan keep = p;
     for (const auto& c : cand) {
@@ -512,6 +512,9 @@ int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int3
               std::string* log) {
   const Driver& d = driver();
   if (!d.ok) return -1;
+  // the driver-API module calls below need the device's primary context current in THIS host
+  // thread (callers may compile from worker threads); a runtime call binds it
+  if (cudaFree(nullptr) != cudaSuccess) return -3;
   jm.plan = p;
   const std::string ptx = gen_ptx(p, rowptr, colidx, value);
   jm.ptx_bytes = ptx.size();
