@@ -877,6 +877,17 @@ int build_jit(escoin_csr* h, int n_hint, const int* tun) {
     return ESCOIN_ERR_UNSUPPORTED;
   if (int64_t(p.warps) * 32 * p.minb > 2048) return ESCOIN_ERR_UNSUPPORTED;
   if (h->rowptr.size() != size_t(h->M) + 1) return ESCOIN_ERR_UNSUPPORTED;
+  {
+    std::lock_guard<std::mutex> lk(h->jit_mu);
+    for (JitModule* jm : h->jits) {  // this tuning was compiled before: select it
+      const JitPlan& q = jm->plan;
+      if (q.Q == p.Q && q.P == p.P && q.CC == p.CC && q.NS == p.NS && q.warps == p.warps && q.minb == p.minb &&
+          q.pf == p.pf && q.T == p.T && q.L == p.L) {
+        h->jit = jm;
+        return ESCOIN_OK;
+      }
+    }
+  }
   JitModule* jm = new (std::nothrow) JitModule();
   if (!jm) return ESCOIN_ERR_ALLOC;
   const int rc = jit_build(*jm, p, h->rowptr.data(), h->colidx.data(), h->value.data(), nullptr);

@@ -472,30 +472,31 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   p.pf = p.pf < 0 ? 0 : 1;
   n_hint = std::max(1, n_hint);
   if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0) {
-    // Shape choice by a small model: one CTA per SM with as many warps as the registers allow
-    // (all warps of an SM stream the same code: measured +20% for one 16-warp CTA over two
-    // 8-warp CTAs on AlexNet conv3); Q trades FFMAs per input load against grid fill.
-    static const int cand[][3] = {{32, 32, 1}, {32, 16, 1}, {64, 16, 1}};
+    // Shape choice by a small model: one CTA per SM (all warps of an SM stream the same
+    // code), Q in {32, 64} (registers: Q + K*K + ~24 <= 65536 / threads), warps in 16..32
+    // chosen for wave fill (grids are often only 1-3 waves at batch 128), FFMA share, and
+    // instruction-fetch sharing (more warps per fetched instruction; measured ~0.85x at 16
+    // warps vs 32 on AlexNet conv2-4).
     double best = -1;
     JitPlan keep = p;
-    for (const auto& c : cand) {
-      JitPlan t = keep;
-      t.Q = std::min(c[0], M); t.warps = c[1]; t.minb = c[2];
-      plan_geometry(t, n_hint);
-      if (t.smem_bytes > 227 * 1024 / t.minb) continue;
-      const double pixels = double(n_hint) * H * W;
-      const double ctas = std::ceil(pixels / t.T) * t.nmg, per_wave = 148.0 * t.minb;
-      const double wave_eff = ctas / (std::ceil(ctas / per_wave) * per_wave);
-      const double fma = t.Q * K * K * density;
-      const double taps = K * K * (1.0 - std::pow(1.0 - density, t.Q));
-      const double instr_eff = fma / (fma + taps + 2.0 * t.L / t.T);
-      // instruction fetch beyond the i-caches sustains ~1 instruction per 8 cycles per SM
-      // (measured: 16 warps in lockstep reach ~2 IPC), so throughput scales with the warps
-      // that share each fetched instruction, up to the 4-IPC issue limit at 32 warps
-      const double fetch = std::min(1.0, t.warps * t.minb / 32.0);
-      const double score = wave_eff * instr_eff * fetch;
-      if (score > best) { best = score; p = t; }
-    }
+    for (int Qc : {32, 64})
+      for (int wc : {32, 28, 24, 20, 16}) {
+        const int regs = std::min(255, 65536 / (wc * 32)) & ~7;
+        if (std::min(Qc, M) + K * K + 20 > regs && !(Qc == 32 && wc == 32 && K <= 5)) continue;
+        JitPlan t = keep;
+        t.Q = std::min(Qc, M); t.warps = wc; t.minb = 1;
+        plan_geometry(t, n_hint);
+        if (t.smem_bytes > 227 * 1024) continue;
+        const double pixels = double(n_hint) * H * W;
+        const double ctas = std::ceil(pixels / t.T) * t.nmg, per_wave = 148.0;
+        const double wave_eff = ctas / (std::ceil(ctas / per_wave) * per_wave);
+        const double fma = t.Q * K * K * density;
+        const double taps = K * K * (1.0 - std::pow(1.0 - density, t.Q));
+        const double instr_eff = fma / (fma + taps + 2.0 * t.L / t.T);
+        const double fetch = std::pow(t.warps / 32.0, 0.25);
+        const double score = wave_eff * instr_eff * fetch;
+        if (score > best) { best = score; p = t; }
+      }
     if (best < 0) return -1;
   } else {
     if (p.Q <= 0) p.Q = 64;
