@@ -182,10 +182,12 @@ int escoin_csr_autotune(escoin_csr* csr, int N, const float* in, float* out, con
  * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
  *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
  *              forwards accept any N.
- *   tunables   NULL or ntunables (<= 7) ints {Q output channels per CTA,
+ *   tunables   NULL or ntunables (<= 8) ints {Q output channels per CTA,
  *              P pixels per lane, CC channels per stage, NS stages, warps per
- *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off)};
- *              <= 0 entries take the defaults.
+ *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off),
+ *              mbarrier pipeline (> 0 = on: warps drift up to NS-2 chunks
+ *              instead of one CTA barrier per chunk)}; <= 0 entries take the
+ *              defaults.
  * On success the new kernel is added to the handle's specialised kernels
  * and selected (the handle's kernel becomes ESCOIN_KERNEL_JIT); earlier ones
  * stay compiled until escoin_csr_free, and escoin_csr_autotune times all of

@@ -865,11 +865,11 @@ int auto_kernel(const escoin_csr* h) {
 }
 
 // Pattern-specialised kernel (jit_sconv.cpp): plan, generate, compile, load.
-// tun = {Q, P, CC, NS, warps, minb, prefetch} (<= 0: default; prefetch < 0 = off) or NULL.
+// tun = {Q, P, CC, NS, warps, minb, prefetch, mbarrier} (<= 0: default; prefetch < 0 = off) or NULL.
 int build_jit(escoin_csr* h, int n_hint, const int* tun) {
   JitPlan p;
   if (tun) {
-    p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6];
+    p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6]; p.mb = tun[7];
   }
   if (p.P > 8 || p.Q > 256 || p.CC > 64 || p.NS > 6 || p.warps > 32 || p.minb > 8) return ESCOIN_ERR_UNSUPPORTED;
   const double density = double(h->nnz) / (double(h->M) * h->C * h->K * h->K);
@@ -882,7 +882,7 @@ int build_jit(escoin_csr* h, int n_hint, const int* tun) {
     for (JitModule* jm : h->jits) {  // this tuning was compiled before: select it
       const JitPlan& q = jm->plan;
       if (q.Q == p.Q && q.P == p.P && q.CC == p.CC && q.NS == p.NS && q.warps == p.warps && q.minb == p.minb &&
-          q.pf == p.pf && q.T == p.T && q.L == p.L) {
+          q.pf == p.pf && q.mb == p.mb && q.T == p.T && q.L == p.L) {
         h->jit = jm;
         return ESCOIN_OK;
       }
@@ -1316,8 +1316,8 @@ int escoin_csr_autotune(escoin_csr* h, int N, const float* in, float* out, const
 int escoin_csr_jit(escoin_csr* h, int n_hint, const int* tunables, int ntunables) {
   if (!h) return ESCOIN_ERR_NULL;
   if (!h->on_device) return ESCOIN_ERR_NOT_ON_DEVICE;
-  if (ntunables < 0 || ntunables > 7 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
-  int tun[7] = {0, 0, 0, 0, 0, 0, 0};
+  if (ntunables < 0 || ntunables > 8 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
+  int tun[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
   DeviceGuard g(h->device);
   if (!g.ok) return ESCOIN_ERR_CUDA;

@@ -115,7 +115,7 @@ void plan_geometry(JitPlan& p, int /*n_hint*/) {
   p.nmg = cdiv(p.M, p.Q);
   p.nch = cdiv(p.C, p.CC);
   p.KS = cdiv(p.L, p.warps * 32);
-  p.smem_bytes = p.NS * p.CC * p.Ls * 4;
+  p.smem_bytes = p.NS * p.CC * p.Ls * 4 + (p.mb ? 128 : 0);
 }
 
 // ---------------------------------------------------------------- PTX text
@@ -209,6 +209,10 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("mad.lo.u32 %%r34, %%r30, %d, %%r32;", hp);
   o("mad.lo.u32 %%r5, %%r34, %d, %%r33;", p.SWs);
   o("mov.u32 %%r6, smem;");
+  if (p.mb) {  // mbarriers full[NS], empty[NS] in the first 128 bytes, stage buffers after
+    o("mov.u32 %%r36, %%r6;");
+    o("add.u32 %%r6, %%r6, 128;");
+  }
   o("and.b32 %%r7, %%r2, 31;");           // lane
   o("shr.u32 %%r8, %%r2, 5;");            // warp
   o("mul.lo.u32 %%r9, %%r8, %d;", 32 * P);
@@ -321,19 +325,33 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("add.s64 %%rd8, %%rd8, %%rd9;");
   o("ld.global.nc.u32 %%r20, [%%rd8];");    // k_lo
   o("ld.global.nc.u32 %%r21, [%%rd8+4];");  // k_hi
-  for (int s = 0; s < p.NS - 1; ++s) {
+  // Copy-ahead distance D: chunks staged before the one being computed. Bar mode: NS - 1
+  // (one cp.async group per chunk, wait_group + CTA barrier per chunk). mbarrier mode: NS - 2,
+  // so a warp may run one chunk ahead of the slowest (a buffer is refilled only after every
+  // warp arrived on its `empty` barrier; data readiness is the `full` barrier's phase).
+  const int D = p.mb ? std::max(1, p.NS - 2) : p.NS - 1;
+  if (p.mb) {
+    o("setp.eq.u32 %%p15, %%r2, 0;");
+    for (int b = 0; b < p.NS; ++b) {
+      o("@%%p15 mbarrier.init.shared::cta.b64 [%%r36+%d], %d;", 8 * b, NT);
+      o("@%%p15 mbarrier.init.shared::cta.b64 [%%r36+%d], %d;", 8 * (p.NS + b), p.warps);
+    }
+    o("bar.sync 0;");
+  }
+  for (int s = 0; s < D; ++s) {
     o("add.u32 %%r11, %%r20, %d;", s);
     o("setp.ge.u32 %%p3, %%r11, %%r21;");
     o("@%%p3 bra.uni PRO%d;", s);
     o("mov.u32 %%r12, %d;", s * p.CC * p.Ls * 4);
     stage("%r11", "%r12");
+    if (p.mb) o("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%%r36+%d];", 8 * s);
     o("PRO%d:", s);
-    o("cp.async.commit_group;");
+    if (!p.mb) o("cp.async.commit_group;");
   }
   o("mov.u32 %%r15, %%r20;");  // k
   o("setp.ge.u32 %%p3, %%r15, %%r21;");
   o("@%%p3 bra.uni EPI;");
-  o("mov.u32 %%r16, %d;", (p.NS - 1) * p.CC * p.Ls * 4);  // buffer offset of chunk k + NS - 1
+  o("mov.u32 %%r16, %d;", D * p.CC * p.Ls * 4);  // buffer offset of chunk k + D
   // branch targets
   std::string tg = "ts: .branchtargets ";
   for (int g = 0; g < p.nmg; ++g)
@@ -368,14 +386,51 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     for (int q = 0; q < Q * P; ++q) o("mov.f32 %%a%d, 0f00000000;", q);
   }
   o("LOOP:");
-  o("cp.async.wait_group %d;", p.NS - 2);
-  o("bar.sync 0;");
-  o("add.u32 %%r11, %%r15, %d;", p.NS - 1);
+  if (!p.mb) {
+    o("cp.async.wait_group %d;", p.NS - 2);
+    o("bar.sync 0;");
+  }
+  o("add.u32 %%r11, %%r15, %d;", D);
   o("setp.ge.u32 %%p3, %%r11, %%r21;");
   o("@%%p3 bra.uni NOSTAGE;");
+  if (p.mb) {
+    // buffer b = (j + D) % NS (byte offset r16); before refilling it, every warp must have
+    // finished chunk j + D - NS: wait empty[b] with parity ((j + D) / NS + 1) & 1
+    o("sub.u32 %%r48, %%r11, %%r20;");             // jj = j + D
+    o("setp.lt.u32 %%p3, %%r48, %d;", p.NS);       // first use of the buffer: nothing to wait for
+    o("@%%p3 bra.uni EMPTY_OK;");
+    o("rem.u32 %%r49, %%r48, %d;", p.NS);
+    o("div.u32 %%r50, %%r48, %d;", p.NS);
+    o("add.u32 %%r50, %%r50, 1;");
+    o("and.b32 %%r50, %%r50, 1;");
+    o("mad.lo.u32 %%r51, %%r49, 8, %%r36;");
+    o("add.u32 %%r51, %%r51, %d;", 8 * p.NS);
+    o("WAIT_EMPTY:");
+    o("mbarrier.try_wait.parity.shared::cta.b64 %%p15, [%%r51], %%r50;");
+    o("@!%%p15 bra WAIT_EMPTY;");
+    o("EMPTY_OK:");
+  }
   stage("%r11", "%r16");
+  if (p.mb) {
+    o("sub.u32 %%r48, %%r11, %%r20;");
+    o("rem.u32 %%r49, %%r48, %d;", p.NS);
+    o("mad.lo.u32 %%r51, %%r49, 8, %%r36;");
+    o("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%%r51];");
+  }
   o("NOSTAGE:");
-  o("cp.async.commit_group;");
+  if (!p.mb) o("cp.async.commit_group;");
+  if (p.mb) {  // data of chunk j: full[j % NS], parity (j / NS) & 1
+    o("sub.u32 %%r48, %%r15, %%r20;");
+    o("rem.u32 %%r52, %%r48, %d;", p.NS);
+    o("div.u32 %%r50, %%r48, %d;", p.NS);
+    o("and.b32 %%r50, %%r50, 1;");
+    o("mad.lo.u32 %%r51, %%r52, 8, %%r36;");
+    o("WAIT_FULL:");
+    o("mbarrier.try_wait.parity.shared::cta.b64 %%p15, [%%r51], %%r50;");
+    o("@!%%p15 bra WAIT_FULL;");
+    o("mad.lo.u32 %%r53, %%r52, 8, %%r36;");
+    o("add.u32 %%r53, %%r53, %d;", 8 * p.NS);     // empty[j % NS], arrived on after the block
+  }
   o("add.u32 %%r16, %%r16, %d;", p.CC * p.Ls * 4);
   o("setp.ge.u32 %%p4, %%r16, %d;", p.NS * p.CC * p.Ls * 4);
   o("@%%p4 mov.u32 %%r16, 0;");
@@ -413,6 +468,10 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     }
   o("NEXT:");
   if (p.pf) o("@!%%p12 bra.uni PF_DONE;");
+  if (p.mb) {
+    o("setp.eq.u32 %%p15, %%r7, 0;");
+    o("@%%p15 mbarrier.arrive.shared::cta.b64 %%rd10, [%%r53];");
+  }
   o("add.u32 %%r15, %%r15, 1;");
   o("setp.lt.u32 %%p5, %%r15, %%r21;");
   o("@%%p5 bra.uni LOOP;");
@@ -470,6 +529,7 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   if (p.CC <= 0) p.CC = 8;
   if (p.NS <= 1) p.NS = 3;
   p.pf = p.pf < 0 ? 0 : 1;
+  p.mb = p.mb > 0 ? 1 : 0;
   n_hint = std::max(1, n_hint);
   if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0) {
     // Shape choice by a small model: one CTA per SM (all warps of an SM stream the same

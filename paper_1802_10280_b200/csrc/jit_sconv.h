@@ -16,6 +16,7 @@ struct JitPlan {
   int warps = 0;  // warps per CTA
   int minb = 0;   // CTAs per SM the register budget is compiled for
   int pf = 0;     // instruction prefetch pass: 0 = default (on), < 0 = off
+  int mb = 0;     // > 0: mbarrier pipeline (warps drift up to NS-2 chunks) instead of a CTA barrier per chunk
   // layer
   int C = 0, H = 0, W = 0, M = 0, K = 0, pad = 0, E = 0, F = 0;
   // derived

@@ -194,10 +194,10 @@ class Csr:
                                                                 ctypes.byref(bms)))
         return bid.value, bms.value
 
-    def jit(self, n_hint=128, Q=0, P=0, CC=0, NS=0, warps=0, minb=0, prefetch=0) -> "Csr":
+    def jit(self, n_hint=128, Q=0, P=0, CC=0, NS=0, warps=0, minb=0, prefetch=0, mbarrier=0) -> "Csr":
         """escoin_csr_jit: compile this layer's pattern-specialised kernel and select it."""
-        tun = (ctypes.c_int * 7)(Q, P, CC, NS, warps, minb, prefetch)
-        _check("escoin_csr_jit", lib().escoin_csr_jit(self._h, n_hint, tun, 7))
+        tun = (ctypes.c_int * 8)(Q, P, CC, NS, warps, minb, prefetch, mbarrier)
+        _check("escoin_csr_jit", lib().escoin_csr_jit(self._h, n_hint, tun, 8))
         return self
 
     def jit_info(self):

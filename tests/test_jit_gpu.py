@@ -70,7 +70,8 @@ GRID = [  # N, C, H, W, M, K, pad, density — stride 1, "same" padding
     (3, 37, 7, 7, 26, 1, 0, 0.2), (9, 13, 13, 13, 65, 3, 1, 0.2),
 ]
 TUNINGS = [dict(), dict(Q=16, P=2, CC=3, NS=2), dict(Q=32, P=3, CC=5, NS=4, warps=4, minb=3),
-           dict(Q=8, P=1, CC=1, NS=2, warps=2, minb=1)]
+           dict(Q=8, P=1, CC=1, NS=2, warps=2, minb=1), dict(NS=4, mbarrier=1),
+           dict(Q=16, CC=3, NS=3, warps=4, mbarrier=1, prefetch=-1), dict(Q=8, CC=1, NS=5, warps=2, mbarrier=1)]
 
 
 @pytest.mark.parametrize("tun", range(len(TUNINGS)))
@@ -168,7 +169,8 @@ def test_autotune_considers_jit():
     assert info["regs"] > 0 and info["code_bytes"] > 0 and info["Q"] > 0
 
 
-@pytest.mark.parametrize("tun", [dict(), dict(Q=8, CC=3, NS=2, warps=4, minb=2), dict(Q=16, CC=5, NS=4)])
+@pytest.mark.parametrize("tun", [dict(), dict(Q=8, CC=3, NS=2, warps=4, minb=2), dict(Q=16, CC=5, NS=4),
+                                 dict(Q=16, CC=2, NS=4, mbarrier=1)])
 def test_grouped_block_diagonal_and_empty_groups(tun):
     # block-diagonal expansion of a g=3 grouped layer (R#18): every m-group touches a channel
     # sub-range only (the kernel skips the other chunks); one whole group of rows is empty
