@@ -363,20 +363,26 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   tg += ";";
   // Instruction prefetch pass (p.pf): the code of one m-group is hundreds of KB and, after
   // an L2 flush, every CTA running that group would stall on the same sequential i-cache
-  // misses (ncu: no_instructions dominates). Before the main loop, warp 0 of each CTA runs
-  // ONE chunk block of its group — chunk k_lo + blockIdx.x mod (active chunks) — on whatever
-  // the stage buffers hold, then the accumulators are reset: the CTAs of a group pull
-  // different parts of its code into L2 in parallel, nothing computed is kept. (Guard
-  // predicates instead would make ptxas if-convert every FFMA into FFMA + FSEL; one chunk
-  // per warp instead of per CTA measured slower when L2 is warm: 16 streams per SM.)
+  // misses (ncu: no_instructions dominates). Before the main loop, warp w < ceil(chunks /
+  // gridDim.x) of each CTA runs ONE chunk block of its group — chunk k_lo + (blockIdx.x +
+  // w * gridDim.x) mod (active chunks) — on whatever the stage buffers hold, then the
+  // accumulators are reset: the CTAs of a group pull all parts of its code into L2 in
+  // parallel, nothing computed is kept. (Guard predicates instead would make ptxas
+  // if-convert every FFMA into FFMA + FSEL; one chunk per warp in EVERY warp measured slower
+  // when L2 is warm: 16 streams per SM.)
   if (p.pf) {
     std::string tp = tg;
     tp[1] = 'p';  // "tp: .branchtargets ..."
     o("setp.eq.u32 %%p12, %%r1, 0;");              // false at run time (N >= 1), opaque to ptxas
-    o("setp.ne.u32 %%p14, %%r8, 0;");
-    o("@%%p14 bra.uni PF_DONE;");
     o("sub.u32 %%r23, %%r21, %%r20;");             // active chunks (>= 1 here)
-    o("rem.u32 %%r26, %%r3, %%r23;");
+    o("mov.u32 %%r22, %%nctaid.x;");
+    o("add.u32 %%r24, %%r23, %%r22;");
+    o("sub.u32 %%r24, %%r24, 1;");
+    o("div.u32 %%r24, %%r24, %%r22;");             // warps needed so the group's CTAs cover every chunk
+    o("setp.ge.u32 %%p14, %%r8, %%r24;");
+    o("@%%p14 bra.uni PF_DONE;");
+    o("mad.lo.u32 %%r26, %%r8, %%r22, %%r3;");     // blockIdx.x + warp * gridDim.x
+    o("rem.u32 %%r26, %%r26, %%r23;");
     o("add.u32 %%r26, %%r26, %%r20;");
     o("mad.lo.u32 %%r17, %%r4, %d, %%r26;", p.nch);
     o("%s", tp.c_str());
