@@ -188,7 +188,8 @@ def setup(args, wl, device, rank, world, torch, escoin):
             return round(time.time() - t0, 2)
         tasks = [(r, t) for r in runs for t in tunings]
         tasks.sort(key=lambda rt: -rt[0].nnz)  # largest compiles first
-        with ThreadPoolExecutor(max(1, min(len(tasks), os.cpu_count() or 1))) as ex:
+        # host cores are shared by the ranks of this node (compile memory and time)
+        with ThreadPoolExecutor(max(1, min(len(tasks), (os.cpu_count() or 1) // max(1, world)))) as ex:
             for (r, _), t in zip(tasks, ex.map(jit, tasks)):
                 if t is not None:
                     r.jit_s = round(getattr(r, "jit_s", 0.0) + t, 2)
