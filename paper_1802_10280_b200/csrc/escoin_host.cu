@@ -1396,4 +1396,32 @@ int escoin_internal_plan(const escoin_csr* h, int id, int64_t* out) {
   return ESCOIN_OK;
 }
 
+/* Internal (not in escoin.h): the PTX escoin_csr_jit would generate for this handle with these
+ * tunables (host only, no device needed), and an in-process compile of PTX text for sm_100a.
+ * Two-call pattern: *len receives the size; the text is copied when cap >= size + 1. */
+int escoin_internal_jit_ptx(const escoin_csr* h, int n_hint, const int* tunables, int ntunables, char* buf,
+                            int64_t cap, int64_t* len) {
+  if (!h || !len || ntunables < 0 || ntunables > 8 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
+  JitPlan p;
+  int tun[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
+  p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6];
+  p.mb = tun[7];
+  const double density = double(h->nnz) / (double(h->M) * h->C * h->K * h->K);
+  if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint > 0 ? n_hint : 128, density) != 0)
+    return ESCOIN_ERR_UNSUPPORTED;
+  const std::string ptx = jit_ptx_text(p, h->rowptr.data(), h->colidx.data(), h->value.data());
+  *len = int64_t(ptx.size());
+  if (buf && cap >= int64_t(ptx.size()) + 1) std::memcpy(buf, ptx.c_str(), ptx.size() + 1);
+  return ESCOIN_OK;
+}
+
+int escoin_internal_ptx_compile(const char* ptx, int64_t* cubin_bytes) {
+  if (!ptx || !cubin_bytes) return ESCOIN_ERR_NULL;
+  size_t n = 0;
+  if (jit_compile_only(ptx, &n) != 0) return ESCOIN_ERR_UNSUPPORTED;
+  *cubin_bytes = int64_t(n);
+  return ESCOIN_OK;
+}
+
 }  // extern "C"

@@ -620,6 +620,16 @@ int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int3
   return 0;
 }
 
+int jit_compile_only(const char* ptx, size_t* cubin_bytes) {
+  nvPTXCompilerHandle c = nullptr;
+  if (nvPTXCompilerCreate(&c, std::strlen(ptx), ptx) != NVPTXCOMPILE_SUCCESS) return -1;
+  const char* opts[] = {"--gpu-name=sm_100a", "-O3"};
+  const bool ok = nvPTXCompilerCompile(c, 2, opts) == NVPTXCOMPILE_SUCCESS &&
+                  nvPTXCompilerGetCompiledProgramSize(c, cubin_bytes) == NVPTXCOMPILE_SUCCESS;
+  nvPTXCompilerDestroy(&c);
+  return ok ? 0 : -2;
+}
+
 std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value) {
   return gen_ptx(p, rowptr, colidx, value);
 }

@@ -44,6 +44,8 @@ int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int3
               std::string* log);
 std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value);
 void jit_free(JitModule& jm);
+// Compile PTX for sm_100a in-process without loading it (host only); 0 = OK.
+int jit_compile_only(const char* ptx, size_t* cubin_bytes);
 int jit_launch(const JitModule& jm, const float* in, float* out, const float* bias, int relu, int N,
                cudaStream_t s);
 

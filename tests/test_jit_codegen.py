@@ -1,0 +1,128 @@
+"""Host-side checks of the pattern-specialised kernel's code generator (no GPU needed).
+
+escoin_csr_jit compiles one `fma.rn.f32 acc, x, <weight immediate>, acc` per nonzero and
+pixel.  These tests read the generated PTX (internal export escoin_internal_jit_ptx) and
+check, independently of any device, that every accumulator receives exactly its CSR row —
+the stretched CSR values bit for bit, at the taps its colidx encodes, in ascending
+(c, kh, kw) order (reading R#10) — and that the text compiles for sm_100a in-process.
+"""
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+from paper_1802_10280_b200 import escoin, inputs, workloads
+
+
+def _lib():
+    L = escoin.lib()
+    L.escoin_internal_jit_ptx.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                          ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+    L.escoin_internal_ptx_compile.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]
+    return L
+
+
+def gen_ptx(csr, n_hint=16, **tun):
+    keys = ["Q", "P", "CC", "NS", "warps", "minb", "prefetch", "mbarrier"]
+    arr = (ctypes.c_int * 8)(*[tun.get(k, 0) for k in keys])
+    L, n = _lib(), ctypes.c_int64()
+    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 8, None, 0, ctypes.byref(n)) == 0
+    buf = ctypes.create_string_buffer(n.value + 1)
+    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 8, buf, n.value + 1, ctypes.byref(n)) == 0
+    return buf.value.decode()
+
+
+FMA = re.compile(r"fma\.rn\.f32 %a(\d+), %x(\d+), 0f([0-9A-F]{8}), %a(\d+);")
+BLOCK = re.compile(r"^B(\d+)_(\d+):")
+
+
+def fma_stream(ptx):
+    """[(group, acc, xreg, bits)] in program order of the chunk blocks."""
+    g, out = None, []
+    for line in ptx.splitlines():
+        m = BLOCK.match(line)
+        if m:
+            g = int(m.group(1))
+            continue
+        m = FMA.search(line)
+        if m:
+            assert m.group(1) == m.group(4), line  # accumulates in place
+            out.append((g, int(m.group(1)), int(m.group(2)), int(m.group(3), 16)))
+    return out
+
+
+def check_rows(csr, ptx, Q, P):
+    info = csr.info()
+    M, K, H, W, pad = info["M"], info["K"], info["H"], info["W"], info["pad"]
+    Hp, Wp = H + 2 * pad, W + 2 * pad
+    rowptr, colidx, value = csr.host_arrays()
+    stream = fma_stream(ptx)
+    assert len(stream) == info["nnz"] * P  # one FFMA per nonzero and pixel, nothing else
+    per_acc = {}
+    for g, a, x, bits in stream:
+        per_acc.setdefault((g, a), []).append((x, bits))
+    for m in range(M):
+        g, q = divmod(m, Q)
+        r0, r1 = rowptr[m], rowptr[m + 1]
+        bits = value[r0:r1].view(np.uint32).tolist()
+        rem = colidx[r0:r1] % (Hp * Wp)
+        taps = ((rem // Wp) * K + rem % Wp).tolist()
+        for j in range(P):
+            got = per_acc.get((g, q * P + j), [])
+            assert [b for _, b in got] == bits, "row %d pixel %d: weights or order differ" % (m, j)
+            assert [x for x, _ in got] == [t * P + j for t in taps], "row %d pixel %d: taps differ" % (m, j)
+
+
+def resolved_q(ptx):
+    return int(re.search(r"\.reg \.f32 %a<(\d+)>;", ptx).group(1))
+
+
+CASES = [  # C, H, W, M, K, pad, density, tunables
+    (16, 14, 14, 32, 3, 1, 0.2, dict()),
+    (7, 9, 11, 33, 3, 1, 0.3, dict(Q=8, P=2, CC=3)),
+    (6, 8, 8, 20, 5, 2, 0.25, dict(Q=16, CC=4, NS=4, mbarrier=1)),
+    (12, 6, 7, 19, 1, 0, 0.4, dict(Q=4, P=3, warps=4, prefetch=-1)),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_generated_fma_stream_is_the_csr(case):
+    C, H, W, M, K, pad, d, tun = case
+    rng = np.random.default_rng(C * 1000 + M)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= d] = 0.0
+    w[min(3, M - 1)] = 0.0  # an empty row
+    csr = escoin.Csr.stretch(w, H, W, 1, pad)
+    ptx = gen_ptx(csr, **tun)
+    P = tun.get("P", 1) or 1
+    Q = resolved_q(ptx) // P
+    check_rows(csr, ptx, Q, P)
+
+
+def test_config_layer_and_grouped_blocks():
+    # AlexNet conv4 (g = 2, block-diagonal expansion): every group only runs its channel half
+    L = [l for l in workloads.workload("alexnet").layers if l.name == "conv4"][0]
+    w = inputs.layer_weights("alexnet", L, 800)
+    csr = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad)
+    ptx = gen_ptx(csr, n_hint=128, Q=32, warps=32, minb=1)
+    check_rows(csr, ptx, 32, 1)
+
+
+def test_generated_ptx_compiles_for_sm100a():
+    L = workloads.TINY
+    w = inputs.layer_weights("tiny", L, 800)
+    csr = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad)
+    for tun in [dict(), dict(mbarrier=1, NS=4), dict(Q=8, P=2, prefetch=-1)]:
+        n = ctypes.c_int64()
+        assert _lib().escoin_internal_ptx_compile(gen_ptx(csr, n_hint=1, **tun).encode(), ctypes.byref(n)) == 0
+        assert n.value > 0
+
+
+def test_unsupported_shapes_have_no_specialised_form():
+    w = np.ones((4, 3, 3, 3), np.float32)
+    for stride, pad in [(2, 1), (1, 0), (1, 2)]:
+        csr = escoin.Csr.stretch(w, 9, 9, stride, pad)
+        n = ctypes.c_int64()
+        arr = (ctypes.c_int * 8)()
+        assert _lib().escoin_internal_jit_ptx(csr.handle, 4, arr, 8, None, 0, ctypes.byref(n)) == escoin.ERR_UNSUPPORTED
