@@ -106,7 +106,7 @@ void plan_geometry(JitPlan& p, int /*n_hint*/) {
   p.SWs = p.W + 2 * p.pad;
   auto pos = [&](int64_t g) {
     const int64_t n = g / EF, r = g % EF;
-    return (n * (p.H + p.pad) + r / p.F) * p.SWs + r % p.F;
+    return (n * (p.H + p.pad) + (r / p.F) * p.S) * p.SWs + (r % p.F) * p.S;
   };
   int64_t span = 0;  // max pos(g0 + T - 1) - pos(g0); periodic in g0 with period EF
   for (int64_t g0 = 0; g0 < EF; ++g0) span = std::max(span, pos(g0 + T - 1) - pos(g0));
@@ -116,6 +116,17 @@ void plan_geometry(JitPlan& p, int /*n_hint*/) {
   p.nch = cdiv(p.C, p.CC);
   p.KS = cdiv(p.L, p.warps * 32);
   p.smem_bytes = p.NS * p.CC * p.Ls * 4 + (p.mb ? 128 : 0);
+}
+
+// Geometry with the channel chunk halved until the stage ring fits shared memory (strided
+// layers stage S*S times more input per output pixel).
+bool plan_fit(JitPlan& p, int n_hint) {
+  for (;;) {
+    plan_geometry(p, n_hint);
+    if (p.smem_bytes <= 227 * 1024 / p.minb) return true;
+    if (p.CC == 1) return false;
+    p.CC = (p.CC + 1) / 2;
+  }
 }
 
 // ---------------------------------------------------------------- PTX text
@@ -206,6 +217,10 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("div.u32 %%r32, %%r31, %d;", p.F);
   o("mul.lo.u32 %%r33, %%r32, %d;", p.F);
   o("sub.u32 %%r33, %%r31, %%r33;");
+  if (p.S > 1) {  // window origin of output (oh, ow): stacked row oh*S, column ow*S (R#1)
+    o("mul.lo.u32 %%r32, %%r32, %d;", p.S);
+    o("mul.lo.u32 %%r33, %%r33, %d;", p.S);
+  }
   o("mad.lo.u32 %%r34, %%r30, %d, %%r32;", hp);
   o("mad.lo.u32 %%r5, %%r34, %d, %%r33;", p.SWs);
   o("mov.u32 %%r6, smem;");
@@ -227,6 +242,10 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("div.u32 %%r32, %%r31, %d;", p.F);
     o("mul.lo.u32 %%r33, %%r32, %d;", p.F);
     o("sub.u32 %%r33, %%r31, %%r33;");
+    if (p.S > 1) {
+      o("mul.lo.u32 %%r32, %%r32, %d;", p.S);
+      o("mul.lo.u32 %%r33, %%r33, %d;", p.S);
+    }
     o("mad.lo.u32 %%r34, %%r30, %d, %%r32;", hp);
     o("mad.lo.u32 %%r34, %%r34, %d, %%r33;", p.SWs);
     o("sub.u32 %%r34, %%r34, %%r5;");
@@ -528,9 +547,14 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
 }  // namespace
 
 int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad, int n_hint, double density) {
-  if (stride != 1 || 2 * pad != K - 1 || K > 7) return -1;
+  // Any stride and padding: the stacked layout shares `pad` zero rows between neighbouring
+  // images (image n's bottom padding is image n+1's top padding) and every window an output
+  // reads lies inside its own image's padded extent, rows [oh*S, oh*S + K) of H + 2*pad.
+  if (stride < 1 || pad < 0 || K > 7) return -1;
+  const int E = (H + 2 * pad - K) / stride + 1, F = (W + 2 * pad - K) / stride + 1;
+  if (H + 2 * pad < K || W + 2 * pad < K || E < 1 || F < 1) return -1;
   p.C = C; p.H = H; p.W = W; p.M = M; p.K = K; p.pad = pad;
-  p.E = H; p.F = W;
+  p.E = E; p.F = F; p.S = stride;
   if (p.P <= 0) p.P = 1;
   if (p.CC <= 0) p.CC = 8;
   if (p.NS <= 1) p.NS = 3;
@@ -551,9 +575,8 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
         if (std::min(Qc, M) + K * K + 20 > regs && !(Qc == 32 && wc == 32 && K <= 5)) continue;
         JitPlan t = keep;
         t.Q = std::min(Qc, M); t.warps = wc; t.minb = 1;
-        plan_geometry(t, n_hint);
-        if (t.smem_bytes > 227 * 1024) continue;
-        const double pixels = double(n_hint) * H * W;
+        if (!plan_fit(t, n_hint)) continue;
+        const double pixels = double(n_hint) * E * F;
         const double ctas = std::ceil(pixels / t.T) * t.nmg, per_wave = 148.0;
         const double wave_eff = ctas / (std::ceil(ctas / per_wave) * per_wave);
         const double fma = t.Q * K * K * density;
@@ -569,7 +592,7 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
     if (p.warps <= 0) p.warps = 16;
     if (p.minb <= 0) p.minb = 1;
     p.Q = std::min(p.Q, M);
-    plan_geometry(p, n_hint);
+    if (!plan_fit(p, n_hint)) return -1;
   }
   if (p.smem_bytes > 227 * 1024 / p.minb) return -1;
   return 0;

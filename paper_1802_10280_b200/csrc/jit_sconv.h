@@ -18,7 +18,7 @@ struct JitPlan {
   int pf = 0;     // instruction prefetch pass: 0 = default (on), < 0 = off
   int mb = 0;     // > 0: mbarrier pipeline (warps drift up to NS-2 chunks) instead of a CTA barrier per chunk
   // layer
-  int C = 0, H = 0, W = 0, M = 0, K = 0, pad = 0, E = 0, F = 0;
+  int C = 0, H = 0, W = 0, M = 0, K = 0, pad = 0, E = 0, F = 0, S = 1;
   // derived
   int mos = 1;    // images per mosaic super-row
   int SWs = 0;    // super-image row stride (words)

@@ -84,6 +84,20 @@ CASES = [  # C, H, W, M, K, pad, density, tunables
     (6, 8, 8, 20, 5, 2, 0.25, dict(Q=16, CC=4, NS=4, mbarrier=1)),
     (12, 6, 7, 19, 1, 0, 0.4, dict(Q=4, P=3, warps=4, prefetch=-1)),
 ]
+STRIDED = [  # C, H, W, M, K, stride, pad
+    (6, 15, 11, 13, 3, 2, 1), (5, 9, 9, 7, 3, 1, 0), (3, 11, 11, 5, 5, 2, 2), (7, 13, 12, 6, 3, 3, 1),
+]
+
+
+@pytest.mark.parametrize("case", STRIDED)
+def test_strided_and_padded_fma_stream(case):
+    C, H, W, M, K, st, pad = case
+    rng = np.random.default_rng(C * 100 + H)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.3] = 0.0
+    csr = escoin.Csr.stretch(w, H, W, st, pad)
+    ptx = gen_ptx(csr, Q=8)
+    check_rows(csr, ptx, 8, 1)
 
 
 @pytest.mark.parametrize("case", CASES)
@@ -120,9 +134,8 @@ def test_generated_ptx_compiles_for_sm100a():
 
 
 def test_unsupported_shapes_have_no_specialised_form():
-    w = np.ones((4, 3, 3, 3), np.float32)
-    for stride, pad in [(2, 1), (1, 0), (1, 2)]:
-        csr = escoin.Csr.stretch(w, 9, 9, stride, pad)
-        n = ctypes.c_int64()
-        arr = (ctypes.c_int * 8)()
-        assert _lib().escoin_internal_jit_ptx(csr.handle, 4, arr, 8, None, 0, ctypes.byref(n)) == escoin.ERR_UNSUPPORTED
+    w = np.ones((4, 3, 9, 9), np.float32)  # K > 7
+    csr = escoin.Csr.stretch(w, 19, 19, 2, 1)
+    n = ctypes.c_int64()
+    arr = (ctypes.c_int * 8)()
+    assert _lib().escoin_internal_jit_ptx(csr.handle, 4, arr, 8, None, 0, ctypes.byref(n)) == escoin.ERR_UNSUPPORTED

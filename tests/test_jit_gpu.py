@@ -116,14 +116,38 @@ def test_exact_integer_regime():
     assert np.array_equal(out.astype(np.float64), ref)
 
 
+STRIDE_PAD = [  # N, C, H, W, M, K, stride, pad — window origins oh*S, ow*S in the stacked layout
+    (3, 6, 15, 11, 13, 3, 2, 1), (2, 5, 9, 9, 7, 3, 1, 0), (2, 4, 8, 10, 9, 3, 1, 2), (4, 8, 16, 16, 12, 1, 2, 0),
+    (2, 3, 11, 11, 5, 5, 2, 2), (3, 7, 13, 12, 6, 3, 3, 1), (5, 6, 14, 14, 40, 3, 2, 1), (2, 3, 7, 9, 4, 5, 1, 0),
+]
+
+
+@pytest.mark.parametrize("tun", [dict(), dict(Q=8, CC=3, NS=2, warps=4, minb=2)])
+@pytest.mark.parametrize("case", STRIDE_PAD)
+def test_stride_and_padding(case, tun):
+    N, C, H, W, M, K, st, p = case
+    rng = np.random.default_rng(abs(hash(case)) % 2**32)
+    x = rng.random((N, C, H, W)).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.3] = 0.0
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    ref, scale = oracle_ref(w, x, b, st, p, True)
+    csr = escoin.Csr.stretch(w, H, W, st, p).to_device(0)
+    csr.jit(n_hint=N, **tun)
+    assert csr.kernel() == escoin.KERNEL_JIT
+    out = fwd(csr, x, b, True)
+    check(out, ref, scale, b)
+    csr.set_kernel(0)
+    assert out.tobytes() == fwd(csr, x, b, True).tobytes()
+
+
 def test_unsupported_shapes_rejected():
-    w = np.ones((4, 3, 3, 3), np.float32)
-    for stride, pad in [(2, 1), (1, 0), (1, 2)]:
-        csr = escoin.Csr.stretch(w, 9, 9, stride, pad).to_device(0)
-        with pytest.raises(escoin.EscoinError) as e:
-            csr.jit()
-        assert e.value.status == escoin.ERR_UNSUPPORTED
-        assert csr.kernel() != escoin.KERNEL_JIT  # the previous kernel stays selected
+    w = np.ones((4, 3, 9, 9), np.float32)  # K > 7: no specialised form
+    csr = escoin.Csr.stretch(w, 19, 19, 2, 1).to_device(0)
+    with pytest.raises(escoin.EscoinError) as e:
+        csr.jit()
+    assert e.value.status == escoin.ERR_UNSUPPORTED
+    assert csr.kernel() != escoin.KERNEL_JIT  # the previous kernel stays selected
 
 
 @pytest.mark.parametrize("wl,name", [("alexnet", "conv3"), ("alexnet", "conv2"), ("resnet50", "res2a_branch2b"),
