@@ -193,8 +193,8 @@ int escoin_csr_autotune(escoin_csr* csr, int N, const float* in, float* out, con
  * stay compiled until escoin_csr_free, and escoin_csr_autotune times all of
  * them.  Thread-safe per handle (several tunings may compile concurrently);
  * not concurrent with forwards on the same handle.  Compile time grows with
- * nnz (about 20 s for 180k nonzeros on one host core).  Only stride 1 with
- * "same" padding (2*pad == K-1) has a specialised form.
+ * nnz (about 20 s for 180k nonzeros on one host core).  Filters up to 7x7,
+ * any stride and padding (K > 7 returns UNSUPPORTED).
  * Errors: NULL, NOT_ON_DEVICE, UNSUPPORTED (shape, tunables, compile), CUDA (load). */
 #define ESCOIN_KERNEL_JIT 1000
 int escoin_csr_jit(escoin_csr* csr, int n_hint, const int* tunables, int ntunables);
