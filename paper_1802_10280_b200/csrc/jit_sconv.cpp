@@ -462,7 +462,6 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("mad.lo.u32 %%r17, %%r4, %d, %%r15;", p.nch);
   o("%s", tg.c_str());
   o("brx.idx.uni %%r17, ts;");
-  const char* pg = "";
   for (int g = 0; g < p.nmg; ++g)
     for (int k = 0; k < p.nch; ++k) {
       o("B%d_%d:", g, k);
@@ -482,12 +481,12 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
           if (!used[t]) continue;
           const int kh = t / p.K, kw = t % p.K;
           for (int j = 0; j < P; ++j)
-            o("%sld.shared.f32 %%x%d, [%%r%d+%d];", pg, t * P + j, 40 + j,
+            o("ld.shared.f32 %%x%d, [%%r%d+%d];", t * P + j, 40 + j,
               ((buf * p.CC + cc) * p.Ls + kh * p.SWs + kw) * 4);
         }
         for (const Nz& z : l)
           for (int j = 0; j < P; ++j)
-            o("%sfma.rn.f32 %%a%d, %%x%d, 0f%08X, %%a%d;", pg, z.q * P + j, z.t * P + j, z.bits, z.q * P + j);
+            o("fma.rn.f32 %%a%d, %%x%d, 0f%08X, %%a%d;", z.q * P + j, z.t * P + j, z.bits, z.q * P + j);
       }
       o("bra.uni NEXT;");
     }

@@ -20,7 +20,7 @@ struct JitPlan {
   // layer
   int C = 0, H = 0, W = 0, M = 0, K = 0, pad = 0, E = 0, F = 0, S = 1;
   // derived
-  int mos = 1;    // images per mosaic super-row
+  int mos = 1;    // images per staged row: always 1 (stacked layout, jit_sconv.cpp header)
   int SWs = 0;    // super-image row stride (words)
   int T = 0;      // slots per CTA
   int L = 0, Ls = 0;  // staged words per channel (and padded stride)
