@@ -55,7 +55,7 @@ def parse():
     p.add_argument("--kernel", type=int, default=-1, help="sconv variant id (-1 = auto)")
     p.add_argument("--no-autotune", action="store_true", help="skip escoin_csr_autotune at setup")
     p.add_argument("--no-jit", action="store_true", help="skip the pattern-specialised kernels (escoin_csr_jit)")
-    p.add_argument("--jit-tunings", default="0;32,1,8,3,32,1;64,1,8,3,16,1",
+    p.add_argument("--jit-tunings", default="0;32,1,0,0,32,1;64,1,0,0,16,1",
                    help="';'-separated escoin_csr_jit tunings compiled per layer (0 = the library's model pick); "
                         "autotune keeps the fastest")
     p.add_argument("--no-baselines", action="store_true")

@@ -555,8 +555,11 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   p.C = C; p.H = H; p.W = W; p.M = M; p.K = K; p.pad = pad;
   p.E = E; p.F = F; p.S = stride;
   if (p.P <= 0) p.P = 1;
-  if (p.CC <= 0) p.CC = 8;
-  if (p.NS <= 1) p.NS = 3;
+  // channel chunk / stages: 5x5 (and larger) filters stage a wider halo per channel and run
+  // 2.8x the FFMAs per staged word; measured best with 4 channels x 4 stages (AlexNet conv2
+  // +5% over 8 x 3), 3x3 and 1x1 with 8 x 3 (conv3 -14% with 4 x 4).
+  if (p.CC <= 0) p.CC = K >= 5 ? 4 : 8;
+  if (p.NS <= 1) p.NS = K >= 5 ? 4 : 3;
   p.pf = p.pf < 0 ? 0 : 1;
   p.mb = p.mb > 0 ? 1 : 0;
   n_hint = std::max(1, n_hint);
