@@ -185,6 +185,37 @@ def test_alg2_equals_alg1_bitwise(shape, relu):
     assert np.all(np.abs(pre) <= scale)
 
 
+SCALE_SHAPES = [  # N, C, H, W, M, K, stride, pad — strides 1-3, pads 0-2
+    (2, 3, 6, 6, 4, 3, 1, 0), (1, 2, 7, 5, 3, 3, 2, 1), (2, 4, 9, 8, 2, 5, 1, 2), (1, 3, 8, 11, 5, 1, 1, 0),
+    (1, 2, 10, 7, 3, 3, 3, 2), (3, 1, 5, 5, 2, 5, 2, 2), (2, 5, 11, 9, 4, 3, 3, 0), (1, 4, 12, 12, 3, 5, 2, 1),
+]
+
+
+@pytest.mark.parametrize("shape", SCALE_SHAPES)
+def test_scale_equals_abs_conv(shape):
+    # scale = sum |w * x| over the stored nonzeros of row m (R#11, R#21) is the denominator of every
+    # parity tolerance.  Pinned independently of the oracle: torch conv2d in float64 of |x| (zero
+    # padded) with |w| computes sum_{c,kh,kw} |w| |x~| — the same set of terms (zero weights add 0,
+    # taps in the padding add 0).  Signed x, so a scale that dropped the |.| on x would fail.
+    # Every term is an exact fp64 product of two fp32 numbers; the sums differ only in order, so
+    # they agree to a few ulps of the sum.
+    torch = pytest.importorskip("torch")
+    N, C, H, W, M, K, s, p = shape
+    rng = np.random.default_rng(sum(shape) * 7919)
+    x = (rng.random((N, C, H, W)) * 2 - 1).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.4] = 0.0
+    rp, ci, v = oracle.csr_stretch(w, H, W, s, p)
+    _, scale = oracle.sconv(x, rp, ci, v, M, K, s, p, bias=None, relu=False)
+    ind = torch.nn.functional.conv2d(torch.from_numpy(np.abs(x).astype(np.float64)),
+                                     torch.from_numpy(np.abs(w).astype(np.float64)), stride=s, padding=p).numpy()
+    assert scale.shape == ind.shape
+    assert np.allclose(scale, ind, rtol=1e-13, atol=0.0)
+    # and a bias does not enter scale (the tolerance adds |bias| separately)
+    _, scale_b = oracle.sconv(x, rp, ci, v, M, K, s, p, bias=np.full(M, 5.0, np.float32), relu=True)
+    assert np.array_equal(scale_b, scale)
+
+
 @pytest.mark.parametrize("shape", SHAPES[:5])
 def test_points_equal_full(shape):
     N, C, H, W, M, K, s, p = shape
