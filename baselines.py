@@ -5,7 +5,11 @@ P:699-703): im2col followed by cuBLAS sgemm (dense pruned weights) or by
 cuSPARSE csrmm (CSR weights).  Here:
   * im2col          torch.nn.functional.unfold (one CUDA kernel, all images)
   * cublas          torch.matmul -> cublasSgemmStridedBatched, FP32 compute,
-                    TF32 disabled (same precision as the sparse path)
+                    TF32 disabled (same precision as the sparse path): one
+                    [M x CRS] x [CRS x EF] GEMM per image (Caffe's per-image loop)
+  * cublas_gemm     the same lowering as ONE GEMM per group over the whole
+                    batch: [M x CRS] x [CRS x N*EF] (the lowered matrix is
+                    re-laid out once; bigger GEMMs, the fairer dense baseline)
   * cusparse        torch.sparse CSR @ dense -> cusparseSpMM (the legacy
                     csrmm API no longer exists), on the [CRS x N*EF] lowered
                     matrix; the two layout permutes it needs are included
@@ -50,6 +54,10 @@ class LoweredConv:
             col = torch.nn.functional.unfold(xg, L.K, padding=L.pad, stride=L.stride)  # [N, CRS, EF]
             if self.mode == "cublas":
                 torch.matmul(self.w[gi], col, out=o[:, gi * Mg:(gi + 1) * Mg])
+            elif self.mode == "cublas_gemm":
+                B = col.transpose(0, 1).reshape(col.shape[1], N * EF)
+                Y = torch.mm(self.w[gi], B)                              # [Mg, N*EF], one SGEMM
+                o[:, gi * Mg:(gi + 1) * Mg].copy_(Y.view(Mg, N, EF).transpose(0, 1))
             else:
                 B = col.transpose(0, 1).reshape(col.shape[1], N * EF)
                 Y = torch.sparse.mm(self.a[gi], B)                       # [Mg, N*EF]

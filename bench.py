@@ -2,12 +2,18 @@
 """Benchmark of the Escoin direct sparse convolution on B200.
 
 One step = one pass of the hot path over one batch: every sparse CONV layer
-of the workload (default: pruned AlexNet conv2-conv5, BASELINE configs[1]),
-batch 128 per GPU, through escoin_sconv_forward (stretched CSR x dense NCHW,
-bias + ReLU fused).  Inputs resident in HBM; L2 flushed between steps (a
-256 MB write, outside the per-step events).  Multi-GPU: torchrun, one rank
-per GPU, each rank runs its own 128 images (weak scaling; weights broadcast
-once over NCCL; no per-layer collectives); time = MAX over ranks.
+of the workload (default: pruned ResNet-50 v1, its 16 sparse 3x3 layers,
+BASELINE configs[3]) over the global batch of 128, through
+escoin_sconv_forward (stretched CSR x dense NCHW, bias + ReLU fused).  Inputs
+resident in HBM; L2 flushed before every step (a 256 MB write, outside the
+per-step events).  The step is captured once as a CUDA graph and replayed.
+
+Multi-GPU (torchrun, one rank per GPU): STRONG scaling by default — the
+global batch is split contiguously (rank r owns images shard_range(128, r, G)),
+weights are stretched on rank 0 and broadcast once over NCCL, the
+specialised kernels are compiled once per node (rank 0 fills the cubin cache
+ESCOIN_JIT_CACHE, the other ranks load it), no per-layer collectives; time =
+MAX over ranks.  `--weak` gives every rank its own 128 images instead.
 
 Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle
 instead (the reference arm for this tier).
@@ -28,6 +34,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# cubins of the specialised kernels, shared by the ranks of this node (never shipped: .gpurunignore)
+os.environ.setdefault("ESCOIN_JIT_CACHE", os.path.join(ROOT, "build", "jit_cache"))
+os.makedirs(os.environ["ESCOIN_JIT_CACHE"], exist_ok=True)
 
 from paper_1802_10280_b200 import inputs, shard, workloads  # noqa: E402
 
@@ -40,22 +49,27 @@ WL_NAMES = {"alexnet": "pruned AlexNet conv2-conv5 (4 sparse CONV layers)",
             "resnet50": "pruned ResNet-50 v1 16 sparse 3x3 CONV layers",
             "resnet50_v15": "pruned ResNet-50 v1.5 16 sparse 3x3 CONV layers (3 with stride 2)",
             "tiny": "tiny conv layer N=1 C=16 14x14 M=32 3x3"}
-METRIC = "sparse-conv images/s (whole stack) at batch 128/GPU"
+METRIC = "sparse-conv images/s (whole stack of sparse layers, global batch 128)"
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=100)
-    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="escoin", choices=["escoin", "reference"])
-    p.add_argument("--workload", default="alexnet", choices=list(WL_NAMES))
-    p.add_argument("--batch", type=int, default=None, help="images per GPU (default: the workload's, 128)")
+    p.add_argument("--workload", default="resnet50", choices=list(WL_NAMES))
+    p.add_argument("--batch", type=int, default=None, help="GLOBAL batch (default: the workload's, 128)")
+    p.add_argument("--weak", action="store_true", help="weak scaling: every rank runs its own --batch images")
+    p.add_argument("--tune-variants", action="store_true",
+                   help="autotune also over the compiled interpreter variants (default: specialised kernels only, "
+                        "the variants only where no specialised kernel exists)")
+    p.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured graph")
     p.add_argument("--sparsity", type=int, default=800, help="per-mille (ASSUMED 800, reading R#14)")
     p.add_argument("--kernel", type=int, default=-1, help="sconv variant id (-1 = auto)")
     p.add_argument("--no-autotune", action="store_true", help="skip escoin_csr_autotune at setup")
     p.add_argument("--no-jit", action="store_true", help="skip the pattern-specialised kernels (escoin_csr_jit)")
-    p.add_argument("--jit-tunings", default="0;32,1,0,0,32,1;64,1,0,0,16,1",
+    p.add_argument("--jit-tunings", default="0;32,1,0,0,32,1;64,1,0,0,16,1;16,1,0,0,16,2",
                    help="';'-separated escoin_csr_jit tunings compiled per layer (0 = the library's model pick); "
                         "autotune keeps the fastest")
     p.add_argument("--no-baselines", action="store_true")
@@ -129,9 +143,18 @@ class LayerRun:
     pass
 
 
-def setup(args, wl, device, rank, world, torch, escoin):
-    B = args.batch or wl.batch
-    n0 = rank * B  # weak scaling: rank r owns global images [r*B, (r+1)*B)
+def batch_range(args, wl, rank, world):
+    """Global image range [n0, n0 + B) of this rank: strong scaling splits the global batch
+    (shard.shard_range), weak scaling gives every rank its own full batch."""
+    GB = args.batch or wl.batch
+    if args.weak:
+        return rank * GB, GB, GB * world
+    a, b = shard.shard_range(GB, rank, world)
+    return a, b - a, GB
+
+
+def setup(args, wl, device, rank, world, torch, escoin, flush):
+    n0, B, GB = batch_range(args, wl, rank, world)
     runs = []
     for L in wl.layers:
         r = LayerRun()
@@ -145,7 +168,7 @@ def setup(args, wl, device, rank, world, torch, escoin):
         else:
             rp = ci = v = bias = None
             r.w_dense = None
-        if world > 1:
+        if world > 1:  # A3: weights replicated once from rank 0 (NCCL broadcast over NVLink)
             t = shard.broadcast_csr(rp, ci, v, bias, device)
             r.d_csr = t[:3]
             r.bias = t[3]
@@ -170,41 +193,57 @@ def setup(args, wl, device, rank, world, torch, escoin):
         r.alg_bytes = 4.0 * (B * L.C * L.H * L.W + B * L.M * L.E * L.F + 2 * r.nnz + L.M + 1 + L.M)
         runs.append(r)
     torch.cuda.synchronize()
+    setup_t = {}
     if args.kernel == -1 and not args.no_jit:
-        # pattern-specialised kernels (escoin_csr_jit): compiled once at setup, untimed, one host
-        # thread per layer (the library releases the GIL; compile time grows with nnz)
+        # pattern-specialised kernels (escoin_csr_jit): compiled at setup, untimed.  Every (layer,
+        # tuning) is submitted at once; the library bounds concurrent compiler threads to the host's
+        # cores and splits large layers into units compiled in parallel.  Rank 0 compiles into the
+        # node's cubin cache (ESCOIN_JIT_CACHE) first; the other ranks then load the same cubins.
         tunings = [[int(v) for v in t.split(",")] if t.strip() not in ("", "0") else []
                    for t in args.jit_tunings.split(";")]
 
         def jit(task):
             r, tun = task
-            t0 = time.time()
             try:
                 r.csr.jit(B, *tun)
             except escoin.EscoinError as e:
                 if e.status != escoin.ERR_UNSUPPORTED:
                     raise
                 return None
-            return round(time.time() - t0, 2)
+            st = r.csr.jit_stats()
+            return st["compile_s"], st["cache_hits"], st["units"]
         tasks = [(r, t) for r in runs for t in tunings]
         tasks.sort(key=lambda rt: -rt[0].nnz)  # largest compiles first
-        # host cores are shared by the ranks of this node (compile memory and time)
-        with ThreadPoolExecutor(max(1, min(len(tasks), (os.cpu_count() or 1) // max(1, world)))) as ex:
-            for (r, _), t in zip(tasks, ex.map(jit, tasks)):
-                if t is not None:
-                    r.jit_s = round(getattr(r, "jit_s", 0.0) + t, 2)
+
+        def compile_all():
+            t0 = time.time()
+            with ThreadPoolExecutor(max(1, min(len(tasks), 64))) as ex:
+                for (r, _), res in zip(tasks, ex.map(jit, tasks)):
+                    if res is not None:
+                        r.jit_s = round(getattr(r, "jit_s", 0.0) + res[0], 2)
+                        r.jit_hits = getattr(r, "jit_hits", 0) + res[1]
+            return round(time.time() - t0, 1)
+        if world > 1 and rank != 0:
+            torch.distributed.barrier()  # rank 0 compiles first
+        setup_t["jit_compile_wall_s"] = compile_all()
+        if world > 1 and rank == 0:
+            torch.distributed.barrier()
+    t0 = time.time()
     for r in runs:
         if args.kernel == -1 and not args.no_autotune:
-            # kernel customization (paper §3.4): measured once at setup, untimed; includes the
-            # pattern-specialised kernel when one was compiled
-            kid, kms = r.csr.autotune(B, r.x, r.out, r.bias, True, 3, torch.cuda.current_stream().cuda_stream)
+            # kernel customization (paper §3.4): measured once at setup, untimed, each candidate
+            # timed alone after an L2 flush like the timed steps (escoin_csr_autotune_ex)
+            flags = escoin.TUNE_JIT
+            if args.tune_variants or getattr(r, "jit_s", None) is None:
+                flags |= escoin.TUNE_VARIANTS
+            kid, kms = r.csr.autotune_ex(B, r.x, r.out, r.bias, True, 5, torch.cuda.current_stream().cuda_stream,
+                                         flush=flush, flags=flags)
             r.tune = {"kernel_id": kid, "ms": round(kms, 4)}
-        r.kernel = escoin.kernel_name(r.csr.kernel())
-        if r.csr.kernel() == escoin.KERNEL_JIT:
-            ji = r.csr.jit_info()
-            r.kernel = "jit_q%d_p%d_w%d" % (ji["Q"], ji["P"], ji["warps"])
+        r.kernel = r.csr.label()
+        r.units = r.csr.jit_info()["units"] if r.csr.kernel() == escoin.KERNEL_JIT else 1
+    setup_t["autotune_s"] = round(time.time() - t0, 1)
     torch.cuda.synchronize()
-    return runs, B
+    return runs, n0, B, GB, setup_t
 
 
 def fwd(escoin, r, stream):
@@ -214,24 +253,56 @@ def fwd(escoin, r, stream):
 
 
 def time_device(torch, runs, steps, warmup, flush, step_fn):
-    """Per-step CUDA events around each layer; L2 flushed before every step."""
+    """Eager launches, per-step CUDA events around each layer; L2 flushed before every step."""
     s = torch.cuda.current_stream()
     for _ in range(warmup):
         flush.zero_()
         step_fn()
     torch.cuda.synchronize()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(runs) + 1)] for _ in range(steps)]
-    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" profiles only these launches
     for k in range(steps):
         flush.zero_()
         ev[k][0].record(s)
         for i, r in enumerate(runs):
             step_fn(i)
             ev[k][i + 1].record(s)
-    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     per_layer = np.array([[ev[k][i].elapsed_time(ev[k][i + 1]) for i in range(len(runs))] for k in range(steps)])
     return per_layer  # ms [steps][layers]
+
+
+def capture_step(torch, step_fn):
+    """The whole step (every layer's launch, incl. multi-unit fork/join) as one CUDA graph."""
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):  # one eager pass on the capture stream first (module/bind warm-up)
+        step_fn()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step_fn()
+    torch.cuda.synchronize()
+    return g
+
+
+def time_graph(torch, g, steps, warmup, flush):
+    """K replays of the step graph, each between its own events; L2 flushed before every step (outside)."""
+    s = torch.cuda.current_stream()
+    for _ in range(warmup):
+        flush.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" profiles only these launches
+    for a, b in ev:
+        flush.zero_()
+        a.record(s)
+        g.replay()
+        b.record(s)
+    torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
+    return np.array([a.elapsed_time(b) for a, b in ev])  # ms per step
 
 
 def cpu_oracle_timed(wl, args, seconds, max_images):
@@ -265,6 +336,15 @@ def load_traffic(workload):
         return json.load(open(path)).get(workload, {})
     except Exception:
         return {}
+
+
+def load_ffma_peak():
+    """The FFMA microbenchmark's measured FP32 peak (profiles/ffma_peak.json), for context."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ffma_peak.json")))
+        return {"tflops": d.get("best_tflops"), "source": "profiles/ffma_peak.json"}
+    except Exception:
+        return None
 
 
 def measured_peaks():
@@ -303,9 +383,9 @@ def run_reference(args):
     value = per_step_images / (ms / 1e3)
     sample = "%d image(s) through all %d layers per step" % (per_step_images, len(items))
     line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": WL_NAMES[args.workload], "batch_per_gpu": wl.batch,
+            "config": {"workload": WL_NAMES[args.workload], "global_batch": wl.batch,
                        "sparsity": args.sparsity / 1000.0, "sample": sample},
             "cpu_baseline": {"value": value, "unit": "images/s", "cores": oracle.num_threads(), "kind": "oracle",
                              "sample": sample},
@@ -328,22 +408,31 @@ def main():
     device = torch.device("cuda", 0 if args.same_device else local)
     torch.cuda.set_device(device)
     if world > 1:
+        import datetime
+
         import torch.distributed as dist
+        # setup compiles the specialised kernels while the other ranks wait at a barrier
+        to = datetime.timedelta(minutes=60)
         if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=device)
+            dist.init_process_group("nccl", device_id=device, timeout=to)
         else:
-            dist.init_process_group(args.dist_backend)
+            dist.init_process_group(args.dist_backend, timeout=to)
     wl = workloads.workload(args.workload)
-    runs, B = setup(args, wl, device, rank, world, torch, escoin)
-    stream = torch.cuda.current_stream().cuda_stream
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+    runs, n0, B, GB, setup_t = setup(args, wl, device, rank, world, torch, escoin, flush)
+    stream = torch.cuda.current_stream().cuda_stream
+    images = GB if not args.weak else B * world  # images all ranks process per step
 
     def step_fn(i=None):
+        s_ = torch.cuda.current_stream().cuda_stream  # the capture stream inside torch.cuda.graph
         if i is None:
             for r in runs:
-                fwd(escoin, r, stream)
+                fwd(escoin, r, s_)
         else:
-            fwd(escoin, runs[i], stream)
+            fwd(escoin, runs[i], s_)
+
+    graph = None if args.no_graph else capture_step(torch, step_fn)
+    launches_per_step = sum(r.units for r in runs)
 
     # ---------------- device-timed region (K steps, barrier + sync both sides)
     if world > 1:
@@ -351,14 +440,20 @@ def main():
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         wall0 = time.perf_counter()
-        per_layer = time_device(torch, runs, args.steps, args.warmup, flush, step_fn)
+        if graph is not None:
+            step_times = time_graph(torch, graph, args.steps, args.warmup, flush)
+        else:
+            step_times = time_device(torch, runs, args.steps, args.warmup, flush, step_fn).sum(1)
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
     if world > 1:
         torch.distributed.barrier()
-    step_ms_local = float(per_layer.sum(1).mean())
+    step_ms_local = float(np.mean(step_times))
     step_ms = shard.max_over_ranks(step_ms_local, device)
-    value = B * world / (step_ms / 1e3)
+    value = images / (step_ms / 1e3)
+    # per-layer breakdown (the roofline's dominant kernel): the same launches eagerly, one event
+    # pair per layer on the launching stream, same flush, same number of steps
+    per_layer = time_device(torch, runs, args.steps, max(2, args.warmup // 2), flush, step_fn)
     layer_ms = per_layer.mean(0)
     layer_ms_min, layer_ms_med = per_layer.min(0), np.median(per_layer, 0)
 
@@ -419,18 +514,23 @@ def main():
     for r, ms, mn, md in zip(runs, layer_ms, layer_ms_min, layer_ms_med):
         layers_out.append({"layer": r.L.name, "ms": round(float(ms), 5), "ms_min": round(float(mn), 5),
                            "ms_median": round(float(md), 5), "kernel": r.kernel, "nnz": r.nnz,
-                           "jit_compile_s": getattr(r, "jit_s", None),
+                           "jit_compile_s": getattr(r, "jit_s", None), "units": r.units,
+                           "autotune_ms": (r.tune or {}).get("ms"),
                            "gflop": round(r.flops / 1e9, 4),
                            "tflops": round(r.flops / (ms / 1e3) / 1e12, 3),
                            "frac_fp32": round(r.flops / (ms / 1e3) / 1e12 / peak_tf, 4),
                            "alg_gbs": round(r.alg_bytes / (ms / 1e3) / 1e9, 1)})
 
     line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WL_NAMES[args.workload], "batch_per_gpu": B, "global_batch": B * world,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; He-normal weights magnitude-pruned, "
+                                                      "U[0,1) activations)",
+            "config": {"workload": WL_NAMES[args.workload], "global_batch": images, "batch_per_gpu": B,
+                       "rank0_images": [n0, n0 + B],
                        "sparsity": args.sparsity / 1000.0, "sparsity_note": "ASSUMED 80% (paper prints none)",
                        "parallelism": "dp%d (batch-sharded, weights replicated)" % world,
+                       "timing": "CUDA graph of the whole step" if graph is not None else "eager launches",
                        "l2": "flushed (256 MB write) before every step, outside the per-step events"},
             "roofline": {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak_tf, 2),
                          "unit": "TFLOP/s", "frac": round(achieved / peak_tf, 4), "traffic": traffic,
@@ -438,12 +538,18 @@ def main():
                          "peak_basis": "FP32 FFMA %d SMs x 128 lanes x 2 x %.0f MHz (derived, DESIGN.md)" % (
                              nsm, sm_max),
                          "hbm_view": {"alg_gbs": round(rd.alg_bytes / (layer_ms[dom] / 1e3) / 1e9, 1),
-                                      "peak_gbs": peaks.get("hbm_gbs")}},
+                                      "peak_gbs": peaks.get("hbm_gbs")},
+                         "measured_ffma_peak": load_ffma_peak(),
+                         "stack": {"gflop": round(sum(r.flops for r in runs) / 1e9, 3),
+                                   "tflops_graph": round(sum(r.flops for r in runs) / (step_ms_local / 1e3) / 1e12, 3),
+                                   "frac_graph": round(sum(r.flops for r in runs) / (step_ms_local / 1e3) / 1e12
+                                                       / peak_tf, 4)}},
             "layers": layers_out,
-            "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": "images/s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": images / (e2e_ms / 1e3), "unit": "images/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": len(runs) * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
+            "setup": setup_t,
             "wall_s_timed_region": round(wall, 3)}
 
     if rank == 0 and world == 1 and not args.no_baselines:
@@ -486,9 +592,10 @@ def run_baselines(torch, escoin, runs, flush, stream, args, sconv_value):
         return float(np.median(tot))
 
     B = runs[0].x.shape[0]
-    names = {"cublas": "im2col+cublas_sgemm", "cusparse": "im2col+cusparse_spmm", "cudnn": "cudnn_fp32_dense",
+    names = {"cublas": "im2col+cublas_sgemm", "cublas_gemm": "im2col+cublas_sgemm_one_gemm_per_batch",
+             "cusparse": "im2col+cusparse_spmm", "cudnn": "cudnn_fp32_dense",
              "cudnn_tf32": "cudnn_tf32_dense_tensorcore", "cudnn_bf16": "cudnn_bf16_dense_tensorcore"}
-    for mode in ["cublas", "cusparse", "cudnn", "cudnn_tf32", "cudnn_bf16"]:
+    for mode in ["cublas", "cublas_gemm", "cusparse", "cudnn", "cudnn_tf32", "cudnn_bf16"]:
         per = {}
         try:
             for r in runs:

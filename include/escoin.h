@@ -170,6 +170,26 @@ int escoin_csr_get_kernel(const escoin_csr* csr, int* id);
  * Errors: as escoin_sconv_forward, plus CUDA/ALLOC from the rebuilds. */
 int escoin_csr_autotune(escoin_csr* csr, int N, const float* in, float* out, const float* bias, int relu,
                         int reps, void* cuda_stream, int* best_id, float* best_ms);
+/* escoin_csr_autotune under the caller's measurement conditions:
+ *   flush_buf / flush_bytes  device scratch (or NULL / 0) memset before EVERY timed rep, outside the
+ *              timing events, so candidates are timed with a cold L2 like a flushed benchmark step
+ *              (give >= 2x the L2 size, e.g. 256 MB on B200);
+ *   flags      ESCOIN_TUNE_VARIANTS (the compiled variants and the paper mapping) and/or
+ *              ESCOIN_TUNE_JIT (every specialised kernel compiled by escoin_csr_jit).
+ * Each candidate: one warm-up forward, then `reps` single forwards each between its own events;
+ * the candidate's time is the median (*best_ms).  The label of the winner is
+ * escoin_csr_kernel_label.  Errors: as escoin_csr_autotune; NULL (flush_bytes > 0, no buffer),
+ * UNSUPPORTED (no flag, or no candidate). */
+#define ESCOIN_TUNE_VARIANTS 1
+#define ESCOIN_TUNE_JIT 2
+int escoin_csr_autotune_ex(escoin_csr* csr, int N, const float* in, float* out, const float* bias, int relu,
+                           int reps, void* cuda_stream, void* flush_buf, int64_t flush_bytes, int flags,
+                           int* best_id, float* best_ms);
+/* Full label of the handle's current kernel, every tunable included, into buf (NUL-terminated,
+ * truncated to cap): specialised kernels "jit_q<Q>_p<P>_cc<CC>_ns<NS>_w<warps>_b<CTAs/SM>_pf<prefetch>
+ * _mb<mbarrier>_u<units>_sw<staged row stride>", variants "<name>_wm.._wp.._nb.._tr.._cc.._ns.._mos.._scs..",
+ * "paper_mapping".  Errors: NULL; OVERFLOW if truncated. */
+int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
 
 /* ---------------------------------------------------------------- pattern-specialised kernel
  * Kernel customisation (§3.4) taken to the layer's weights: the
@@ -182,12 +202,19 @@ int escoin_csr_autotune(escoin_csr* csr, int N, const float* in, float* out, con
  * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
  *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
  *              forwards accept any N.
- *   tunables   NULL or ntunables (<= 8) ints {Q output channels per CTA,
+ *   tunables   NULL or ntunables (<= 9) ints {Q output channels per CTA,
  *              P pixels per lane, CC channels per stage, NS stages, warps per
  *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off),
  *              mbarrier pipeline (> 0 = on: warps drift up to NS-2 chunks
- *              instead of one CTA barrier per chunk)}; <= 0 entries take the
- *              defaults.
+ *              instead of one CTA barrier per chunk), units (separately
+ *              compiled modules the output-channel groups are split into,
+ *              compiled in parallel host threads and launched concurrently
+ *              on forked streams; <= 0: about one per 24k nonzeros, <= 32)};
+ *              <= 0 entries take the defaults.
+ * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
+ * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE
+ * names a writable directory, cubins are stored there keyed by a hash of their PTX
+ * and reused by later calls and other processes (the ranks of a node compile once).
  * On success the new kernel is added to the handle's specialised kernels
  * and selected (the handle's kernel becomes ESCOIN_KERNEL_JIT); earlier ones
  * stay compiled until escoin_csr_free, and escoin_csr_autotune times all of
@@ -199,9 +226,15 @@ int escoin_csr_autotune(escoin_csr* csr, int N, const float* in, float* out, con
 #define ESCOIN_KERNEL_JIT 1000
 int escoin_csr_jit(escoin_csr* csr, int n_hint, const int* tunables, int ntunables);
 /* Parameters of the handle's specialised kernel: tunables6 (6 ints, as above,
- * defaults resolved), mosaic width, registers per thread, cubin bytes.  Any
+ * defaults resolved), units, registers per thread (max over units), cubin bytes
+ * (sum over units).  Any output pointer may be NULL.  Errors: NULL, UNSUPPORTED
+ * (no specialised kernel). */
+int escoin_csr_jit_info(const escoin_csr* csr, int* tunables6, int* units, int* regs, int64_t* code_bytes);
+/* Build statistics of the handle's selected specialised kernel: units, units loaded from
+ * ESCOIN_JIT_CACHE, wall seconds of the build (generate + compile + load), PTX bytes.  Any
  * output pointer may be NULL.  Errors: NULL, UNSUPPORTED (no specialised kernel). */
-int escoin_csr_jit_info(const escoin_csr* csr, int* tunables6, int* mos, int* regs, int64_t* code_bytes);
+int escoin_csr_jit_stats(const escoin_csr* csr, int* units, int* cache_hits, double* compile_s,
+                         int64_t* ptx_bytes);
 
 /* ---- Benchmark-only comparison point (NOT the method; SURVEY 8(b) "escoin_bench_*",
  * north_star: "a dense tcgen05 implicit-GEMM is kept only as a measured comparison point").

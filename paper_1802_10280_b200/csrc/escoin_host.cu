@@ -8,6 +8,7 @@
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <string>
 #include <vector>
 
 #include "escoin.h"
@@ -865,28 +866,32 @@ int auto_kernel(const escoin_csr* h) {
 }
 
 // Pattern-specialised kernel (jit_sconv.cpp): plan, generate, compile, load.
-// tun = {Q, P, CC, NS, warps, minb, prefetch, mbarrier} (<= 0: default; prefetch < 0 = off) or NULL.
+// tun = {Q, P, CC, NS, warps, minb, prefetch, mbarrier, units} (<= 0: default; prefetch < 0 = off) or NULL.
 int build_jit(escoin_csr* h, int n_hint, const int* tun) {
   JitPlan p;
   if (tun) {
     p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6]; p.mb = tun[7];
+    p.units = tun[8];
   }
-  if (p.P > 8 || p.Q > 256 || p.CC > 64 || p.NS > 6 || p.warps > 32 || p.minb > 8) return ESCOIN_ERR_UNSUPPORTED;
+  if (p.P > 8 || p.Q > 256 || p.CC > 64 || p.NS > 6 || p.warps > 32 || p.minb > 8 || p.units > 32)
+    return ESCOIN_ERR_UNSUPPORTED;
   const double density = double(h->nnz) / (double(h->M) * h->C * h->K * h->K);
   if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint, density) != 0)
     return ESCOIN_ERR_UNSUPPORTED;
   if (int64_t(p.warps) * 32 * p.minb > 2048) return ESCOIN_ERR_UNSUPPORTED;
   if (h->rowptr.size() != size_t(h->M) + 1) return ESCOIN_ERR_UNSUPPORTED;
+  auto same = [&](const JitPlan& q) {
+    return q.Q == p.Q && q.P == p.P && q.CC == p.CC && q.NS == p.NS && q.warps == p.warps && q.minb == p.minb &&
+           q.pf == p.pf && q.mb == p.mb && q.units == p.units && q.T == p.T && q.L == p.L && q.SWs == p.SWs;
+  };
   {
     std::lock_guard<std::mutex> lk(h->jit_mu);
-    for (JitModule* jm : h->jits) {  // this tuning was compiled before: select it
-      const JitPlan& q = jm->plan;
-      if (q.Q == p.Q && q.P == p.P && q.CC == p.CC && q.NS == p.NS && q.warps == p.warps && q.minb == p.minb &&
-          q.pf == p.pf && q.mb == p.mb && q.T == p.T && q.L == p.L) {
+    for (JitModule* jm : h->jits)  // this tuning was compiled before: select it
+      if (same(jm->plan)) {
         h->jit = jm;
+        h->kernel = ESCOIN_KERNEL_JIT;
         return ESCOIN_OK;
       }
-    }
   }
   JitModule* jm = new (std::nothrow) JitModule();
   if (!jm) return ESCOIN_ERR_ALLOC;
@@ -896,8 +901,17 @@ int build_jit(escoin_csr* h, int n_hint, const int* tun) {
     return rc == -2 ? ESCOIN_ERR_UNSUPPORTED : ESCOIN_ERR_CUDA;
   }
   std::lock_guard<std::mutex> lk(h->jit_mu);
+  for (JitModule* o : h->jits)  // compiled concurrently by another thread meanwhile: keep that one
+    if (same(o->plan)) {
+      jit_free(*jm);
+      delete jm;
+      h->jit = o;
+      h->kernel = ESCOIN_KERNEL_JIT;
+      return ESCOIN_OK;
+    }
   h->jits.push_back(jm);
   h->jit = jm;
+  h->kernel = ESCOIN_KERNEL_JIT;
   return ESCOIN_OK;
 }
 
@@ -1254,54 +1268,73 @@ int escoin_csr_set_kernel(escoin_csr* h, int id) {
 
 int escoin_csr_autotune(escoin_csr* h, int N, const float* in, float* out, const float* bias, int relu, int reps,
                         void* cuda_stream, int* best_id, float* best_ms) {
+  return escoin_csr_autotune_ex(h, N, in, out, bias, relu, reps, cuda_stream, nullptr, 0,
+                                ESCOIN_TUNE_VARIANTS | ESCOIN_TUNE_JIT, best_id, best_ms);
+}
+
+int escoin_csr_autotune_ex(escoin_csr* h, int N, const float* in, float* out, const float* bias, int relu, int reps,
+                           void* cuda_stream, void* flush_buf, int64_t flush_bytes, int flags, int* best_id,
+                           float* best_ms) {
   if (!h) return ESCOIN_ERR_NULL;
   if (!h->on_device) return ESCOIN_ERR_NOT_ON_DEVICE;
+  if (flush_bytes < 0 || (flush_bytes > 0 && !flush_buf)) return ESCOIN_ERR_NULL;
+  if (!(flags & (ESCOIN_TUNE_VARIANTS | ESCOIN_TUNE_JIT))) return ESCOIN_ERR_UNSUPPORTED;
   if (reps < 1) reps = 1;
   DeviceGuard g(h->device);
   if (!g.ok) return ESCOIN_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return ESCOIN_ERR_CUDA;
+  int rc = ESCOIN_OK;
+  // one warm-up forward, then `reps` forwards each timed alone (events on s) after an optional L2
+  // flush (a memset of flush_buf, outside the events) — the conditions bench.py measures under;
+  // the candidate's time is the median
+  auto time_it = [&](float* ms_out) -> int {
+    int r = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
+    if (r != ESCOIN_OK) return r;
+    std::vector<float> t;
+    for (int k = 0; k < reps; ++k) {
+      if (flush_bytes > 0 && cudaMemsetAsync(flush_buf, k & 0xff, size_t(flush_bytes), s) != cudaSuccess)
+        return ESCOIN_ERR_CUDA;
+      cudaEventRecord(e0, s);
+      r = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
+      if (r != ESCOIN_OK) return r;
+      cudaEventRecord(e1, s);
+      if (cudaEventSynchronize(e1) != cudaSuccess) return ESCOIN_ERR_CUDA;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      t.push_back(ms);
+    }
+    std::sort(t.begin(), t.end());
+    *ms_out = t[t.size() / 2];
+    return ESCOIN_OK;
+  };
   int nv = 0;
   const TiledVariant* tv = tiled_variants(&nv);
   int best = -1, best_rank = 0;
   float best_t = 0.f;
-  int rc = ESCOIN_OK;
   constexpr int kRanks = 4;  // tiling candidates (distinct geometries) measured per variant
-  for (int idr = 0; idr <= nv * kRanks && rc == ESCOIN_OK; ++idr) {
+  for (int idr = 0; (flags & ESCOIN_TUNE_VARIANTS) && idr <= nv * kRanks && rc == ESCOIN_OK; ++idr) {
     const int id = idr / kRanks, rank = idr % kRanks;
     if (id == 0 && rank > 0) continue;
     if (id > 0 && (tv[id - 1].K != h->K || tv[id - 1].S != h->stride)) continue;
     if (cudaStreamSynchronize(s) != cudaSuccess) { rc = ESCOIN_ERR_CUDA; break; }
     if (set_kernel(h, id, s, rank) != ESCOIN_OK) continue;  // no (further) tiling fits: skip
-    rc = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
-    if (rc != ESCOIN_OK) break;
-    cudaEventRecord(e0, s);
-    for (int r = 0; r < reps && rc == ESCOIN_OK; ++r)
-      rc = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
-    cudaEventRecord(e1, s);
-    if (cudaEventSynchronize(e1) != cudaSuccess) { rc = ESCOIN_ERR_CUDA; break; }
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    ms /= reps;
+    if ((rc = time_it(&ms)) != ESCOIN_OK) break;
     if (best < 0 || ms < best_t) { best = id; best_rank = rank; best_t = ms; }
   }
   JitModule* best_jit = h->jit;
-  for (size_t ji = 0; ji < h->jits.size() && rc == ESCOIN_OK; ++ji) {  // every compiled specialised kernel
-    h->jit = h->jits[ji];
+  const int prev_kernel = h->kernel;
+  for (size_t ji = 0; (flags & ESCOIN_TUNE_JIT) && ji < h->jits.size() && rc == ESCOIN_OK; ++ji) {
+    h->jit = h->jits[ji];  // every compiled specialised kernel
     h->kernel = ESCOIN_KERNEL_JIT;
-    rc = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
-    cudaEventRecord(e0, s);
-    for (int r = 0; r < reps && rc == ESCOIN_OK; ++r)
-      rc = escoin_sconv_forward(N, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, h, in, out, bias, relu, s);
-    cudaEventRecord(e1, s);
-    if (rc == ESCOIN_OK && cudaEventSynchronize(e1) != cudaSuccess) rc = ESCOIN_ERR_CUDA;
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    ms /= reps;
-    if (rc == ESCOIN_OK && (best < 0 || ms < best_t)) { best = ESCOIN_KERNEL_JIT; best_t = ms; best_jit = h->jit; }
+    if ((rc = time_it(&ms)) != ESCOIN_OK) break;
+    if (best < 0 || ms < best_t) { best = ESCOIN_KERNEL_JIT; best_t = ms; best_jit = h->jit; }
   }
   h->jit = best_jit;
+  h->kernel = prev_kernel;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (rc != ESCOIN_OK) return rc;
@@ -1313,18 +1346,47 @@ int escoin_csr_autotune(escoin_csr* h, int N, const float* in, float* out, const
   return ESCOIN_OK;
 }
 
+int escoin_csr_kernel_label(const escoin_csr* h, char* buf, int cap) {
+  if (!h || !buf || cap < 1) return ESCOIN_ERR_NULL;
+  std::string l;
+  if (h->kernel == ESCOIN_KERNEL_JIT && h->jit) {
+    l = jit_label(*h->jit);
+  } else if (h->kernel == 0) {
+    l = "paper_mapping";
+  } else if (h->kernel > 0) {
+    int nv = 0;
+    const TiledVariant* tv = tiled_variants(&nv);
+    char b[160];
+    const TiledArgs& a = h->targs;
+    snprintf(b, sizeof b, "%s_wm%d_wp%d_nb%d_tr%d_cc%d_ns%d_mos%d_scs%d", h->kernel <= nv ? tv[h->kernel - 1].name : "?",
+             a.WM, a.WP, a.NB, a.TR, a.CC, a.NS, a.mos, a.SCs);
+    l = b;
+  } else {
+    l = "auto";
+  }
+  std::snprintf(buf, size_t(cap), "%s", l.c_str());
+  return int(l.size()) < cap ? ESCOIN_OK : ESCOIN_ERR_OVERFLOW;
+}
+
+int escoin_csr_jit_stats(const escoin_csr* h, int* units, int* cache_hits, double* compile_s, int64_t* ptx_bytes) {
+  if (!h) return ESCOIN_ERR_NULL;
+  if (!h->jit) return ESCOIN_ERR_UNSUPPORTED;
+  if (units) *units = int(h->jit->units.size());
+  if (cache_hits) *cache_hits = h->jit->cache_hits;
+  if (compile_s) *compile_s = h->jit->compile_s;
+  if (ptx_bytes) *ptx_bytes = int64_t(h->jit->ptx_bytes);
+  return ESCOIN_OK;
+}
+
 int escoin_csr_jit(escoin_csr* h, int n_hint, const int* tunables, int ntunables) {
   if (!h) return ESCOIN_ERR_NULL;
   if (!h->on_device) return ESCOIN_ERR_NOT_ON_DEVICE;
-  if (ntunables < 0 || ntunables > 8 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
-  int tun[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (ntunables < 0 || ntunables > 9 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
+  int tun[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
   DeviceGuard g(h->device);
   if (!g.ok) return ESCOIN_ERR_CUDA;
-  const int rc = build_jit(h, n_hint > 0 ? n_hint : 128, tun);  // adds a module, frees none
-  if (rc != ESCOIN_OK) return rc;
-  h->kernel = ESCOIN_KERNEL_JIT;
-  return ESCOIN_OK;
+  return build_jit(h, n_hint > 0 ? n_hint : 128, tun);  // adds a module (selected under jit_mu), frees none
 }
 
 int escoin_csr_jit_info(const escoin_csr* h, int* tunables6, int* mos, int* regs, int64_t* code_bytes) {
@@ -1335,7 +1397,7 @@ int escoin_csr_jit_info(const escoin_csr* h, int* tunables6, int* mos, int* regs
     tunables6[0] = p.Q; tunables6[1] = p.P; tunables6[2] = p.CC;
     tunables6[3] = p.NS; tunables6[4] = p.warps; tunables6[5] = p.minb;
   }
-  if (mos) *mos = p.mos;
+  if (mos) *mos = int(h->jit->units.size());
   if (regs) *regs = h->jit->regs;
   if (code_bytes) *code_bytes = int64_t(h->jit->cubin_bytes);
   return ESCOIN_OK;
@@ -1401,18 +1463,46 @@ int escoin_internal_plan(const escoin_csr* h, int id, int64_t* out) {
  * Two-call pattern: *len receives the size; the text is copied when cap >= size + 1. */
 int escoin_internal_jit_ptx(const escoin_csr* h, int n_hint, const int* tunables, int ntunables, char* buf,
                             int64_t cap, int64_t* len) {
-  if (!h || !len || ntunables < 0 || ntunables > 8 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
+  if (!h || !len || ntunables < 0 || ntunables > 9 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
   JitPlan p;
-  int tun[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int tun[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
   p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6];
-  p.mb = tun[7];
+  p.mb = tun[7]; p.units = tun[8];
   const double density = double(h->nnz) / (double(h->M) * h->C * h->K * h->K);
   if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint > 0 ? n_hint : 128, density) != 0)
     return ESCOIN_ERR_UNSUPPORTED;
   const std::string ptx = jit_ptx_text(p, h->rowptr.data(), h->colidx.data(), h->value.data());
   *len = int64_t(ptx.size());
   if (buf && cap >= int64_t(ptx.size()) + 1) std::memcpy(buf, ptx.c_str(), ptx.size() + 1);
+  return ESCOIN_OK;
+}
+
+/* Internal: the unit split escoin_csr_jit would use (ranges[2*u], ranges[2*u+1] = m-group range of unit u;
+ * *count = units) and the PTX of m-groups [g_lo, g_hi) (two-call pattern as above). */
+int escoin_internal_jit_units(const escoin_csr* h, int n_hint, const int* tunables, int ntunables, int* ranges,
+                              int cap, int* count, char* buf, int64_t bufcap, int64_t* len, int g_lo, int g_hi) {
+  if (!h || !count || ntunables < 0 || ntunables > 9 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
+  JitPlan p;
+  int tun[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
+  p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6];
+  p.mb = tun[7]; p.units = tun[8];
+  const double density = double(h->nnz) / (double(h->M) * h->C * h->K * h->K);
+  if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint > 0 ? n_hint : 128, density) != 0)
+    return ESCOIN_ERR_UNSUPPORTED;
+  const auto r = jit_units(p, h->rowptr.data());
+  *count = int(r.size());
+  for (int u = 0; u < int(r.size()) && 2 * u + 1 < cap && ranges; ++u) {
+    ranges[2 * u] = r[u].first;
+    ranges[2 * u + 1] = r[u].second;
+  }
+  if (len && g_hi > g_lo) {
+    if (g_lo < 0 || g_hi > p.nmg) return ESCOIN_ERR_SHAPE;
+    const std::string ptx = jit_ptx_text(p, h->rowptr.data(), h->colidx.data(), h->value.data(), g_lo, g_hi);
+    *len = int64_t(ptx.size());
+    if (buf && bufcap >= int64_t(ptx.size()) + 1) std::memcpy(buf, ptx.c_str(), ptx.size() + 1);
+  }
   return ESCOIN_OK;
 }
 

@@ -42,7 +42,13 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
 #include <mutex>
+#include <thread>
+#include <unistd.h>
 #include <string>
 #include <vector>
 
@@ -157,15 +163,18 @@ struct Nz {
   uint32_t bits;
 };
 
-std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value) {
+// PTX of one unit: the m-groups [g_lo, g_hi) (blockIdx.y = g - g_lo).
+std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value, int g_lo,
+                    int g_hi) {
   const int KK = p.K * p.K, Q = p.Q, P = p.P, NT = p.warps * 32;
+  const int ng = g_hi - g_lo;  // groups of this unit
   const int Hpd = p.H + 2 * p.pad, Wpd = p.W + 2 * p.pad;  // stretched geometry (R#3)
   const int hp = p.H + p.pad, wp = p.W + p.pad;
   const int HW = p.H * p.W, EF = p.E * p.F;
   // nonzeros per (m-group, channel), ascending tap then row
-  std::vector<std::vector<Nz>> lists(size_t(p.nmg) * p.C);
-  for (int m = 0; m < p.M; ++m) {
-    const int g = m / Q, q = m % Q;
+  std::vector<std::vector<Nz>> lists(size_t(ng) * p.C);
+  for (int m = g_lo * Q; m < std::min(p.M, g_hi * Q); ++m) {
+    const int g = m / Q - g_lo, q = m % Q;
     for (int j = rowptr[m]; j < rowptr[m + 1]; ++j) {
       const int col = colidx[j];
       const int c = col / (Hpd * Wpd), r = col % (Hpd * Wpd);
@@ -323,8 +332,8 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   for (int q = 0; q < Q * P; ++q) o("mov.f32 %%a%d, 0f00000000;", q);
   // Active chunk range per m-group (grouped layers: an m-group touches only its group's
   // channels; empty groups run no chunk at all and store bias only).
-  std::vector<int> klo(p.nmg, 0), khi(p.nmg, 0);
-  for (int g = 0; g < p.nmg; ++g) {
+  std::vector<int> klo(ng, 0), khi(ng, 0);
+  for (int g = 0; g < ng; ++g) {
     int lo = p.nch, hi = 0;
     for (int c = 0; c < p.C; ++c)
       if (!lists[size_t(g) * p.C + c].empty()) {
@@ -335,7 +344,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   }
   {
     std::string tbl;
-    for (int g = 0; g < p.nmg; ++g) tbl += (g ? ", " : "") + std::to_string(klo[g]) + ", " + std::to_string(khi[g]);
+    for (int g = 0; g < ng; ++g) tbl += (g ? ", " : "") + std::to_string(klo[g]) + ", " + std::to_string(khi[g]);
     // (declared at module scope below via a placeholder replaced after generation)
     mgr_table = tbl;
   }
@@ -373,7 +382,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("mov.u32 %%r16, %d;", D * p.CC * p.Ls * 4);  // buffer offset of chunk k + D
   // branch targets
   std::string tg = "ts: .branchtargets ";
-  for (int g = 0; g < p.nmg; ++g)
+  for (int g = 0; g < ng; ++g)
     for (int k = 0; k < p.nch; ++k) {
       char b[32];
       snprintf(b, sizeof b, "%sB%d_%d", (g || k) ? ", " : "", g, k);
@@ -462,7 +471,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("mad.lo.u32 %%r17, %%r4, %d, %%r15;", p.nch);
   o("%s", tg.c_str());
   o("brx.idx.uni %%r17, ts;");
-  for (int g = 0; g < p.nmg; ++g)
+  for (int g = 0; g < ng; ++g)
     for (int k = 0; k < p.nch; ++k) {
       o("B%d_%d:", g, k);
       if (k < klo[g] || k >= khi[g]) {  // never entered
@@ -503,7 +512,8 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   // epilogue
   o("setp.ne.u64 %%p6, %%rd2, 0;");
   o("setp.ne.u32 %%p7, %%r0, 0;");
-  o("mul.lo.u32 %%r18, %%r4, %d;", Q);           // m0
+  o("add.u32 %%r18, %%r4, %d;", g_lo);          // global m-group
+  o("mul.lo.u32 %%r18, %%r18, %d;", Q);          // m0
   o("mul.wide.u32 %%rd5, %%r18, 4;");
   o("add.s64 %%rd5, %%rd5, %%rd2;");             // bias + m0
   o("mul.wide.u32 %%rd6, %%r18, %d;", EF * 4);   // m0 * EF bytes
@@ -539,7 +549,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   }
   o("ret;");
   o("}");
-  o.s.insert(table_pos, ".global .align 8 .u32 mgr[" + std::to_string(2 * p.nmg) + "] = {" + mgr_table + "};\n");
+  o.s.insert(table_pos, ".global .align 8 .u32 mgr[" + std::to_string(2 * ng) + "] = {" + mgr_table + "};\n");
   return o.s;
 }
 
@@ -564,22 +574,26 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   p.mb = p.mb > 0 ? 1 : 0;
   n_hint = std::max(1, n_hint);
   if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0) {
-    // Shape choice by a small model: one CTA per SM (all warps of an SM stream the same
-    // code), Q in {32, 64} (registers: Q + K*K + ~24 <= 65536 / threads), warps in 16..32
-    // chosen for wave fill (grids are often only 1-3 waves at batch 128), FFMA share, and
-    // instruction-fetch sharing (more warps per fetched instruction; measured ~0.85x at 16
-    // warps vs 32 on AlexNet conv2-4).
+    // Shape choice by a small model (escoin_csr_autotune_ex measures the real choice among the
+    // compiled tunings).  Registers: Q accumulators + K*K taps + ~20 <= 65536 / (threads * CTAs/SM).
+    // Terms: wave fill of the tiles x m-groups grid over 148 SMs x CTAs/SM (grids are often only
+    // 1-3 waves at batch 128; 7x7 and 14x14 layers need small Q / several CTAs per SM to cover the
+    // SMs), FFMA share (one LDS per used tap feeds Q*density FFMAs), and instruction-fetch
+    // sharing (warps of one CTA run the same code; measured ~0.85x at 16 warps vs 32).
     double best = -1;
     JitPlan keep = p;
-    for (int Qc : {32, 64})
-      for (int wc : {32, 28, 24, 20, 16}) {
-        const int regs = std::min(255, 65536 / (wc * 32)) & ~7;
+    static const int shapes[][2] = {{32, 1}, {28, 1}, {24, 1}, {20, 1}, {16, 1}, {16, 2}, {12, 2}, {8, 2},
+                                    {10, 3}, {8, 3}, {8, 4}, {6, 4}, {4, 4}};
+    for (int Qc : {16, 32, 64})
+      for (const auto& sh : shapes) {
+        const int wc = sh[0], mb = sh[1];
+        const int regs = std::min(255, 65536 / (wc * 32 * mb)) & ~7;
         if (std::min(Qc, M) + K * K + 20 > regs && !(Qc == 32 && wc == 32 && K <= 5)) continue;
         JitPlan t = keep;
-        t.Q = std::min(Qc, M); t.warps = wc; t.minb = 1;
+        t.Q = std::min(Qc, M); t.warps = wc; t.minb = mb;
         if (!plan_fit(t, n_hint)) continue;
         const double pixels = double(n_hint) * E * F;
-        const double ctas = std::ceil(pixels / t.T) * t.nmg, per_wave = 148.0;
+        const double ctas = std::ceil(pixels / t.T) * t.nmg, per_wave = 148.0 * mb;
         const double wave_eff = ctas / (std::ceil(ctas / per_wave) * per_wave);
         const double fma = t.Q * K * K * density;
         const double taps = K * K * (1.0 - std::pow(1.0 - density, t.Q));
@@ -600,21 +614,112 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   return 0;
 }
 
-int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
-              std::string* log) {
-  const Driver& d = driver();
-  if (!d.ok) return -1;
-  // the driver-API module calls below need the device's primary context current in THIS host
-  // thread (callers may compile from worker threads); a runtime call binds it
-  if (cudaFree(nullptr) != cudaSuccess) return -3;
-  jm.plan = p;
-  const std::string ptx = gen_ptx(p, rowptr, colidx, value);
-  jm.ptx_bytes = ptx.size();
+namespace {
+
+// ---------------------------------------------------------------- compile pool
+// nvPTXCompiler runs single-threaded per call; the units of every jit_build in the process share
+// one bound on concurrent compiles (ESCOIN_JIT_THREADS, else the host's cores), so callers may
+// compile many layers at once without oversubscribing the host.
+class CompileSlots {
+ public:
+  CompileSlots() {
+    const char* e = std::getenv("ESCOIN_JIT_THREADS");
+    n_ = e ? std::atoi(e) : int(std::thread::hardware_concurrency());
+    if (n_ < 1) n_ = 1;
+  }
+  void acquire() {
+    std::unique_lock<std::mutex> lk(m_);
+    cv_.wait(lk, [&] { return n_ > 0; });
+    --n_;
+  }
+  void release() {
+    { std::lock_guard<std::mutex> lk(m_); ++n_; }
+    cv_.notify_one();
+  }
+
+ private:
+  std::mutex m_;
+  std::condition_variable cv_;
+  int n_;
+};
+
+CompileSlots& slots() {
+  static CompileSlots s;
+  return s;
+}
+
+const char* const kOpts[] = {"--gpu-name=sm_100a", "-O3"};
+
+// ---------------------------------------------------------------- cubin cache
+// ESCOIN_JIT_CACHE=<dir>: cubins keyed by two 64-bit FNV-1a hashes (different offset bases) of the
+// PTX text, the compile options and the compiler version.  Files are written to a temporary name
+// and renamed, so concurrent processes (the ranks of one node) never read a partial cubin.
+uint64_t fnv1a(const std::string& s, uint64_t h) {
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 0x100000001B3ULL;
+  }
+  return h;
+}
+
+std::string cache_key(const std::string& ptx) {
+  unsigned maj = 0, min = 0;
+  nvPTXCompilerGetVersion(&maj, &min);
+  std::string salt = "escoin-jit-v2|" + std::to_string(maj) + "." + std::to_string(min);
+  for (const char* o : kOpts) salt += std::string("|") + o;
+  char b[64];
+  snprintf(b, sizeof b, "%016llx%016llx", (unsigned long long)fnv1a(salt + ptx, 0xCBF29CE484222325ULL),
+           (unsigned long long)fnv1a(ptx + salt, 0x84222325CBF29CE4ULL));
+  return b;
+}
+
+std::string cache_dir() {
+  const char* e = std::getenv("ESCOIN_JIT_CACHE");
+  return e ? std::string(e) : std::string();
+}
+
+bool cache_get(const std::string& dir, const std::string& key, std::vector<char>* out) {
+  FILE* f = std::fopen((dir + "/" + key + ".cubin").c_str(), "rb");
+  if (!f) return false;
+  std::fseek(f, 0, SEEK_END);
+  const long n = std::ftell(f);
+  std::fseek(f, 0, SEEK_SET);
+  bool ok = n > 0;
+  if (ok) {
+    out->resize(size_t(n));
+    ok = std::fread(out->data(), 1, size_t(n), f) == size_t(n);
+  }
+  std::fclose(f);
+  return ok;
+}
+
+void cache_put(const std::string& dir, const std::string& key, const std::vector<char>& cubin) {
+  static std::atomic<unsigned> seq{0};
+  char tmpn[64];
+  snprintf(tmpn, sizeof tmpn, ".tmp.%d.%u", int(getpid()), seq.fetch_add(1));
+  const std::string fin = dir + "/" + key + ".cubin", tmp = fin + tmpn;
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) return;  // unwritable cache: compile-only behaviour
+  const bool ok = std::fwrite(cubin.data(), 1, cubin.size(), f) == cubin.size();
+  std::fclose(f);
+  if (!ok || std::rename(tmp.c_str(), fin.c_str()) != 0) std::remove(tmp.c_str());
+}
+
+// PTX -> cubin (cache first); 0 = OK, -2 = compile error (log filled).
+int compile_ptx(const std::string& ptx, std::vector<char>* cubin, std::string* log, bool* hit) {
+  const std::string dir = cache_dir();
+  const std::string key = dir.empty() ? std::string() : cache_key(ptx);
+  if (!dir.empty() && cache_get(dir, key, cubin)) {
+    *hit = true;
+    return 0;
+  }
+  *hit = false;
+  slots().acquire();
   nvPTXCompilerHandle c = nullptr;
-  if (nvPTXCompilerCreate(&c, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) return -1;
-  const char* opts[] = {"--gpu-name=sm_100a", "-O3"};
-  const nvPTXCompileResult r = nvPTXCompilerCompile(c, 2, opts);
-  if (r != NVPTXCOMPILE_SUCCESS) {
+  int rc = 0;
+  if (nvPTXCompilerCreate(&c, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) {
+    rc = -2;
+  } else if (nvPTXCompilerCompile(c, 2, kOpts) != NVPTXCOMPILE_SUCCESS) {
     if (log) {
       size_t n = 0;
       nvPTXCompilerGetErrorLogSize(c, &n);
@@ -622,47 +727,153 @@ int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int3
       if (n) nvPTXCompilerGetErrorLog(c, &e[0]);
       *log = e;
     }
-    nvPTXCompilerDestroy(&c);
-    return -2;
+    rc = -2;
+  } else {
+    size_t n = 0;
+    nvPTXCompilerGetCompiledProgramSize(c, &n);
+    cubin->resize(n);
+    nvPTXCompilerGetCompiledProgram(c, cubin->data());
   }
-  size_t n = 0;
-  nvPTXCompilerGetCompiledProgramSize(c, &n);
-  std::vector<char> cubin(n);
-  nvPTXCompilerGetCompiledProgram(c, cubin.data());
-  nvPTXCompilerDestroy(&c);
-  jm.cubin_bytes = n;
-  CUmodule mod = nullptr;
-  if (d.load(&mod, cubin.data()) != CUDA_SUCCESS) return -3;
-  CUfunction f = nullptr;
-  if (d.get(&f, mod, "escoin_jit_sconv") != CUDA_SUCCESS) { d.unload(mod); return -3; }
-  if (d.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, p.smem_bytes) != CUDA_SUCCESS) {
-    d.unload(mod);
-    return -3;
+  if (c) nvPTXCompilerDestroy(&c);
+  slots().release();
+  if (rc == 0 && !dir.empty()) cache_put(dir, key, *cubin);
+  return rc;
+}
+
+}  // namespace
+
+std::vector<std::pair<int, int>> jit_units(const JitPlan& p, const int32_t* rowptr) {
+  // nonzeros per m-group; units are contiguous group ranges of about equal nonzeros, about
+  // kUnitNnz each (ptxas time grows with the code: ~0.25 ms per FFMA on one host core), so
+  // the largest layers compile in parallel; never more units than groups or than 32.
+  constexpr int64_t kUnitNnz = 24000;
+  std::vector<int64_t> gn(p.nmg, 0);
+  int64_t tot = 0;
+  for (int g = 0; g < p.nmg; ++g) {
+    gn[g] = int64_t(rowptr[std::min(p.M, (g + 1) * p.Q)]) - rowptr[g * p.Q];
+    tot += gn[g];
   }
-  d.getattr(&jm.regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f);
-  jm.module = mod;
-  jm.func = f;
+  int U = p.units > 0 ? p.units : int((tot + kUnitNnz - 1) / kUnitNnz);
+  U = std::max(1, std::min(U, std::min(p.nmg, 32)));
+  std::vector<std::pair<int, int>> r;
+  int g = 0;
+  int64_t acc = 0;
+  for (int u = 0; u < U; ++u) {
+    const int lo = g;
+    const int64_t target = (tot * (u + 1) + U - 1) / U;  // cumulative share of units 0..u
+    while (g < p.nmg && (g == lo || acc + gn[g] <= target) && p.nmg - g > U - 1 - u) acc += gn[g++];
+    if (u == U - 1) while (g < p.nmg) acc += gn[g++];
+    r.emplace_back(lo, g);
+  }
+  return r;
+}
+
+int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
+              std::string* log) {
+  const Driver& d = driver();
+  if (!d.ok) return -1;
+  // the driver-API module calls below need the device's primary context current in THIS host
+  // thread (callers may compile from worker threads); a runtime call binds it
+  int dev = 0;
+  if (cudaFree(nullptr) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess) return -3;
+  const auto t0 = std::chrono::steady_clock::now();
+  jm.plan = p;
+  const auto ranges = jit_units(p, rowptr);
+  const int U = int(ranges.size());
+  jm.units.assign(U, JitUnit());
+  std::vector<std::vector<char>> cubins(U);
+  std::vector<int> rcs(U, 0);
+  std::vector<std::string> logs(U);
+  auto work = [&](int u) {
+    JitUnit& ju = jm.units[u];
+    ju.g_lo = ranges[u].first;
+    ju.g_hi = ranges[u].second;
+    ju.nnz = int64_t(rowptr[std::min(p.M, ju.g_hi * p.Q)]) - rowptr[ju.g_lo * p.Q];
+    const std::string ptx = gen_ptx(p, rowptr, colidx, value, ju.g_lo, ju.g_hi);
+    ju.ptx_bytes = ptx.size();
+    rcs[u] = compile_ptx(ptx, &cubins[u], &logs[u], &ju.cache_hit);
+    ju.cubin_bytes = cubins[u].size();
+  };
+  if (U == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int u = 0; u < U; ++u) th.emplace_back(work, u);
+    for (auto& t : th) t.join();
+  }
+  for (int u = 0; u < U; ++u)
+    if (rcs[u] != 0) {
+      if (log) *log = logs[u];
+      jm.units.clear();
+      return -2;
+    }
+  int rc = 0;
+  jm.regs = 0;
+  jm.ptx_bytes = jm.cubin_bytes = 0;
+  jm.cache_hits = 0;
+  for (int u = 0; u < U && rc == 0; ++u) {
+    JitUnit& ju = jm.units[u];
+    CUmodule mod = nullptr;
+    CUfunction f = nullptr;
+    if (d.load(&mod, cubins[u].data()) != CUDA_SUCCESS) { rc = -3; break; }
+    ju.module = mod;
+    if (d.get(&f, mod, "escoin_jit_sconv") != CUDA_SUCCESS ||
+        d.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, p.smem_bytes) != CUDA_SUCCESS) {
+      rc = -3;
+      break;
+    }
+    ju.func = f;
+    d.getattr(&ju.regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f);
+    jm.regs = std::max(jm.regs, ju.regs);
+    jm.ptx_bytes += ju.ptx_bytes;
+    jm.cubin_bytes += ju.cubin_bytes;
+    jm.cache_hits += ju.cache_hit ? 1 : 0;
+  }
+  for (int u = 1; u < U && rc == 0; ++u) {
+    cudaStream_t st = nullptr;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) { rc = -3; break; }
+    jm.aux.push_back(st);
+  }
+  if (rc != 0) {
+    jit_free(jm);
+    return rc;
+  }
+  (void)dev;
+  jm.compile_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return 0;
 }
 
 int jit_compile_only(const char* ptx, size_t* cubin_bytes) {
-  nvPTXCompilerHandle c = nullptr;
-  if (nvPTXCompilerCreate(&c, std::strlen(ptx), ptx) != NVPTXCOMPILE_SUCCESS) return -1;
-  const char* opts[] = {"--gpu-name=sm_100a", "-O3"};
-  const bool ok = nvPTXCompilerCompile(c, 2, opts) == NVPTXCOMPILE_SUCCESS &&
-                  nvPTXCompilerGetCompiledProgramSize(c, cubin_bytes) == NVPTXCOMPILE_SUCCESS;
-  nvPTXCompilerDestroy(&c);
-  return ok ? 0 : -2;
+  std::vector<char> cubin;
+  bool hit = false;
+  if (compile_ptx(std::string(ptx), &cubin, nullptr, &hit) != 0) return -2;
+  *cubin_bytes = cubin.size();
+  return 0;
 }
 
-std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value) {
-  return gen_ptx(p, rowptr, colidx, value);
+std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
+                         int g_lo, int g_hi) {
+  if (g_hi <= 0) g_hi = p.nmg;
+  return gen_ptx(p, rowptr, colidx, value, g_lo, g_hi);
+}
+
+std::string jit_label(const JitModule& jm) {
+  const JitPlan& p = jm.plan;
+  char b[160];
+  snprintf(b, sizeof b, "jit_q%d_p%d_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d", p.Q, p.P, p.CC, p.NS, p.warps, p.minb,
+           p.pf, p.mb, int(jm.units.size()), p.SWs);
+  return b;
 }
 
 void jit_free(JitModule& jm) {
-  if (jm.module && driver().ok) driver().unload(static_cast<CUmodule>(jm.module));
-  jm.module = nullptr;
-  jm.func = nullptr;
+  for (cudaStream_t st : jm.aux) cudaStreamDestroy(st);
+  jm.aux.clear();
+  for (JitUnit& ju : jm.units) {
+    if (ju.module && driver().ok) driver().unload(static_cast<CUmodule>(ju.module));
+    ju.module = nullptr;
+    ju.func = nullptr;
+  }
+  jm.units.clear();
 }
 
 int jit_launch(const JitModule& jm, const float* in, float* out, const float* bias, int relu, int N,
@@ -671,16 +882,46 @@ int jit_launch(const JitModule& jm, const float* in, float* out, const float* bi
   const int64_t pixels = int64_t(N) * p.E * p.F;
   const int64_t tiles = (pixels + p.T - 1) / p.T;
   const int64_t last_pos = (int64_t(N) * (p.H + p.pad) + p.pad) * p.SWs + p.L;  // staged positions stay int32
-  if (pixels > 0x7fffffff || last_pos > 0x7fffffff) return -1;
+  if (pixels > 0x7fffffff || last_pos > 0x7fffffff || jm.units.empty()) return -1;
   unsigned relu_u = relu ? 1u : 0u, n_u = unsigned(N);
   const void* a_in = in;
   void* a_out = out;
   const void* a_bias = bias;
   void* args[] = {&a_in, &a_out, &a_bias, &relu_u, &n_u};
-  const CUresult r = driver().launch(static_cast<CUfunction>(jm.func), unsigned(tiles), unsigned(p.nmg), 1,
-                                     unsigned(p.warps * 32), 1, 1, unsigned(p.smem_bytes), (CUstream)s, args,
-                                     nullptr);
-  return r == CUDA_SUCCESS ? 0 : -1;
+  auto launch = [&](const JitUnit& ju, cudaStream_t st) {
+    return driver().launch(static_cast<CUfunction>(ju.func), unsigned(tiles), unsigned(ju.g_hi - ju.g_lo), 1,
+                           unsigned(p.warps * 32), 1, 1, unsigned(p.smem_bytes), (CUstream)st, args, nullptr) ==
+                   CUDA_SUCCESS
+               ? 0
+               : -1;
+  };
+  const int U = int(jm.units.size());
+  if (U == 1) return launch(jm.units[0], s);
+  // Units run concurrently: fork from s onto the aux streams, join back into s.  Events are
+  // per call (no state shared between concurrent forwards), released once they complete; the
+  // pattern is legal under stream capture (it becomes parallel graph branches).
+  cudaEvent_t fork = nullptr;
+  if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return -1;
+  int rc = cudaEventRecord(fork, s) == cudaSuccess ? 0 : -1;
+  std::vector<cudaEvent_t> joins;
+  for (int u = 1; u < U && rc == 0; ++u) {
+    cudaStream_t st = jm.aux[u - 1];
+    cudaEvent_t join = nullptr;
+    if (cudaStreamWaitEvent(st, fork, 0) != cudaSuccess || launch(jm.units[u], st) != 0 ||
+        cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess) {
+      rc = -1;
+      break;
+    }
+    joins.push_back(join);
+    if (cudaEventRecord(join, st) != cudaSuccess) rc = -1;
+  }
+  if (rc == 0) rc = launch(jm.units[0], s);  // unit 0 on s itself, before s waits for the others
+  for (cudaEvent_t join : joins) {
+    if (cudaStreamWaitEvent(s, join, 0) != cudaSuccess) rc = -1;
+    cudaEventDestroy(join);
+  }
+  cudaEventDestroy(fork);
+  return rc;
 }
 
 }  // namespace escoin

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 namespace escoin {
 
@@ -17,6 +18,7 @@ struct JitPlan {
   int minb = 0;   // CTAs per SM the register budget is compiled for
   int pf = 0;     // instruction prefetch pass: 0 = default (on), < 0 = off
   int mb = 0;     // > 0: mbarrier pipeline (warps drift up to NS-2 chunks) instead of a CTA barrier per chunk
+  int units = 0;  // separately compiled modules the m-groups are split into (<= 0: by nnz, jit_build)
   // layer
   int C = 0, H = 0, W = 0, M = 0, K = 0, pad = 0, E = 0, F = 0, S = 1;
   // derived
@@ -29,20 +31,41 @@ struct JitPlan {
   int smem_bytes = 0;
 };
 
-struct JitModule {
-  JitPlan plan;
+// One separately compiled module: the code of m-groups [g_lo, g_hi) (blockIdx.y = g - g_lo).
+struct JitUnit {
+  int g_lo = 0, g_hi = 0;
+  int64_t nnz = 0;
   void* module = nullptr;  // CUmodule
   void* func = nullptr;    // CUfunction
   int regs = 0;
   size_t ptx_bytes = 0, cubin_bytes = 0;
+  bool cache_hit = false;
+};
+
+struct JitModule {
+  JitPlan plan;
+  std::vector<JitUnit> units;      // launched concurrently (fork/join over aux streams) by jit_launch
+  std::vector<cudaStream_t> aux;   // units.size() - 1 non-blocking streams on the handle's device
+  int regs = 0;                    // max over units
+  size_t ptx_bytes = 0, cubin_bytes = 0;
+  double compile_s = 0.0;          // wall time of jit_build (all units, parallel)
+  int cache_hits = 0;              // units loaded from ESCOIN_JIT_CACHE instead of compiled
 };
 
 // 0 = supported (plan filled), < 0 = this layer has no JIT form (stride != 1, 2*pad != K-1, smem).
 int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad, int n_hint, double density);
-// Generate, compile and load; 0 = OK. log receives the compiler error log on failure.
+// Generate, compile (units in parallel host threads, bounded by ESCOIN_JIT_THREADS or the
+// host's cores; cubins reused from / stored in the directory ESCOIN_JIT_CACHE when set) and
+// load; 0 = OK. log receives the compiler error log on failure.
 int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
               std::string* log);
-std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value);
+// The m-group ranges of the units jit_build would compile (balanced by nonzeros).
+std::vector<std::pair<int, int>> jit_units(const JitPlan& p, const int32_t* rowptr);
+// PTX of one unit (m-groups [g_lo, g_hi); g_hi <= 0: all groups).
+std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
+                         int g_lo = 0, int g_hi = 0);
+// Human-readable label of the plan, every tunable included (e.g. "jit_q32_p1_cc8_ns3_w32_b1_pf1_mb0_u4_sw15").
+std::string jit_label(const JitModule& jm);
 void jit_free(JitModule& jm);
 // Compile PTX for sm_100a in-process without loading it (host only); 0 = OK.
 int jit_compile_only(const char* ptx, size_t* cubin_bytes);

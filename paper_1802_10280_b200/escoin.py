@@ -32,8 +32,10 @@ EXPORTS = [
     "escoin_csr_wrap_device", "escoin_csr_free", "escoin_sconv_forward", "escoin_sconv_forward_hostio",
     "escoin_kernel_count", "escoin_kernel_info", "escoin_csr_set_kernel", "escoin_csr_get_kernel",
     "escoin_status_string", "escoin_version", "escoin_csr_autotune", "escoin_csr_stretch_device",
-    "escoin_bench_dense_tc_forward", "escoin_csr_jit", "escoin_csr_jit_info",
+    "escoin_bench_dense_tc_forward", "escoin_csr_jit", "escoin_csr_jit_info", "escoin_csr_autotune_ex",
+    "escoin_csr_kernel_label", "escoin_csr_jit_stats",
 ]
+TUNE_VARIANTS, TUNE_JIT = 1, 2
 
 
 class EscoinError(RuntimeError):
@@ -78,6 +80,10 @@ def lib():
             L.escoin_bench_dense_tc_forward.argtypes = [ci] * 8 + [vp, vp, vp, vp, ci, ci, vp]
             L.escoin_csr_jit.argtypes = [vp, ci, ip, ci]
             L.escoin_csr_jit_info.argtypes = [vp, ip, ip, ip, ctypes.POINTER(cl)]
+            L.escoin_csr_autotune_ex.argtypes = [vp, ci, vp, vp, vp, ci, ci, vp, vp, cl, ci, ip,
+                                                 ctypes.POINTER(ctypes.c_float)]
+            L.escoin_csr_kernel_label.argtypes = [vp, ctypes.c_char_p, ci]
+            L.escoin_csr_jit_stats.argtypes = [vp, ip, ip, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(cl)]
             L.escoin_status_string.argtypes = [ci]
             L.escoin_status_string.restype = ctypes.c_char_p
             L.escoin_version.restype = ctypes.c_char_p
@@ -194,21 +200,45 @@ class Csr:
                                                                 ctypes.byref(bms)))
         return bid.value, bms.value
 
-    def jit(self, n_hint=128, Q=0, P=0, CC=0, NS=0, warps=0, minb=0, prefetch=0, mbarrier=0) -> "Csr":
+    def autotune_ex(self, N, inp, out, bias=None, relu=False, reps=3, stream=0, flush=None,
+                    flags=TUNE_VARIANTS | TUNE_JIT):
+        """escoin_csr_autotune_ex: as autotune, timing each rep alone after an L2 flush (memset of `flush`,
+        a device tensor or None), median of reps; flags choose the candidate sets."""
+        bid, bms = ctypes.c_int(), ctypes.c_float()
+        nbytes = 0 if flush is None else flush.numel() * flush.element_size()
+        _check("escoin_csr_autotune_ex", lib().escoin_csr_autotune_ex(
+            self._h, N, _ptr(inp), _ptr(out), _ptr(bias), 1 if relu else 0, reps, stream, _ptr(flush), nbytes, flags,
+            ctypes.byref(bid), ctypes.byref(bms)))
+        return bid.value, bms.value
+
+    def label(self) -> str:
+        """escoin_csr_kernel_label: the current kernel with every tunable."""
+        buf = ctypes.create_string_buffer(256)
+        _check("escoin_csr_kernel_label", lib().escoin_csr_kernel_label(self._h, buf, 256))
+        return buf.value.decode()
+
+    def jit(self, n_hint=128, Q=0, P=0, CC=0, NS=0, warps=0, minb=0, prefetch=0, mbarrier=0, units=0) -> "Csr":
         """escoin_csr_jit: compile this layer's pattern-specialised kernel and select it."""
-        tun = (ctypes.c_int * 8)(Q, P, CC, NS, warps, minb, prefetch, mbarrier)
-        _check("escoin_csr_jit", lib().escoin_csr_jit(self._h, n_hint, tun, 8))
+        tun = (ctypes.c_int * 9)(Q, P, CC, NS, warps, minb, prefetch, mbarrier, units)
+        _check("escoin_csr_jit", lib().escoin_csr_jit(self._h, n_hint, tun, 9))
         return self
 
     def jit_info(self):
-        """dict(Q, P, CC, NS, warps, minb, mos, regs, code_bytes) of the specialised kernel."""
+        """dict(Q, P, CC, NS, warps, minb, units, regs, code_bytes) of the specialised kernel."""
         tun = (ctypes.c_int * 6)()
-        mos, regs, code = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
-        _check("escoin_csr_jit_info", lib().escoin_csr_jit_info(self._h, tun, ctypes.byref(mos), ctypes.byref(regs),
-                                                                ctypes.byref(code)))
+        units, regs, code = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+        _check("escoin_csr_jit_info", lib().escoin_csr_jit_info(self._h, tun, ctypes.byref(units),
+                                                                ctypes.byref(regs), ctypes.byref(code)))
         d = dict(zip(["Q", "P", "CC", "NS", "warps", "minb"], list(tun)))
-        d.update(mos=mos.value, regs=regs.value, code_bytes=code.value)
+        d.update(units=units.value, regs=regs.value, code_bytes=code.value)
         return d
+
+    def jit_stats(self):
+        """dict(units, cache_hits, compile_s, ptx_bytes) of the selected specialised kernel's build."""
+        u, hits, sec, ptx = ctypes.c_int(), ctypes.c_int(), ctypes.c_double(), ctypes.c_int64()
+        _check("escoin_csr_jit_stats", lib().escoin_csr_jit_stats(self._h, ctypes.byref(u), ctypes.byref(hits),
+                                                                  ctypes.byref(sec), ctypes.byref(ptx)))
+        return dict(units=u.value, cache_hits=hits.value, compile_s=sec.value, ptx_bytes=ptx.value)
 
     def free(self):
         if self._h.value:

@@ -52,12 +52,12 @@ def fma_stream(ptx):
     return out
 
 
-def check_rows(csr, ptx, Q, P):
+def check_rows(csr, ptx, Q, P, stream=None):
     info = csr.info()
     M, K, H, W, pad = info["M"], info["K"], info["H"], info["W"], info["pad"]
     Hp, Wp = H + 2 * pad, W + 2 * pad
     rowptr, colidx, value = csr.host_arrays()
-    stream = fma_stream(ptx)
+    stream = fma_stream(ptx) if stream is None else stream
     assert len(stream) == info["nnz"] * P  # one FFMA per nonzero and pixel, nothing else
     per_acc = {}
     for g, a, x, bits in stream:
@@ -139,3 +139,68 @@ def test_unsupported_shapes_have_no_specialised_form():
     n = ctypes.c_int64()
     arr = (ctypes.c_int * 8)()
     assert _lib().escoin_internal_jit_ptx(csr.handle, 4, arr, 8, None, 0, ctypes.byref(n)) == escoin.ERR_UNSUPPORTED
+
+
+def unit_split(csr, n_hint=16, **tun):
+    keys = ["Q", "P", "CC", "NS", "warps", "minb", "prefetch", "mbarrier", "units"]
+    arr = (ctypes.c_int * 9)(*[tun.get(k, 0) for k in keys])
+    L = _lib()
+    L.escoin_internal_jit_units.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                            ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                            ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                                            ctypes.c_int, ctypes.c_int]
+    rng = (ctypes.c_int * 64)()
+    cnt = ctypes.c_int()
+    assert L.escoin_internal_jit_units(csr.handle, n_hint, arr, 9, rng, 64, ctypes.byref(cnt), None, 0, None,
+                                       0, 0) == 0
+    ranges = [(rng[2 * u], rng[2 * u + 1]) for u in range(cnt.value)]
+    ptxs = []
+    for lo, hi in ranges:
+        n = ctypes.c_int64()
+        assert L.escoin_internal_jit_units(csr.handle, n_hint, arr, 9, None, 0, ctypes.byref(cnt), None, 0,
+                                           ctypes.byref(n), lo, hi) == 0
+        buf = ctypes.create_string_buffer(n.value + 1)
+        assert L.escoin_internal_jit_units(csr.handle, n_hint, arr, 9, None, 0, ctypes.byref(cnt), buf,
+                                           n.value + 1, ctypes.byref(n), lo, hi) == 0
+        ptxs.append(buf.value.decode())
+    return ranges, ptxs
+
+
+@pytest.mark.parametrize("units", [1, 2, 3, 5])
+def test_units_partition_groups_and_union_is_the_csr(units):
+    # escoin_csr_jit splits the m-groups into separately compiled units (compiled in parallel,
+    # launched concurrently): the ranges must tile [0, groups) and the union of the units'
+    # FFMA streams (local group + the unit's first group) must still be exactly the CSR
+    rng = np.random.default_rng(77 + units)
+    M, C, H, K = 70, 9, 11, 3
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.3] = 0.0
+    w[8:16] = 0.0  # an empty group
+    csr = escoin.Csr.stretch(w, H, H, 1, 1)
+    ranges, ptxs = unit_split(csr, Q=8, units=units)
+    ngroups = -(-M // 8)
+    assert ranges[0][0] == 0 and ranges[-1][1] == ngroups and len(ranges) == min(units, ngroups)
+    assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:])) and all(lo < hi for lo, hi in ranges)
+    stream = []
+    for (lo, hi), ptx in zip(ranges, ptxs):
+        assert ".global .align 8 .u32 mgr[%d]" % (2 * (hi - lo)) in ptx
+        stream += [(g + lo, a, x, b) for g, a, x, b in fma_stream(ptx)]
+    check_rows(csr, None, 8, 1, stream=stream)
+
+
+def test_default_unit_split_balances_nonzeros():
+    # about one unit per 24k nonzeros, contiguous ranges of about equal work (ResNet res5: 472k)
+    L = [l for l in workloads.workload("resnet50").layers if l.name == "res5a_branch2b"][0]
+    w = inputs.layer_weights("resnet50", L, 800)
+    csr = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad)
+    keys = (ctypes.c_int * 9)(32, 1, 0, 0, 32, 1, 0, 0, 0)
+    L_ = _lib()
+    rng = (ctypes.c_int * 64)()
+    cnt = ctypes.c_int()
+    unit_split(csr, n_hint=128, Q=32, warps=32, minb=1)  # sets argtypes
+    assert L_.escoin_internal_jit_units(csr.handle, 128, keys, 9, rng, 64, ctypes.byref(cnt), None, 0, None,
+                                        0, 0) == 0
+    rowptr = csr.host_arrays()[0]
+    nnz = [int(rowptr[min(L.M, rng[2 * u + 1] * 32)] - rowptr[rng[2 * u] * 32]) for u in range(cnt.value)]
+    assert cnt.value == 16  # 16 groups of 32 rows, 472k nonzeros: one group per unit
+    assert max(nnz) < 1.2 * (sum(nnz) / len(nnz))

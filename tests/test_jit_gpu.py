@@ -212,3 +212,94 @@ def test_grouped_block_diagonal_and_empty_groups(tun):
     out, paper, _ = jit_and_paper(w, x, b, 1, True, **tun)
     check(out, ref, scale, b)
     assert out.tobytes() == paper.tobytes()
+
+
+# ------------------------------------------------------------------ units, graphs, cache, flushed autotune
+def _layer_case(seed, N=6, C=24, H=13, M=96, K=3, pad=1, d=0.25):
+    rng = np.random.default_rng(seed)
+    x = rng.random((N, C, H, H)).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= d] = 0.0
+    w[20:24] = 0.0
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    return x, w, b
+
+
+@pytest.mark.parametrize("units", [1, 2, 3, 6])
+def test_units_parity_bitwise(units):
+    # the m-groups split into separately compiled units launched concurrently on forked streams:
+    # same bits as the paper-mapping kernel, within tolerance of the oracle
+    x, w, b = _layer_case(100 + units)
+    ref, scale = oracle_ref(w, x, b, 1, 1, True)
+    out, paper, csr = jit_and_paper(w, x, b, 1, True, Q=16, units=units)
+    assert csr.jit_info()["units"] == units
+    check(out, ref, scale, b)
+    assert out.tobytes() == paper.tobytes()
+
+
+def test_multi_unit_forward_captures_into_a_graph():
+    x, w, b = _layer_case(7, N=9)
+    csr = escoin.Csr.stretch(w, 13, 13, 1, 1).to_device(0)
+    csr.jit(n_hint=9, Q=16, units=4)
+    dx = torch.from_numpy(x).cuda()
+    db = torch.from_numpy(b).cuda()
+    eager = escoin.forward(csr, dx, bias=db, relu=True)
+    out = torch.zeros_like(eager)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        escoin.forward(csr, dx, bias=db, relu=True, out=out)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
+    out.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
+
+
+def test_cubin_cache_roundtrip(tmp_path, monkeypatch):
+    x, w, b = _layer_case(9)
+    monkeypatch.setenv("ESCOIN_JIT_CACHE", str(tmp_path))
+    c1 = escoin.Csr.stretch(w, 13, 13, 1, 1).to_device(0)
+    c1.jit(n_hint=6, Q=16, units=3)
+    st1 = c1.jit_stats()
+    assert st1["units"] == 3 and st1["cache_hits"] == 0
+    assert len(list(tmp_path.glob("*.cubin"))) == 3
+    c2 = escoin.Csr.stretch(w, 13, 13, 1, 1).to_device(0)
+    c2.jit(n_hint=6, Q=16, units=3)
+    assert c2.jit_stats()["cache_hits"] == 3
+    assert fwd(c1, x, b, True).tobytes() == fwd(c2, x, b, True).tobytes()
+    w2 = w.copy()
+    w2[0, 0, 0, 0] = 0.5  # one weight differs: a different kernel, no stale hit
+    c3 = escoin.Csr.stretch(w2, 13, 13, 1, 1).to_device(0)
+    c3.jit(n_hint=6, Q=16, units=3)
+    assert c3.jit_stats()["cache_hits"] < 3
+    ref, scale = oracle_ref(w2, x, b, 1, 1, True)
+    check(fwd(c3, x, b, True), ref, scale, b)
+
+
+def test_autotune_ex_flushed_jit_only_and_label():
+    x, w, b = _layer_case(13, N=8)
+    csr = escoin.Csr.stretch(w, 13, 13, 1, 1).to_device(0)
+    ref = fwd(csr, x, b, True)
+    csr.jit(n_hint=8, Q=16, units=2)
+    csr.jit(n_hint=8, Q=32, warps=8, minb=2)
+    dx = torch.from_numpy(x).cuda()
+    db = torch.from_numpy(b).cuda()
+    out = torch.empty((8, 96, 13, 13), device="cuda")
+    flush = torch.empty(64 * 1024 * 1024 // 4, device="cuda")
+    kid, ms = csr.autotune_ex(8, dx, out, db, True, 3, torch.cuda.current_stream().cuda_stream, flush=flush,
+                              flags=escoin.TUNE_JIT)
+    assert kid == escoin.KERNEL_JIT and ms > 0
+    lab = csr.label()
+    assert lab.startswith("jit_q") and "_u" in lab and "_ns" in lab and "_mb" in lab
+    assert fwd(csr, x, b, True).tobytes() == ref.tobytes()
+    kid, _ = csr.autotune_ex(8, dx, out, db, True, 2, torch.cuda.current_stream().cuda_stream,
+                             flags=escoin.TUNE_VARIANTS)
+    assert kid != escoin.KERNEL_JIT
+    assert not csr.label().startswith("jit_")
+    assert fwd(csr, x, b, True).tobytes() == ref.tobytes()

@@ -74,3 +74,20 @@ def test_shard_range_partition(n, w):
         assert b == c
     sizes = [b - a for a, b in rs]
     assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_bench_strong_scaling_ranges(world):
+    # bench.py's default: the GLOBAL batch 128 is split across ranks (strong scaling), every image once
+    import argparse
+    import bench
+    wl = workloads.workload("resnet50")
+    args = argparse.Namespace(batch=None, weak=False)
+    seen = []
+    for r in range(world):
+        n0, B, GB = bench.batch_range(args, wl, r, world)
+        assert GB == 128 and B == 128 // world
+        seen += list(range(n0, n0 + B))
+    assert seen == list(range(128))
+    args.weak = True
+    assert bench.batch_range(args, wl, 1, world) == (128, 128, 128 * world)
