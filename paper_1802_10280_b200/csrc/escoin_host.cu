@@ -1506,6 +1506,33 @@ int escoin_internal_jit_units(const escoin_csr* h, int n_hint, const int* tunabl
   return ESCOIN_OK;
 }
 
+/* Internal: host-only build of the cubin escoin_csr_jit would load (generate, compile the units,
+ * link) — *units, *cubin_bytes; the compiler/linker log on failure into buf (cap bytes). */
+int escoin_internal_jit_cubin(const escoin_csr* h, int n_hint, const int* tunables, int ntunables, int* units,
+                              int64_t* cubin_bytes, char* buf, int64_t cap) {
+  if (!h || !units || !cubin_bytes || ntunables < 0 || ntunables > 9 || (ntunables > 0 && !tunables))
+    return ESCOIN_ERR_NULL;
+  JitPlan p;
+  int tun[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
+  p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6];
+  p.mb = tun[7]; p.units = tun[8];
+  const double density = double(h->nnz) / (double(h->M) * h->C * h->K * h->K);
+  if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint > 0 ? n_hint : 128, density) != 0)
+    return ESCOIN_ERR_UNSUPPORTED;
+  JitModule jm;
+  std::vector<char> cubin;
+  std::string log;
+  const int rc = jit_cubin(jm, p, h->rowptr.data(), h->colidx.data(), h->value.data(), &cubin, &log);
+  if (rc != 0) {
+    if (buf && cap > 0) std::snprintf(buf, size_t(cap), "%s", log.c_str());
+    return ESCOIN_ERR_UNSUPPORTED;
+  }
+  *units = int(jm.units.size());
+  *cubin_bytes = int64_t(cubin.size());
+  return ESCOIN_OK;
+}
+
 int escoin_internal_ptx_compile(const char* ptx, int64_t* cubin_bytes) {
   if (!ptx || !cubin_bytes) return ESCOIN_ERR_NULL;
   size_t n = 0;

@@ -35,6 +35,7 @@
 // has no link-time dependency on libcuda).
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvJitLink.h>
 #include <nvPTXCompiler.h>
 
 #include <algorithm>
@@ -163,9 +164,11 @@ struct Nz {
   uint32_t bits;
 };
 
-// PTX of one unit: the m-groups [g_lo, g_hi) (blockIdx.y = g - g_lo).
+// PTX of the m-groups [g_lo, g_hi).  unit < 0: a complete kernel `escoin_jit_sconv` (blockIdx.y =
+// g - g_lo).  unit >= 0: the device function `escoin_unit_<unit>` of a linked multi-unit kernel
+// (gen_entry below calls it with the local group index), compiled relocatable on its own.
 std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value, int g_lo,
-                    int g_hi) {
+                    int g_hi, int unit) {
   const int KK = p.K * p.K, Q = p.Q, P = p.P, NT = p.warps * 32;
   const int ng = g_hi - g_lo;  // groups of this unit
   const int Hpd = p.H + 2 * p.pad, Wpd = p.W + 2 * p.pad;  // stretched geometry (R#3)
@@ -194,10 +197,16 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o(".extern .shared .align 16 .b8 smem[];");
   const size_t table_pos = o.s.size();
   std::string mgr_table;
-  o(".visible .entry escoin_jit_sconv(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
-    ".param .u32 p_relu, .param .u32 p_N)");
-  o(".maxntid %d, 1, 1", NT);
-  o(".minnctapersm %d", p.minb);
+  const std::string mgr = unit < 0 ? std::string("mgr") : "mgr" + std::to_string(unit);
+  if (unit < 0) {
+    o(".visible .entry escoin_jit_sconv(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
+      ".param .u32 p_relu, .param .u32 p_N)");
+    o(".maxntid %d, 1, 1", NT);
+    o(".minnctapersm %d", p.minb);
+  } else {
+    o(".visible .func escoin_unit_%d(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
+      ".param .u32 p_relu, .param .u32 p_N, .param .u32 p_gy)", unit);
+  }
   o("{");
   o(".reg .pred %%p<%d>;", 16 + 2 * p.KS + P);
   o(".reg .b32 %%r<%d>;", 64 + 4 * p.KS + 8 * P);
@@ -215,7 +224,10 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("ld.param.u32 %%r1, [p_N];");
   o("mov.u32 %%r2, %%tid.x;");
   o("mov.u32 %%r3, %%ctaid.x;");
-  o("mov.u32 %%r4, %%ctaid.y;");
+  if (unit < 0)
+    o("mov.u32 %%r4, %%ctaid.y;");
+  else
+    o("ld.param.u32 %%r4, [p_gy];");     // local m-group (the entry subtracted g_lo)
   o("mul.lo.u32 %%r28, %%r3, %d;", p.T);  // g0: first output pixel of the tile
   o("mul.lo.u32 %%r29, %%r1, %d;", EF);
   o("sub.u32 %%r29, %%r29, 1;");           // last pixel N*E*F - 1
@@ -348,7 +360,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     // (declared at module scope below via a placeholder replaced after generation)
     mgr_table = tbl;
   }
-  o("mov.u64 %%rd8, mgr;");
+  o("mov.u64 %%rd8, %s;", mgr.c_str());
   o("mul.wide.u32 %%rd9, %%r4, 8;");
   o("add.s64 %%rd8, %%rd8, %%rd9;");
   o("ld.global.nc.u32 %%r20, [%%rd8];");    // k_lo
@@ -549,7 +561,60 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   }
   o("ret;");
   o("}");
-  o.s.insert(table_pos, ".global .align 8 .u32 mgr[" + std::to_string(2 * ng) + "] = {" + mgr_table + "};\n");
+  o.s.insert(table_pos, ".global .align 8 .u32 " + mgr + "[" + std::to_string(2 * ng) + "] = {" + mgr_table + "};\n");
+  return o.s;
+}
+
+// Entry of a linked multi-unit kernel: picks the unit of blockIdx.y and calls its function with the
+// local group index (one call per CTA); the units are compiled separately and linked (nvJitLink).
+std::string gen_entry(const JitPlan& p, const std::vector<std::pair<int, int>>& ranges) {
+  Out o;
+  o(".version 8.7");
+  o(".target sm_100a");
+  o(".address_size 64");
+  const char* sig = "(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, .param .u32 p_relu, "
+                    ".param .u32 p_N, .param .u32 p_gy)";
+  for (size_t u = 0; u < ranges.size(); ++u) o(".extern .func escoin_unit_%d%s;", int(u), sig);
+  o(".visible .entry escoin_jit_sconv(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
+    ".param .u32 p_relu, .param .u32 p_N)");
+  o(".maxntid %d, 1, 1", p.warps * 32);
+  o(".minnctapersm %d", p.minb);
+  o("{");
+  o(".reg .pred %%p<2>;");
+  o(".reg .b32 %%r<8>;");
+  o(".reg .b64 %%rd<4>;");
+  o("ld.param.u64 %%rd0, [p_in];");
+  o("ld.param.u64 %%rd1, [p_out];");
+  o("ld.param.u64 %%rd2, [p_bias];");
+  o("ld.param.u32 %%r0, [p_relu];");
+  o("ld.param.u32 %%r1, [p_N];");
+  o("mov.u32 %%r2, %%ctaid.y;");
+  for (size_t u = 0; u < ranges.size(); ++u) {
+    o("setp.lt.u32 %%p0, %%r2, %d;", ranges[u].second);
+    o("@%%p0 bra.uni U%d;", int(u));
+  }
+  o("ret;");
+  for (size_t u = 0; u < ranges.size(); ++u) {
+    o("U%d:", int(u));
+    o("sub.u32 %%r3, %%r2, %d;", ranges[u].first);
+    o("{");
+    o(".param .u64 a0;");
+    o(".param .u64 a1;");
+    o(".param .u64 a2;");
+    o(".param .u32 a3;");
+    o(".param .u32 a4;");
+    o(".param .u32 a5;");
+    o("st.param.u64 [a0], %%rd0;");
+    o("st.param.u64 [a1], %%rd1;");
+    o("st.param.u64 [a2], %%rd2;");
+    o("st.param.u32 [a3], %%r0;");
+    o("st.param.u32 [a4], %%r1;");
+    o("st.param.u32 [a5], %%r3;");
+    o("call.uni escoin_unit_%d, (a0, a1, a2, a3, a4, a5);", int(u));
+    o("}");
+    o("ret;");
+  }
+  o("}");
   return o.s;
 }
 
@@ -649,6 +714,7 @@ CompileSlots& slots() {
 }
 
 const char* const kOpts[] = {"--gpu-name=sm_100a", "-O3"};
+typedef std::vector<std::string> Opts;
 
 // ---------------------------------------------------------------- cubin cache
 // ESCOIN_JIT_CACHE=<dir>: cubins keyed by two 64-bit FNV-1a hashes (different offset bases) of the
@@ -662,11 +728,11 @@ uint64_t fnv1a(const std::string& s, uint64_t h) {
   return h;
 }
 
-std::string cache_key(const std::string& ptx) {
+std::string cache_key(const std::string& ptx, const Opts& opts) {
   unsigned maj = 0, min = 0;
   nvPTXCompilerGetVersion(&maj, &min);
-  std::string salt = "escoin-jit-v2|" + std::to_string(maj) + "." + std::to_string(min);
-  for (const char* o : kOpts) salt += std::string("|") + o;
+  std::string salt = "escoin-jit-v3|" + std::to_string(maj) + "." + std::to_string(min);
+  for (const std::string& o : opts) salt += "|" + o;
   char b[64];
   snprintf(b, sizeof b, "%016llx%016llx", (unsigned long long)fnv1a(salt + ptx, 0xCBF29CE484222325ULL),
            (unsigned long long)fnv1a(ptx + salt, 0x84222325CBF29CE4ULL));
@@ -705,10 +771,10 @@ void cache_put(const std::string& dir, const std::string& key, const std::vector
   if (!ok || std::rename(tmp.c_str(), fin.c_str()) != 0) std::remove(tmp.c_str());
 }
 
-// PTX -> cubin (cache first); 0 = OK, -2 = compile error (log filled).
-int compile_ptx(const std::string& ptx, std::vector<char>* cubin, std::string* log, bool* hit) {
+// PTX -> cubin (or relocatable object with --compile-only) (cache first); 0 = OK, -2 = compile error.
+int compile_ptx(const std::string& ptx, const Opts& opts, std::vector<char>* cubin, std::string* log, bool* hit) {
   const std::string dir = cache_dir();
-  const std::string key = dir.empty() ? std::string() : cache_key(ptx);
+  const std::string key = dir.empty() ? std::string() : cache_key(ptx, opts);
   if (!dir.empty() && cache_get(dir, key, cubin)) {
     *hit = true;
     return 0;
@@ -719,7 +785,11 @@ int compile_ptx(const std::string& ptx, std::vector<char>* cubin, std::string* l
   int rc = 0;
   if (nvPTXCompilerCreate(&c, ptx.size(), ptx.c_str()) != NVPTXCOMPILE_SUCCESS) {
     rc = -2;
-  } else if (nvPTXCompilerCompile(c, 2, kOpts) != NVPTXCOMPILE_SUCCESS) {
+  } else if ([&] {
+               std::vector<const char*> o;
+               for (const std::string& x : opts) o.push_back(x.c_str());
+               return nvPTXCompilerCompile(c, int(o.size()), o.data());
+             }() != NVPTXCOMPILE_SUCCESS) {
     if (log) {
       size_t n = 0;
       nvPTXCompilerGetErrorLogSize(c, &n);
@@ -737,6 +807,36 @@ int compile_ptx(const std::string& ptx, std::vector<char>* cubin, std::string* l
   if (c) nvPTXCompilerDestroy(&c);
   slots().release();
   if (rc == 0 && !dir.empty()) cache_put(dir, key, *cubin);
+  return rc;
+}
+
+// Link relocatable objects (the units + the entry) into one cubin; 0 = OK.
+int link_objects(const std::vector<std::vector<char>>& objs, std::vector<char>* cubin, std::string* log) {
+  nvJitLinkHandle h = nullptr;
+  const char* lo[] = {"-arch=sm_100a"};
+  if (nvJitLinkCreate(&h, 1, lo) != NVJITLINK_SUCCESS) return -2;
+  int rc = 0;
+  for (size_t i = 0; i < objs.size() && rc == 0; ++i) {
+    const std::string name = "unit" + std::to_string(i);
+    if (nvJitLinkAddData(h, NVJITLINK_INPUT_CUBIN, objs[i].data(), objs[i].size(), name.c_str()) !=
+        NVJITLINK_SUCCESS)
+      rc = -2;
+  }
+  if (rc == 0 && nvJitLinkComplete(h) != NVJITLINK_SUCCESS) rc = -2;
+  if (rc != 0 && log) {
+    size_t n = 0;
+    nvJitLinkGetErrorLogSize(h, &n);
+    std::string e(n, '\0');
+    if (n) nvJitLinkGetErrorLog(h, &e[0]);
+    *log = e;
+  }
+  if (rc == 0) {
+    size_t n = 0;
+    nvJitLinkGetLinkedCubinSize(h, &n);
+    cubin->resize(n);
+    nvJitLinkGetLinkedCubin(h, cubin->data());
+  }
+  nvJitLinkDestroy(&h);
   return rc;
 }
 
@@ -768,77 +868,98 @@ std::vector<std::pair<int, int>> jit_units(const JitPlan& p, const int32_t* rowp
   return r;
 }
 
-int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
-              std::string* log) {
-  const Driver& d = driver();
-  if (!d.ok) return -1;
-  // the driver-API module calls below need the device's primary context current in THIS host
-  // thread (callers may compile from worker threads); a runtime call binds it
-  int dev = 0;
-  if (cudaFree(nullptr) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess) return -3;
-  const auto t0 = std::chrono::steady_clock::now();
+int jit_cubin(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
+              std::vector<char>* cubin_out, std::string* log) {
   jm.plan = p;
   const auto ranges = jit_units(p, rowptr);
   const int U = int(ranges.size());
   jm.units.assign(U, JitUnit());
-  std::vector<std::vector<char>> cubins(U);
-  std::vector<int> rcs(U, 0);
-  std::vector<std::string> logs(U);
+  // One unit: a complete kernel.  Several: each unit is the device function of its m-groups,
+  // compiled relocatable in its own host thread (register budget of the kernel's occupancy),
+  // then linked with a small entry kernel that calls the unit of blockIdx.y — ONE launch.
+  const int maxreg = std::min(255, 65536 / (p.warps * 32 * p.minb)) & ~7;
+  Opts uopts = {kOpts[0], kOpts[1]};
+  if (U > 1) {
+    uopts.push_back("--compile-only");
+    uopts.push_back("--maxrregcount=" + std::to_string(maxreg));
+  }
+  std::vector<std::vector<char>> objs(U + (U > 1 ? 1 : 0));
+  std::vector<int> rcs(U + 1, 0);
+  std::vector<std::string> logs(U + 1);
   auto work = [&](int u) {
     JitUnit& ju = jm.units[u];
     ju.g_lo = ranges[u].first;
     ju.g_hi = ranges[u].second;
     ju.nnz = int64_t(rowptr[std::min(p.M, ju.g_hi * p.Q)]) - rowptr[ju.g_lo * p.Q];
-    const std::string ptx = gen_ptx(p, rowptr, colidx, value, ju.g_lo, ju.g_hi);
+    const std::string ptx = gen_ptx(p, rowptr, colidx, value, ju.g_lo, ju.g_hi, U > 1 ? u : -1);
     ju.ptx_bytes = ptx.size();
-    rcs[u] = compile_ptx(ptx, &cubins[u], &logs[u], &ju.cache_hit);
-    ju.cubin_bytes = cubins[u].size();
+    rcs[u] = compile_ptx(ptx, uopts, &objs[u], &logs[u], &ju.cache_hit);
+    ju.cubin_bytes = objs[u].size();
   };
   if (U == 1) {
     work(0);
   } else {
     std::vector<std::thread> th;
     for (int u = 0; u < U; ++u) th.emplace_back(work, u);
+    bool hit = false;
+    rcs[U] = compile_ptx(gen_entry(p, ranges), Opts{kOpts[0], kOpts[1], "--compile-only"}, &objs[U], &logs[U],
+                         &hit);
     for (auto& t : th) t.join();
   }
-  for (int u = 0; u < U; ++u)
+  for (int u = 0; u <= U; ++u)
     if (rcs[u] != 0) {
       if (log) *log = logs[u];
       jm.units.clear();
       return -2;
     }
-  int rc = 0;
-  jm.regs = 0;
+  std::vector<char> linked;
+  if (U > 1 && link_objects(objs, &linked, log) != 0) {
+    jm.units.clear();
+    return -2;
+  }
+  *cubin_out = U > 1 ? std::move(linked) : std::move(objs[0]);
+  if (const char* dump = std::getenv("ESCOIN_JIT_DUMP")) {  // inspection only (cuobjdump -sass)
+    if (FILE* f = std::fopen(dump, "wb")) {
+      std::fwrite(cubin_out->data(), 1, cubin_out->size(), f);
+      std::fclose(f);
+    }
+  }
   jm.ptx_bytes = jm.cubin_bytes = 0;
   jm.cache_hits = 0;
-  for (int u = 0; u < U && rc == 0; ++u) {
-    JitUnit& ju = jm.units[u];
-    CUmodule mod = nullptr;
-    CUfunction f = nullptr;
-    if (d.load(&mod, cubins[u].data()) != CUDA_SUCCESS) { rc = -3; break; }
-    ju.module = mod;
-    if (d.get(&f, mod, "escoin_jit_sconv") != CUDA_SUCCESS ||
-        d.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, p.smem_bytes) != CUDA_SUCCESS) {
-      rc = -3;
-      break;
-    }
-    ju.func = f;
-    d.getattr(&ju.regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f);
-    jm.regs = std::max(jm.regs, ju.regs);
+  for (const JitUnit& ju : jm.units) {
     jm.ptx_bytes += ju.ptx_bytes;
-    jm.cubin_bytes += ju.cubin_bytes;
     jm.cache_hits += ju.cache_hit ? 1 : 0;
   }
-  for (int u = 1; u < U && rc == 0; ++u) {
-    cudaStream_t st = nullptr;
-    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) { rc = -3; break; }
-    jm.aux.push_back(st);
+  jm.cubin_bytes = cubin_out->size();
+  return 0;
+}
+
+int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
+              std::string* log) {
+  const Driver& d = driver();
+  if (!d.ok) return -1;
+  // the driver-API module calls below need the device's primary context current in THIS host
+  // thread (callers may compile from worker threads); a runtime call binds it
+  if (cudaFree(nullptr) != cudaSuccess) return -3;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<char> cubin;
+  const int rc = jit_cubin(jm, p, rowptr, colidx, value, &cubin, log);
+  if (rc != 0) return rc;
+  CUmodule mod = nullptr;
+  CUfunction f = nullptr;
+  if (d.load(&mod, cubin.data()) != CUDA_SUCCESS) {
+    jm.units.clear();
+    return -3;
   }
-  if (rc != 0) {
+  jm.module = mod;
+  if (d.get(&f, mod, "escoin_jit_sconv") != CUDA_SUCCESS ||
+      d.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, p.smem_bytes) != CUDA_SUCCESS) {
     jit_free(jm);
-    return rc;
+    return -3;
   }
-  (void)dev;
+  jm.func = f;
+  d.getattr(&jm.regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f);
+  d.getattr(&jm.local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, f);
   jm.compile_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return 0;
 }
@@ -846,7 +967,7 @@ int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int3
 int jit_compile_only(const char* ptx, size_t* cubin_bytes) {
   std::vector<char> cubin;
   bool hit = false;
-  if (compile_ptx(std::string(ptx), &cubin, nullptr, &hit) != 0) return -2;
+  if (compile_ptx(std::string(ptx), Opts{kOpts[0], kOpts[1]}, &cubin, nullptr, &hit) != 0) return -2;
   *cubin_bytes = cubin.size();
   return 0;
 }
@@ -854,7 +975,7 @@ int jit_compile_only(const char* ptx, size_t* cubin_bytes) {
 std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
                          int g_lo, int g_hi) {
   if (g_hi <= 0) g_hi = p.nmg;
-  return gen_ptx(p, rowptr, colidx, value, g_lo, g_hi);
+  return gen_ptx(p, rowptr, colidx, value, g_lo, g_hi, -1);
 }
 
 std::string jit_label(const JitModule& jm) {
@@ -866,13 +987,9 @@ std::string jit_label(const JitModule& jm) {
 }
 
 void jit_free(JitModule& jm) {
-  for (cudaStream_t st : jm.aux) cudaStreamDestroy(st);
-  jm.aux.clear();
-  for (JitUnit& ju : jm.units) {
-    if (ju.module && driver().ok) driver().unload(static_cast<CUmodule>(ju.module));
-    ju.module = nullptr;
-    ju.func = nullptr;
-  }
+  if (jm.module && driver().ok) driver().unload(static_cast<CUmodule>(jm.module));
+  jm.module = nullptr;
+  jm.func = nullptr;
   jm.units.clear();
 }
 
@@ -882,46 +999,16 @@ int jit_launch(const JitModule& jm, const float* in, float* out, const float* bi
   const int64_t pixels = int64_t(N) * p.E * p.F;
   const int64_t tiles = (pixels + p.T - 1) / p.T;
   const int64_t last_pos = (int64_t(N) * (p.H + p.pad) + p.pad) * p.SWs + p.L;  // staged positions stay int32
-  if (pixels > 0x7fffffff || last_pos > 0x7fffffff || jm.units.empty()) return -1;
+  if (pixels > 0x7fffffff || last_pos > 0x7fffffff || !jm.func) return -1;
   unsigned relu_u = relu ? 1u : 0u, n_u = unsigned(N);
   const void* a_in = in;
   void* a_out = out;
   const void* a_bias = bias;
   void* args[] = {&a_in, &a_out, &a_bias, &relu_u, &n_u};
-  auto launch = [&](const JitUnit& ju, cudaStream_t st) {
-    return driver().launch(static_cast<CUfunction>(ju.func), unsigned(tiles), unsigned(ju.g_hi - ju.g_lo), 1,
-                           unsigned(p.warps * 32), 1, 1, unsigned(p.smem_bytes), (CUstream)st, args, nullptr) ==
-                   CUDA_SUCCESS
-               ? 0
-               : -1;
-  };
-  const int U = int(jm.units.size());
-  if (U == 1) return launch(jm.units[0], s);
-  // Units run concurrently: fork from s onto the aux streams, join back into s.  Events are
-  // per call (no state shared between concurrent forwards), released once they complete; the
-  // pattern is legal under stream capture (it becomes parallel graph branches).
-  cudaEvent_t fork = nullptr;
-  if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return -1;
-  int rc = cudaEventRecord(fork, s) == cudaSuccess ? 0 : -1;
-  std::vector<cudaEvent_t> joins;
-  for (int u = 1; u < U && rc == 0; ++u) {
-    cudaStream_t st = jm.aux[u - 1];
-    cudaEvent_t join = nullptr;
-    if (cudaStreamWaitEvent(st, fork, 0) != cudaSuccess || launch(jm.units[u], st) != 0 ||
-        cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess) {
-      rc = -1;
-      break;
-    }
-    joins.push_back(join);
-    if (cudaEventRecord(join, st) != cudaSuccess) rc = -1;
-  }
-  if (rc == 0) rc = launch(jm.units[0], s);  // unit 0 on s itself, before s waits for the others
-  for (cudaEvent_t join : joins) {
-    if (cudaStreamWaitEvent(s, join, 0) != cudaSuccess) rc = -1;
-    cudaEventDestroy(join);
-  }
-  cudaEventDestroy(fork);
-  return rc;
+  const CUresult r = driver().launch(static_cast<CUfunction>(jm.func), unsigned(tiles), unsigned(p.nmg), 1,
+                                     unsigned(p.warps * 32), 1, 1, unsigned(p.smem_bytes), (CUstream)s, args,
+                                     nullptr);
+  return r == CUDA_SUCCESS ? 0 : -1;
 }
 
 }  // namespace escoin

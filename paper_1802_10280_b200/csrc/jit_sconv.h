@@ -31,22 +31,22 @@ struct JitPlan {
   int smem_bytes = 0;
 };
 
-// One separately compiled module: the code of m-groups [g_lo, g_hi) (blockIdx.y = g - g_lo).
+// One separately compiled unit: the code of m-groups [g_lo, g_hi).  Several units are compiled
+// in parallel as relocatable device functions and linked behind one entry kernel (one launch).
 struct JitUnit {
   int g_lo = 0, g_hi = 0;
   int64_t nnz = 0;
-  void* module = nullptr;  // CUmodule
-  void* func = nullptr;    // CUfunction
-  int regs = 0;
   size_t ptx_bytes = 0, cubin_bytes = 0;
   bool cache_hit = false;
 };
 
 struct JitModule {
   JitPlan plan;
-  std::vector<JitUnit> units;      // launched concurrently (fork/join over aux streams) by jit_launch
-  std::vector<cudaStream_t> aux;   // units.size() - 1 non-blocking streams on the handle's device
-  int regs = 0;                    // max over units
+  std::vector<JitUnit> units;
+  void* module = nullptr;          // CUmodule
+  void* func = nullptr;            // CUfunction escoin_jit_sconv
+  int regs = 0;
+  int local_bytes = 0;             // local memory per thread (call-saved registers of linked units)
   size_t ptx_bytes = 0, cubin_bytes = 0;
   double compile_s = 0.0;          // wall time of jit_build (all units, parallel)
   int cache_hits = 0;              // units loaded from ESCOIN_JIT_CACHE instead of compiled
@@ -59,6 +59,9 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
 // load; 0 = OK. log receives the compiler error log on failure.
 int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
               std::string* log);
+// Host only (no device): generate, compile and (several units) link the cubin jit_build loads.
+int jit_cubin(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
+              std::vector<char>* cubin, std::string* log);
 // The m-group ranges of the units jit_build would compile (balanced by nonzeros).
 std::vector<std::pair<int, int>> jit_units(const JitPlan& p, const int32_t* rowptr);
 // PTX of one unit (m-groups [g_lo, g_hi); g_hi <= 0: all groups).

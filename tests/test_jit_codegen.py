@@ -204,3 +204,23 @@ def test_default_unit_split_balances_nonzeros():
     nnz = [int(rowptr[min(L.M, rng[2 * u + 1] * 32)] - rowptr[rng[2 * u] * 32]) for u in range(cnt.value)]
     assert cnt.value == 16  # 16 groups of 32 rows, 472k nonzeros: one group per unit
     assert max(nnz) < 1.2 * (sum(nnz) / len(nnz))
+
+
+@pytest.mark.parametrize("units", [1, 3])
+def test_multi_unit_compile_and_link_on_host(units):
+    # several units: each compiled relocatable (its own host thread), linked with the entry kernel
+    # into ONE cubin by nvJitLink — all on the host, no device needed
+    L_ = _lib()
+    L_.escoin_internal_jit_cubin.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                             ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64),
+                                             ctypes.c_char_p, ctypes.c_int64]
+    rng = np.random.default_rng(5)
+    w = rng.standard_normal((40, 8, 3, 3)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.3] = 0.0
+    csr = escoin.Csr.stretch(w, 10, 10, 1, 1)
+    arr = (ctypes.c_int * 9)(8, 1, 0, 0, 4, 2, 0, 0, units)
+    u, nb = ctypes.c_int(), ctypes.c_int64()
+    log = ctypes.create_string_buffer(4096)
+    rc = L_.escoin_internal_jit_cubin(csr.handle, 4, arr, 9, ctypes.byref(u), ctypes.byref(nb), log, 4096)
+    assert rc == 0, log.value.decode()
+    assert u.value == units and nb.value > 0

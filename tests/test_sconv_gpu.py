@@ -377,7 +377,8 @@ def test_autotune_keeps_bits():
 
 def test_bench_two_ranks_same_device():
     # the batch-shard driver end to end with 2 ranks (gloo over CUDA tensors, both
-    # on cuda:0): CSR broadcast from rank 0, wrap_device on rank 1, max-over-ranks
+    # on cuda:0): CSR broadcast from rank 0, wrap_device on rank 1, strong scaling of the
+    # global batch, max-over-ranks
     import json
     import os
     import subprocess
@@ -385,14 +386,37 @@ def test_bench_two_ranks_same_device():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(root, "bench.py"), "--gpus", "2",
-           "--steps", "3", "--warmup", "1", "--workload", "tiny", "--no-baselines", "--no-cpu", "--no-autotune",
+           "--steps", "3", "--warmup", "1", "--workload", "tiny", "--batch", "6", "--no-baselines", "--no-cpu",
            "--dist-backend", "gloo", "--same-device"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 2 and d["value"] > 0
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 6 and d["config"]["batch_per_gpu"] == 3
+    assert d["scaling"] == "strong" and d["value"] > 0
+
+
+def test_two_ranks_shard_parity():
+    # every rank checks ITS shard of the global batch against the oracle (same global image
+    # indices) and bitwise against the full-batch forward sliced to its range
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29534", os.path.join(root, "tests", "mp_shard_check.py"),
+           "--workload", "alexnet", "--layers", "conv3,conv4", "--batch", "10"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("[")]
+    res = json.loads(lines[-1])
+    assert [x["range"] for x in res] == [[0, 5], [5, 10]]
+    for x in res:
+        assert len(x["layers"]) == 2
+        for l in x["layers"]:
+            assert l["oracle_ok"] and l["slice_bitwise"], (x["rank"], l)
 
 
 @pytest.mark.parametrize("seed", range(6))
