@@ -49,6 +49,9 @@ WL_NAMES = {"alexnet": "pruned AlexNet conv2-conv5 (4 sparse CONV layers)",
             "resnet50": "pruned ResNet-50 v1 16 sparse 3x3 CONV layers",
             "resnet50_v15": "pruned ResNet-50 v1.5 16 sparse 3x3 CONV layers (3 with stride 2)",
             "tiny": "tiny conv layer N=1 C=16 14x14 M=32 3x3"}
+# escoin_csr_jit tunings compiled per layer (Q,P,CC,NS,warps,CTAs/SM; 0 = the library's model pick);
+# escoin_csr_autotune_ex keeps the fastest under the bench's flushed-L2 conditions
+DEFAULT_JIT_TUNINGS = "0;32,1,0,0,32,1;64,1,0,0,16,1;16,1,0,0,16,2"
 METRIC = "sparse-conv images/s (whole stack of sparse layers, global batch 128)"
 
 
@@ -69,7 +72,7 @@ def parse():
     p.add_argument("--kernel", type=int, default=-1, help="sconv variant id (-1 = auto)")
     p.add_argument("--no-autotune", action="store_true", help="skip escoin_csr_autotune at setup")
     p.add_argument("--no-jit", action="store_true", help="skip the pattern-specialised kernels (escoin_csr_jit)")
-    p.add_argument("--jit-tunings", default="0;32,1,0,0,32,1;64,1,0,0,16,1;16,1,0,0,16,2",
+    p.add_argument("--jit-tunings", default=DEFAULT_JIT_TUNINGS,
                    help="';'-separated escoin_csr_jit tunings compiled per layer (0 = the library's model pick); "
                         "autotune keeps the fastest")
     p.add_argument("--no-baselines", action="store_true")

@@ -236,6 +236,33 @@ int escoin_csr_jit_info(const escoin_csr* csr, int* tunables6, int* units, int* 
 int escoin_csr_jit_stats(const escoin_csr* csr, int* units, int* cache_hits, double* compile_s,
                          int64_t* ptx_bytes);
 
+/* ---------------------------------------------------------------- engine selection
+ * "Specifically optimized for convolutions in certain parts of the parameter space" (§3.4,
+ * P:558-560): below some sparsity a dense tensor-core convolution of the pruned weights
+ * (zeros included) is faster than the direct sparse kernel.  Deterministic rule
+ * (SPEC select_engine): SPARSE when sparsity = 1 - nnz/(M*C*K*K) >= threshold
+ * (ties -> SPARSE), else DENSE_TC.  The default threshold is the measured crossover of this
+ * library's two engines on B200 (profiles/*density_sweep*), overridable per call
+ * or process-wide with ESCOIN_SPARSE_THRESHOLD=<0..1>.  Grouped layers count the zeros of the
+ * block-diagonal expansion (the dense engine computes them).
+ * ESCOIN_KERNEL_DENSE_TC selects the dense engine on a handle (escoin_csr_set_kernel): the
+ * handle's CSR is scattered back into dense [M][C][K][K] weights on its device (kept until
+ * free) and forwards run the tcgen05 3xTF32 implicit GEMM (FP32-level accuracy, within the
+ * method's 1e-5*sum|w*x| tolerance; not bitwise equal to the sparse kernels). */
+#define ESCOIN_ENGINE_SPARSE 0
+#define ESCOIN_ENGINE_DENSE_TC 1
+#define ESCOIN_KERNEL_DENSE_TC 2000
+#define ESCOIN_DEFAULT_SPARSE_THRESHOLD 0.35
+/* Active threshold: ESCOIN_SPARSE_THRESHOLD if set to a number in [0, 1], else the default. */
+double escoin_sparse_threshold(void);
+/* The rule; threshold outside [0, 1] (e.g. -1) = escoin_sparse_threshold().  Returns the
+ * engine (>= 0) or SHAPE (< 0). */
+int escoin_select_engine(int M, int C, int K, int64_t nnz, double threshold);
+/* Apply the rule to a handle on its device: DENSE_TC -> escoin_csr_set_kernel(DENSE_TC);
+ * SPARSE -> leaves the handle's sparse kernel (from DENSE_TC: back to AUTO).  *engine (may be
+ * NULL) receives the decision.  Errors: NULL, as escoin_csr_set_kernel. */
+int escoin_csr_select_engine(escoin_csr* csr, double threshold, int* engine);
+
 /* ---- Benchmark-only comparison point (NOT the method; SURVEY 8(b) "escoin_bench_*",
  * north_star: "a dense tcgen05 implicit-GEMM is kept only as a measured comparison point").
  * Dense convolution of the pruned weights INCLUDING their zeros on the 5th-generation

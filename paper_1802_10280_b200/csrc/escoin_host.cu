@@ -37,6 +37,7 @@ struct escoin_csr {
   TiledArgs targs{};  // pointers/tiling filled at DS-6 build; tensors per forward
   std::vector<JitModule*> jits;  // pattern-specialised kernels compiled for this handle (escoin_csr_jit)
   JitModule* jit = nullptr;      // the selected one
+  float* d_dense = nullptr;      // dense [M][C][K][K] weights of the dense engine (ESCOIN_KERNEL_DENSE_TC)
   std::mutex jit_mu;             // escoin_csr_jit may be called from several host threads
 };
 
@@ -918,6 +919,21 @@ int build_jit(escoin_csr* h, int n_hint, const int* tun) {
 int set_kernel(escoin_csr* h, int id, cudaStream_t s, int rank = 0) {
   int nv = 0;
   const TiledVariant* tv = tiled_variants(&nv);
+  if (id == ESCOIN_KERNEL_DENSE_TC) {  // dense tcgen05 engine: the pruned weights re-densified on the device
+    if (!h->d_dense) {
+      if (cudaMalloc(&h->d_dense, sizeof(float) * size_t(h->M) * h->C * h->K * h->K) != cudaSuccess) {
+        h->d_dense = nullptr;
+        return ESCOIN_ERR_ALLOC;
+      }
+      if (launch_densify(h->d_rowptr, h->d_colidx, h->d_value, h->M, h->C, h->K, h->H + 2 * h->pad,
+                         h->W + 2 * h->pad, h->d_dense, s) != 0 ||
+          cudaStreamSynchronize(s) != cudaSuccess)
+        return ESCOIN_ERR_CUDA;
+    }
+    free_ds6(h);
+    h->kernel = id;
+    return ESCOIN_OK;
+  }
   if (id == ESCOIN_KERNEL_JIT) {
     if (!h->jit) {
       const int rc = build_jit(h, 128, nullptr);
@@ -1155,6 +1171,7 @@ void escoin_csr_free(escoin_csr* h) {
     DeviceGuard g(h->device);
     cudaDeviceSynchronize();
     free_ds6(h);
+    if (h->d_dense) cudaFree(h->d_dense);
     for (JitModule* jm : h->jits) {
       jit_free(*jm);
       delete jm;
@@ -1185,6 +1202,8 @@ int escoin_sconv_forward(int N, int C, int H, int W, int M, int K, int stride, i
   if (h->kernel == ESCOIN_KERNEL_JIT) {
     if (int64_t(N) * C * H * W > kInt32Max) return ESCOIN_ERR_OVERFLOW;
     rc = jit_launch(*h->jit, in, out, bias, relu, N, s);
+  } else if (h->kernel == ESCOIN_KERNEL_DENSE_TC) {
+    rc = launch_dense_tc(in, h->d_dense, bias, out, N, C, H, W, M, K, stride, pad, relu ? 1 : 0, 3, s);
   } else if (h->kernel == 0) {
     rc = launch_paper(h->d_rowptr, h->d_colidx, h->d_value, in, out, bias, relu ? 1 : 0, N, C, H, W, M, K, stride,
                       pad, h->E, h->F, s);
@@ -1256,7 +1275,8 @@ int escoin_csr_set_kernel(escoin_csr* h, int id) {
   if (!h->on_device) {
     int nv = 0;
     tiled_variants(&nv);
-    if (id != ESCOIN_KERNEL_AUTO && id != ESCOIN_KERNEL_JIT && (id < 0 || id > nv)) return ESCOIN_ERR_UNSUPPORTED;
+    if (id != ESCOIN_KERNEL_AUTO && id != ESCOIN_KERNEL_JIT && id != ESCOIN_KERNEL_DENSE_TC && (id < 0 || id > nv))
+      return ESCOIN_ERR_UNSUPPORTED;
     h->kernel = id;  // resolved at escoin_csr_to_device
     return ESCOIN_OK;
   }
@@ -1351,6 +1371,8 @@ int escoin_csr_kernel_label(const escoin_csr* h, char* buf, int cap) {
   std::string l;
   if (h->kernel == ESCOIN_KERNEL_JIT && h->jit) {
     l = jit_label(*h->jit);
+  } else if (h->kernel == ESCOIN_KERNEL_DENSE_TC) {
+    l = "dense_tcgen05_3xtf32";
   } else if (h->kernel == 0) {
     l = "paper_mapping";
   } else if (h->kernel > 0) {
@@ -1366,6 +1388,35 @@ int escoin_csr_kernel_label(const escoin_csr* h, char* buf, int cap) {
   }
   std::snprintf(buf, size_t(cap), "%s", l.c_str());
   return int(l.size()) < cap ? ESCOIN_OK : ESCOIN_ERR_OVERFLOW;
+}
+
+double escoin_sparse_threshold(void) {
+  if (const char* e = std::getenv("ESCOIN_SPARSE_THRESHOLD")) {
+    char* end = nullptr;
+    const double v = std::strtod(e, &end);
+    if (end != e && v >= 0.0 && v <= 1.0) return v;
+  }
+  return ESCOIN_DEFAULT_SPARSE_THRESHOLD;
+}
+
+int escoin_select_engine(int M, int C, int K, int64_t nnz, double threshold) {
+  if (M < 1 || C < 1 || K < 1 || nnz < 0) return ESCOIN_ERR_SHAPE;
+  if (!(threshold >= 0.0 && threshold <= 1.0)) threshold = escoin_sparse_threshold();
+  const double total = double(M) * C * K * K;
+  const double sparsity = 1.0 - double(nnz) / total;
+  return sparsity >= threshold ? ESCOIN_ENGINE_SPARSE : ESCOIN_ENGINE_DENSE_TC;
+}
+
+int escoin_csr_select_engine(escoin_csr* h, double threshold, int* engine) {
+  if (!h) return ESCOIN_ERR_NULL;
+  const int e = escoin_select_engine(h->M, h->C, h->K, h->nnz, threshold);
+  if (e < 0) return e;
+  if (engine) *engine = e;
+  if (e == ESCOIN_ENGINE_SPARSE) {
+    if (h->kernel == ESCOIN_KERNEL_DENSE_TC) return escoin_csr_set_kernel(h, ESCOIN_KERNEL_AUTO);
+    return ESCOIN_OK;
+  }
+  return escoin_csr_set_kernel(h, ESCOIN_KERNEL_DENSE_TC);
 }
 
 int escoin_csr_jit_stats(const escoin_csr* h, int* units, int* cache_hits, double* compile_s, int64_t* ptx_bytes) {

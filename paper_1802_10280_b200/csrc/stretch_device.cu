@@ -88,7 +88,30 @@ __global__ void __launch_bounds__(kSt) compact_rows_kernel(const float* __restri
     __syncthreads();
   }
 }
+// Inverse of the stretch, for the dense engine (escoin_csr_set_kernel(ESCOIN_KERNEL_DENSE_TC)):
+// scatter row m's nonzeros back to w[m][c][kh][kw] (w zeroed by the caller).  colidx decodes
+// uniquely (mixed radix, R#4): c = col / (Hp*Wp), kh = (col % (Hp*Wp)) / Wp, kw = col % Wp.
+__global__ void __launch_bounds__(kSt) densify_rows_kernel(const int32_t* __restrict__ rowptr,
+                                                            const int32_t* __restrict__ colidx,
+                                                            const float* __restrict__ value, int C, int K, int Hp,
+                                                            int Wp, float* __restrict__ w) {
+  const int m = blockIdx.x;
+  const int64_t base = static_cast<int64_t>(m) * C * K * K;
+  for (int j = rowptr[m] + threadIdx.x; j < rowptr[m + 1]; j += kSt) {
+    const int col = colidx[j];
+    const int c = col / (Hp * Wp), r = col % (Hp * Wp);
+    w[base + (static_cast<int64_t>(c) * K + r / Wp) * K + r % Wp] = value[j];
+  }
+}
 }  // namespace
+
+int launch_densify(const int32_t* rowptr, const int32_t* colidx, const float* value, int M, int C, int K, int Hp,
+                   int Wp, float* w, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(w, 0, sizeof(float) * size_t(M) * C * K * K, s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  densify_rows_kernel<<<M, kSt, 0, s>>>(rowptr, colidx, value, C, K, Hp, Wp, w);
+  return static_cast<int>(cudaGetLastError());
+}
 
 int launch_stretch_count(const float* w, int M, int64_t crs, int* cnt, cudaStream_t s) {
   count_rows_kernel<<<M, kSt, 0, s>>>(w, crs, cnt);

@@ -33,9 +33,12 @@ EXPORTS = [
     "escoin_kernel_count", "escoin_kernel_info", "escoin_csr_set_kernel", "escoin_csr_get_kernel",
     "escoin_status_string", "escoin_version", "escoin_csr_autotune", "escoin_csr_stretch_device",
     "escoin_bench_dense_tc_forward", "escoin_csr_jit", "escoin_csr_jit_info", "escoin_csr_autotune_ex",
-    "escoin_csr_kernel_label", "escoin_csr_jit_stats",
+    "escoin_csr_kernel_label", "escoin_csr_jit_stats", "escoin_sparse_threshold", "escoin_select_engine",
+    "escoin_csr_select_engine",
 ]
 TUNE_VARIANTS, TUNE_JIT = 1, 2
+ENGINE_SPARSE, ENGINE_DENSE_TC = 0, 1
+KERNEL_DENSE_TC = 2000
 
 
 class EscoinError(RuntimeError):
@@ -84,11 +87,16 @@ def lib():
                                                  ctypes.POINTER(ctypes.c_float)]
             L.escoin_csr_kernel_label.argtypes = [vp, ctypes.c_char_p, ci]
             L.escoin_csr_jit_stats.argtypes = [vp, ip, ip, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(cl)]
+            L.escoin_sparse_threshold.argtypes = []
+            L.escoin_sparse_threshold.restype = ctypes.c_double
+            L.escoin_select_engine.argtypes = [ci, ci, ci, cl, ctypes.c_double]
+            L.escoin_csr_select_engine.argtypes = [vp, ctypes.c_double, ip]
             L.escoin_status_string.argtypes = [ci]
             L.escoin_status_string.restype = ctypes.c_char_p
             L.escoin_version.restype = ctypes.c_char_p
             for name in EXPORTS:
-                if name not in ("escoin_csr_free", "escoin_status_string", "escoin_version"):
+                if name not in ("escoin_csr_free", "escoin_status_string", "escoin_version",
+                                "escoin_sparse_threshold"):
                     getattr(L, name).restype = ci
             _lib = L
     return _lib
@@ -114,10 +122,25 @@ def kernels():
     return out
 
 
+def sparse_threshold() -> float:
+    """The active sparse/dense threshold (ESCOIN_SPARSE_THRESHOLD or the library default)."""
+    return float(lib().escoin_sparse_threshold())
+
+
+def select_engine(M, C, K, nnz, threshold=-1.0) -> int:
+    """escoin_select_engine: ENGINE_SPARSE if sparsity >= threshold (default: the active one)."""
+    r = lib().escoin_select_engine(M, C, K, nnz, threshold)
+    if r < 0:
+        raise EscoinError("escoin_select_engine", r)
+    return r
+
+
 def kernel_name(kernel_id: int) -> str:
     """Name of a kernel id as returned by Csr.kernel() (variants, or "jit" for KERNEL_JIT)."""
     if kernel_id == KERNEL_JIT:
         return "jit"
+    if kernel_id == KERNEL_DENSE_TC:
+        return "dense_tc"
     return kernels()[kernel_id][1]
 
 
@@ -210,6 +233,12 @@ class Csr:
             self._h, N, _ptr(inp), _ptr(out), _ptr(bias), 1 if relu else 0, reps, stream, _ptr(flush), nbytes, flags,
             ctypes.byref(bid), ctypes.byref(bms)))
         return bid.value, bms.value
+
+    def select_engine(self, threshold=-1.0) -> int:
+        """escoin_csr_select_engine: apply the sparse/dense rule to this handle (on its device)."""
+        e = ctypes.c_int()
+        _check("escoin_csr_select_engine", lib().escoin_csr_select_engine(self._h, threshold, ctypes.byref(e)))
+        return e.value
 
     def label(self) -> str:
         """escoin_csr_kernel_label: the current kernel with every tunable."""

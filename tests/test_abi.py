@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "escoin.h")).read()
-    return sorted(set(re.findall(r"^(?:int|void|const char\*)\s+(escoin_[a-z_0-9]+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:int|void|double|const char\*)\s+(escoin_[a-z_0-9]+)\(", src, re.M)))
 
 
 def test_header_symbols_exported():
@@ -95,3 +95,24 @@ def test_stretch_errors():
     assert L.escoin_sconv_forward(0, 2, 5, 5, 2, 3, 1, 0, csr.handle, None, None, None, 0, None) == escoin.OK
     L.escoin_csr_free(None)  # NULL-safe
     assert escoin.lib().escoin_status_string(-6) == b"unsupported kernel variant / shape"
+
+
+def test_select_engine_rule(monkeypatch):
+    # SPEC select_engine: SPARSE iff sparsity >= threshold (ties -> SPARSE), else DENSE_TC
+    monkeypatch.delenv("ESCOIN_SPARSE_THRESHOLD", raising=False)
+    t = escoin.sparse_threshold()
+    assert 0.0 < t < 1.0
+    M, C, K = 64, 32, 3
+    T = M * C * K * K
+    assert escoin.select_engine(M, C, K, int(0.1 * T)) == escoin.ENGINE_SPARSE      # sparsity 0.9
+    assert escoin.select_engine(M, C, K, T) == escoin.ENGINE_DENSE_TC               # sparsity 0.0
+    assert escoin.select_engine(M, C, K, 0) == escoin.ENGINE_SPARSE                 # all zero
+    nnz_at = T - 0.6 * T                                                            # sparsity exactly 0.6
+    assert escoin.select_engine(M, C, K, int(nnz_at), 0.6) == escoin.ENGINE_SPARSE
+    assert escoin.select_engine(M, C, K, int(nnz_at) + 1, 0.6) == escoin.ENGINE_DENSE_TC
+    monkeypatch.setenv("ESCOIN_SPARSE_THRESHOLD", "0.95")                          # process-wide override
+    assert escoin.sparse_threshold() == 0.95
+    assert escoin.select_engine(M, C, K, int(0.1 * T)) == escoin.ENGINE_DENSE_TC
+    assert escoin.select_engine(M, C, K, int(0.1 * T), 0.5) == escoin.ENGINE_SPARSE  # per-call override wins
+    with pytest.raises(escoin.EscoinError):
+        escoin.select_engine(0, C, K, 1)

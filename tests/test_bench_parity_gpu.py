@@ -1,0 +1,70 @@
+"""Full-size parity of exactly what bench.py times (BASELINE configs at batch 128).
+
+For every layer of every workload the bench runs, this replays bench.setup() — the same
+stretch, the same escoin_csr_jit tunings (bench.DEFAULT_JIT_TUNINGS), the same flushed
+autotune — then compares EVERY output element of the selected kernel with the fp64 oracle
+(reading R#11: |gpu - ref| <= 1e-5 * (sum|w*x| + |bias|)), and checks that every other
+compiled tuning of the layer gives bitwise the same tensor (R#12), so each kernel the
+autotune could pick is covered.  Alg.2, weight stretching P:437-442.
+"""
+import argparse
+
+import numpy as np
+import pytest
+
+import bench
+import oracle
+from paper_1802_10280_b200 import escoin, inputs, workloads
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def _setup(wl_name):
+    W = workloads.workload(wl_name)
+    args = argparse.Namespace(batch=None, weak=False, sparsity=800, kernel=-1, no_jit=False, no_autotune=False,
+                              tune_variants=False, jit_tunings=bench.DEFAULT_JIT_TUNINGS)
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    runs, n0, B, GB, _ = bench.setup(args, W, dev, 0, 1, torch, escoin, flush)
+    assert (n0, B, GB) == (0, 128, 128)
+    return W, runs
+
+
+@pytest.mark.parametrize("wl_name", ["alexnet", "resnet50", "googlenet", "googlenet_1x1", "resnet50_v15"])
+def test_bench_setup_every_output_vs_oracle(wl_name):
+    W, runs = _setup(wl_name)
+    tunings = [[int(v) for v in t.split(",")] if t.strip() not in ("", "0") else []
+               for t in bench.DEFAULT_JIT_TUNINGS.split(";")]
+    s = torch.cuda.current_stream().cuda_stream
+    failures = []
+    for r in runs:
+        L = r.L
+        bench.fwd(escoin, r, s)
+        torch.cuda.synchronize()
+        out = r.out.cpu().numpy()
+        label = r.csr.label()
+        w = inputs.layer_weights(W.net, L, 800)
+        b = inputs.bias(W.net, L.name, L.M)
+        x = r.h_x.numpy()
+        rp, ci, v = oracle.csr_stretch(w, L.H, L.W, L.stride, L.pad)
+        ref, scale = oracle.sconv(x, rp, ci, v, L.M, L.K, L.stride, L.pad, bias=b, relu=True)
+        err = np.abs(out.astype(np.float64) - ref)
+        bound = TOL * (scale + np.abs(b.astype(np.float64))[None, :, None, None])
+        if (err > bound).any():
+            failures.append("%s %s: max err/bound %.3g" % (L.name, label, float(np.max(err / bound))))
+        del ref, scale, err, bound
+        # every other compiled tuning: same bits (re-selecting a compiled tuning compiles nothing)
+        if r.csr.kernel() == escoin.KERNEL_JIT:
+            for tun in tunings:
+                try:
+                    r.csr.jit(128, *tun)
+                except escoin.EscoinError:
+                    continue
+                bench.fwd(escoin, r, s)
+                torch.cuda.synchronize()
+                if r.out.cpu().numpy().tobytes() != out.tobytes():
+                    failures.append("%s %s differs from %s" % (L.name, r.csr.label(), label))
+    assert not failures, failures

@@ -44,3 +44,49 @@ def test_dense_tc_matches_oracle(case, nsplit, tol):
     bound = tol * (scale + np.abs(b.astype(np.float64))[None, :, None, None])
     err = np.abs(got - ref)
     assert np.all(err <= bound), "max err ratio %.3g" % np.max(err / np.maximum(bound, 1e-300))
+
+
+@pytest.mark.parametrize("case", CASES[:5])
+def test_dense_engine_on_a_handle(case):
+    # ESCOIN_KERNEL_DENSE_TC: the handle's CSR densified on the device (inverse stretch) and run
+    # through the 3xTF32 tcgen05 kernel behind escoin_sconv_forward — method tolerance vs oracle
+    N, C, H, W, M, K, s, p, d = case
+    rng = np.random.default_rng(23)
+    x = rng.random((N, C, H, W)).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= d] = 0.0
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    rp, ci, v = oracle.csr_stretch(w, H, W, s, p)
+    ref, scale = oracle.sconv(x, rp, ci, v, M, K, s, p, bias=b, relu=True)
+    csr = escoin.Csr.stretch(w, H, W, s, p).to_device(0)
+    csr.set_kernel(escoin.KERNEL_DENSE_TC)
+    assert csr.label() == "dense_tcgen05_3xtf32"
+    out = escoin.forward(csr, torch.from_numpy(x).cuda(), bias=torch.from_numpy(b).cuda(), relu=True)
+    direct = escoin.bench_dense_tc_forward(torch.from_numpy(w).cuda(), torch.from_numpy(x).cuda(),
+                                           torch.from_numpy(b).cuda(), s, p, True, 3)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert got.tobytes() == direct.cpu().numpy().tobytes()  # densify == the original dense weights
+    bound = 1e-5 * (scale + np.abs(b.astype(np.float64))[None, :, None, None])
+    assert np.all(np.abs(got.astype(np.float64) - ref) <= bound)
+
+
+def test_select_engine_on_handles():
+    rng = np.random.default_rng(5)
+    N, C, H, M, K = 2, 16, 12, 32, 3
+    x = torch.from_numpy(rng.random((N, C, H, H)).astype(np.float32)).cuda()
+    for d, want in [(0.9, escoin.ENGINE_DENSE_TC), (0.2, escoin.ENGINE_SPARSE)]:
+        w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+        w[rng.random(w.shape) >= d] = 0.0
+        csr = escoin.Csr.stretch(w, H, H, 1, 1).to_device(0)
+        sparse_out = escoin.forward(csr, x, relu=True)
+        assert csr.select_engine() == want
+        assert (csr.kernel() == escoin.KERNEL_DENSE_TC) == (want == escoin.ENGINE_DENSE_TC)
+        out = escoin.forward(csr, x, relu=True)
+        torch.cuda.synchronize()
+        if want == escoin.ENGINE_SPARSE:
+            assert torch.equal(out, sparse_out)
+        else:
+            assert torch.allclose(out, sparse_out, rtol=1e-4, atol=1e-4)
+            assert csr.select_engine(threshold=0.0) == escoin.ENGINE_SPARSE  # override: back to sparse
+            assert csr.kernel() != escoin.KERNEL_DENSE_TC
