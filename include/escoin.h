@@ -202,14 +202,16 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
  *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
  *              forwards accept any N.
- *   tunables   NULL or ntunables (<= 9) ints {Q output channels per CTA,
+ *   tunables   NULL or ntunables (<= 10) ints {Q output channels per CTA,
  *              P pixels per lane, CC channels per stage, NS stages, warps per
  *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off),
  *              mbarrier pipeline (> 0 = on: warps drift up to NS-2 chunks
  *              instead of one CTA barrier per chunk), units (separately
  *              compiled modules the output-channel groups are split into,
- *              compiled in parallel host threads and launched concurrently
- *              on forked streams; <= 0: about one per 24k nonzeros, <= 32)};
+ *              compiled in parallel host threads (relocatable)
+ *              and linked into one kernel; <= 0: about one per 200k nonzeros,
+ *              <= 32), vec (input words per staging copy: <= 0 = the widest
+ *              the input row allows, 4 / 2 / 1)};
  *              <= 0 entries take the defaults.
  * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
  * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE

@@ -18,10 +18,10 @@
 // fma.rn.f32, then acc + bias[m] and ReLU — bit-identical to every other
 // variant (tested).
 //
-// Geometry (stride 1, "same" padding 2*pad == K-1): a CTA owns T consecutive
-// output pixels g = (n*E + oh)*F + ow (lane l of warp w: g0 + (w*P + j)*32 + l,
-// no idle lanes) and blockIdx.y selects the output-channel group of Q rows whose
-// code it runs.  The input is staged in a stacked layout — images one above
+// Geometry: a CTA owns T consecutive output pixels g = (n*E + oh)*F + ow (tile
+// blockIdx.y; lane l of warp w: g0 + (w*P + j)*32 + l, no idle lanes) and
+// blockIdx.x selects the output-channel group of Q rows whose code it runs (the
+// groups of a tile are consecutive CTAs: they share the tile's input through L2).  The input is staged in a stacked layout — images one above
 // the other, separated by `pad` zero rows shared by neighbours, row stride
 // SWs = W + 2*pad — where pixel g sits at pos(g) = (n*(H+pad) + oh)*SWs + ow and
 // reads tap (kh, kw) at pos(g) + kh*SWs + kw: the stretched offset f(0, kh, kw)
@@ -110,7 +110,13 @@ void plan_geometry(JitPlan& p, int /*n_hint*/) {
   const int EF = p.E * p.F;
   p.mos = 1;
   p.T = T;
-  p.SWs = p.W + 2 * p.pad;
+  // Staging vector width: V input words per cp.async when an input row is a whole number of
+  // V-word (16 / 8 byte) chunks (W % V == 0): every chunk of the stacked window is then either
+  // all data or all padding, and with a row stride SWs that is a multiple of V and a per-CTA
+  // shift of the buffer (bo, below) the data chunks are aligned in global AND shared memory.
+  if (p.vec <= 0) p.V = p.W % 4 == 0 ? 4 : p.W % 2 == 0 ? 2 : 1;
+  else p.V = (p.vec >= 4 && p.W % 4 == 0) ? 4 : (p.vec >= 2 && p.W % 2 == 0) ? 2 : 1;
+  p.SWs = (p.W + 2 * p.pad + p.V - 1) / p.V * p.V;
   auto pos = [&](int64_t g) {
     const int64_t n = g / EF, r = g % EF;
     return (n * (p.H + p.pad) + (r / p.F) * p.S) * p.SWs + (r % p.F) * p.S;
@@ -118,10 +124,11 @@ void plan_geometry(JitPlan& p, int /*n_hint*/) {
   int64_t span = 0;  // max pos(g0 + T - 1) - pos(g0); periodic in g0 with period EF
   for (int64_t g0 = 0; g0 < EF; ++g0) span = std::max(span, pos(g0 + T - 1) - pos(g0));
   p.L = int(span + int64_t(p.K - 1) * (p.SWs + 1) + 1);
-  p.Ls = (p.L + 3) & ~3;
+  p.Lv = cdiv(p.L + p.V - 1, p.V);  // V-word chunks per channel (the window shifted by bo < V)
+  p.Ls = (p.Lv * p.V + 3) & ~3;
   p.nmg = cdiv(p.M, p.Q);
   p.nch = cdiv(p.C, p.CC);
-  p.KS = cdiv(p.L, p.warps * 32);
+  p.KS = cdiv(p.Lv, p.warps * 32);
   p.smem_bytes = p.NS * p.CC * p.Ls * 4 + (p.mb ? 128 : 0);
 }
 
@@ -172,7 +179,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   const int KK = p.K * p.K, Q = p.Q, P = p.P, NT = p.warps * 32;
   const int ng = g_hi - g_lo;  // groups of this unit
   const int Hpd = p.H + 2 * p.pad, Wpd = p.W + 2 * p.pad;  // stretched geometry (R#3)
-  const int hp = p.H + p.pad, wp = p.W + p.pad;
+  const int hp = p.H + p.pad;
   const int HW = p.H * p.W, EF = p.E * p.F;
   // nonzeros per (m-group, channel), ascending tap then row
   std::vector<std::vector<Nz>> lists(size_t(ng) * p.C);
@@ -223,9 +230,11 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("ld.param.u32 %%r0, [p_relu];");
   o("ld.param.u32 %%r1, [p_N];");
   o("mov.u32 %%r2, %%tid.x;");
-  o("mov.u32 %%r3, %%ctaid.x;");
+  // grid = (m-groups, pixel tiles): the m-groups of one tile are consecutive CTAs, so they run
+  // together and read the tile's input from L2 instead of re-reading it from HBM
+  o("mov.u32 %%r3, %%ctaid.y;");
   if (unit < 0)
-    o("mov.u32 %%r4, %%ctaid.y;");
+    o("mov.u32 %%r4, %%ctaid.x;");
   else
     o("ld.param.u32 %%r4, [p_gy];");     // local m-group (the entry subtracted g_lo)
   o("mul.lo.u32 %%r28, %%r3, %d;", p.T);  // g0: first output pixel of the tile
@@ -244,6 +253,10 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   }
   o("mad.lo.u32 %%r34, %%r30, %d, %%r32;", hp);
   o("mad.lo.u32 %%r5, %%r34, %d, %%r33;", p.SWs);
+  // bo = (q0 - pad) mod V: word q of the window is stored at buffer word q - q0 + bo, which puts
+  // every data chunk (input column x = 0 mod V) on a V-word boundary
+  o("add.u32 %%r10, %%r5, %d;", p.V - p.pad % p.V);
+  o("and.b32 %%r10, %%r10, %d;", p.V - 1);
   o("mov.u32 %%r6, smem;");
   if (p.mb) {  // mbarriers full[NS], empty[NS] in the first 128 bytes, stage buffers after
     o("mov.u32 %%r36, %%r6;");
@@ -270,42 +283,42 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("mad.lo.u32 %%r34, %%r30, %d, %%r32;", hp);
     o("mad.lo.u32 %%r34, %%r34, %d, %%r33;", p.SWs);
     o("sub.u32 %%r34, %%r34, %%r5;");
+    o("add.u32 %%r34, %%r34, %%r10;");
     o("shl.b32 %%r34, %%r34, 2;");
     o("add.u32 %%r%d, %%r34, %%r6;", 40 + j);
   }
-  // staging slots: k < KS; regs: rd(32+k) src ptr, r(64+k) dst, r(64+KS+k) size, p(16+k) in range
+  // staging slots: k < KS (V-word chunk i = tid + k*NT of the window); regs: rd(32+k) src ptr,
+  // r(64+k) dst, r(64+KS+k) size (4V bytes, 0 = zero-fill: the virtual padding R#9), p(16+k) i < Lv
   for (int k = 0; k < p.KS; ++k) {
     const int rs = 64 + k, rz = 64 + p.KS + k, t0 = 64 + 2 * p.KS;  // t0.. scratch
     o("add.u32 %%r%d, %%r2, %d;", t0, k * NT);                // i
-    o("setp.lt.u32 %%p%d, %%r%d, %d;", 16 + k, t0, p.L);
-    o("shl.b32 %%r%d, %%r%d, 2;", rs, t0);
+    o("setp.lt.u32 %%p%d, %%r%d, %d;", 16 + k, t0, p.Lv);
+    o("shl.b32 %%r%d, %%r%d, %d;", rs, t0, p.V == 4 ? 4 : p.V == 2 ? 3 : 2);
     o("add.u32 %%r%d, %%r%d, %%r6;", rs, rs);                 // dst
-    o("add.u32 %%r%d, %%r%d, %%r5;", t0 + 1, t0);             // flat
-    o("div.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, p.SWs);    // R'
-    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 2, p.SWs);
-    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 3, t0 + 1, t0 + 3);  // X'
+    if (p.V > 1) o("shl.b32 %%r%d, %%r%d, %d;", t0, t0, p.V == 4 ? 2 : 1);
+    o("add.u32 %%r%d, %%r%d, %%r5;", t0 + 1, t0);
+    o("sub.s32 %%r%d, %%r%d, %%r10;", t0 + 1, t0 + 1);        // flat (may be < 0 before image 0)
+    o("div.s32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, p.SWs);    // R'
+    o("mul.lo.s32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 2, p.SWs);
+    o("sub.s32 %%r%d, %%r%d, %%r%d;", t0 + 3, t0 + 1, t0 + 3);  // X'
     o("sub.s32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 2, p.pad);    // rr
-    o("sub.s32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 3, p.pad);    // cc
-    o("setp.ge.s32 %%p0, %%r%d, 0;", t0 + 2);
+    o("sub.s32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 3, p.pad);    // x
+    o("setp.ge.s32 %%p0, %%r%d, 0;", t0 + 1);
+    o("setp.ge.and.s32 %%p0, %%r%d, 0, %%p0;", t0 + 2);
     o("setp.ge.and.s32 %%p0, %%r%d, 0, %%p0;", t0 + 3);
     o("max.s32 %%r%d, %%r%d, 0;", t0 + 2, t0 + 2);
     o("max.s32 %%r%d, %%r%d, 0;", t0 + 3, t0 + 3);
-    o("div.u32 %%r%d, %%r%d, %d;", t0 + 4, t0 + 2, hp);       // nr
+    o("div.u32 %%r%d, %%r%d, %d;", t0 + 4, t0 + 2, hp);       // n
     o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 5, t0 + 4, hp);
     o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 5, t0 + 2, t0 + 5);  // y
-    o("div.u32 %%r%d, %%r%d, %d;", t0 + 6, t0 + 3, wp);       // nc
-    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 7, t0 + 6, wp);
-    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 7, t0 + 3, t0 + 7);  // x
     o("setp.lt.and.u32 %%p0, %%r%d, %d, %%p0;", t0 + 5, p.H);
-    o("setp.lt.and.u32 %%p0, %%r%d, %d, %%p0;", t0 + 7, p.W);
-    o("setp.lt.and.u32 %%p0, %%r%d, %d, %%p0;", t0 + 6, p.mos);
-    o("mad.lo.u32 %%r%d, %%r%d, %d, %%r%d;", t0 + 4, t0 + 4, p.mos, t0 + 6);  // n
+    o("setp.lt.and.u32 %%p0, %%r%d, %d, %%p0;", t0 + 3, p.W);
     o("setp.lt.and.u32 %%p0, %%r%d, %%r1, %%p0;", t0 + 4);
     o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 4, t0 + 4, p.C * HW);
     o("mad.lo.u32 %%r%d, %%r%d, %d, %%r%d;", t0 + 4, t0 + 5, p.W, t0 + 4);
-    o("add.u32 %%r%d, %%r%d, %%r%d;", t0 + 4, t0 + 4, t0 + 7);  // src element
+    o("add.u32 %%r%d, %%r%d, %%r%d;", t0 + 4, t0 + 4, t0 + 3);  // src element (x = 0 mod V)
     o("selp.u32 %%r%d, %%r%d, 0, %%p0;", t0 + 4, t0 + 4);
-    o("selp.u32 %%r%d, 4, 0, %%p0;", rz);
+    o("selp.u32 %%r%d, %d, 0, %%p0;", rz, 4 * p.V);
     o("mul.wide.u32 %%rd%d, %%r%d, 4;", 32 + k, t0 + 4);
     o("add.s64 %%rd%d, %%rd%d, %%rd0;", 32 + k, 32 + k);
   }
@@ -326,7 +339,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     for (int cc = 0; cc < p.CC; ++cc) {
       if (ragged_c) o("setp.gt.s32 %%p1, %%r13, %d;", cc);
       for (int k = 0; k < p.KS; ++k) {
-        const bool ragged_k = (k + 1) * NT > p.L;
+        const bool ragged_k = (k + 1) * NT > p.Lv;
         std::string pred;
         if (ragged_c && ragged_k) {
           o("and.pred %%p2, %%p1, %%p%d;", 16 + k);
@@ -336,8 +349,8 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
         } else if (ragged_k) {
           pred = "@%p" + std::to_string(16 + k) + " ";
         }
-        o("%scp.async.ca.shared.global [%%r%d+%d], [%%rd%d+%d], 4, %%r%d;", pred.c_str(), 64 + 2 * p.KS + k,
-          cc * p.Ls * 4, 32 + p.KS + P + k, cc * HW * 4, 64 + p.KS + k);
+        o("%scp.async.%s.shared.global [%%r%d+%d], [%%rd%d+%d], %d, %%r%d;", pred.c_str(), p.V == 4 ? "cg" : "ca",
+          64 + 2 * p.KS + k, cc * p.Ls * 4, 32 + p.KS + P + k, cc * HW * 4, 4 * p.V, 64 + p.KS + k);
       }
     }
   };
@@ -415,13 +428,13 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     tp[1] = 'p';  // "tp: .branchtargets ..."
     o("setp.eq.u32 %%p12, %%r1, 0;");              // false at run time (N >= 1), opaque to ptxas
     o("sub.u32 %%r23, %%r21, %%r20;");             // active chunks (>= 1 here)
-    o("mov.u32 %%r22, %%nctaid.x;");
+    o("mov.u32 %%r22, %%nctaid.y;");
     o("add.u32 %%r24, %%r23, %%r22;");
     o("sub.u32 %%r24, %%r24, 1;");
     o("div.u32 %%r24, %%r24, %%r22;");             // warps needed so the group's CTAs cover every chunk
     o("setp.ge.u32 %%p14, %%r8, %%r24;");
     o("@%%p14 bra.uni PF_DONE;");
-    o("mad.lo.u32 %%r26, %%r8, %%r22, %%r3;");     // blockIdx.x + warp * gridDim.x
+    o("mad.lo.u32 %%r26, %%r8, %%r22, %%r3;");     // tile + warp * tiles
     o("rem.u32 %%r26, %%r26, %%r23;");
     o("add.u32 %%r26, %%r26, %%r20;");
     o("mad.lo.u32 %%r17, %%r4, %d, %%r26;", p.nch);
@@ -588,7 +601,7 @@ std::string gen_entry(const JitPlan& p, const std::vector<std::pair<int, int>>& 
   o("ld.param.u64 %%rd2, [p_bias];");
   o("ld.param.u32 %%r0, [p_relu];");
   o("ld.param.u32 %%r1, [p_N];");
-  o("mov.u32 %%r2, %%ctaid.y;");
+  o("mov.u32 %%r2, %%ctaid.x;");
   for (size_t u = 0; u < ranges.size(); ++u) {
     o("setp.lt.u32 %%p0, %%r2, %d;", ranges[u].second);
     o("@%%p0 bra.uni U%d;", int(u));
@@ -845,8 +858,10 @@ int link_objects(const std::vector<std::vector<char>>& objs, std::vector<char>* 
 std::vector<std::pair<int, int>> jit_units(const JitPlan& p, const int32_t* rowptr) {
   // nonzeros per m-group; units are contiguous group ranges of about equal nonzeros, about
   // kUnitNnz each (ptxas time grows with the code: ~0.25 ms per FFMA on one host core), so
-  // the largest layers compile in parallel; never more units than groups or than 32.
-  constexpr int64_t kUnitNnz = 24000;
+  // the largest layers compile in parallel; never more units than groups or than 32.  A linked
+  // unit runs 2-12% slower than the same code compiled as one kernel (measured, r02c: function
+  // ABI around the staging code), so only layers whose single compile would exceed ~50 s split.
+  constexpr int64_t kUnitNnz = 200000;
   std::vector<int64_t> gn(p.nmg, 0);
   int64_t tot = 0;
   for (int g = 0; g < p.nmg; ++g) {
@@ -981,8 +996,8 @@ std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t*
 std::string jit_label(const JitModule& jm) {
   const JitPlan& p = jm.plan;
   char b[160];
-  snprintf(b, sizeof b, "jit_q%d_p%d_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d", p.Q, p.P, p.CC, p.NS, p.warps, p.minb,
-           p.pf, p.mb, int(jm.units.size()), p.SWs);
+  snprintf(b, sizeof b, "jit_q%d_p%d_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d_v%d", p.Q, p.P, p.CC, p.NS, p.warps,
+           p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V);
   return b;
 }
 
@@ -999,13 +1014,14 @@ int jit_launch(const JitModule& jm, const float* in, float* out, const float* bi
   const int64_t pixels = int64_t(N) * p.E * p.F;
   const int64_t tiles = (pixels + p.T - 1) / p.T;
   const int64_t last_pos = (int64_t(N) * (p.H + p.pad) + p.pad) * p.SWs + p.L;  // staged positions stay int32
-  if (pixels > 0x7fffffff || last_pos > 0x7fffffff || !jm.func) return -1;
+  if (!jm.func) return -1;
+  if (pixels > 0x7fffffff || last_pos > 0x7fffffff || tiles > 65535) return -2;  // int32 positions, grid.y
   unsigned relu_u = relu ? 1u : 0u, n_u = unsigned(N);
   const void* a_in = in;
   void* a_out = out;
   const void* a_bias = bias;
   void* args[] = {&a_in, &a_out, &a_bias, &relu_u, &n_u};
-  const CUresult r = driver().launch(static_cast<CUfunction>(jm.func), unsigned(tiles), unsigned(p.nmg), 1,
+  const CUresult r = driver().launch(static_cast<CUfunction>(jm.func), unsigned(p.nmg), unsigned(tiles), 1,
                                      unsigned(p.warps * 32), 1, 1, unsigned(p.smem_bytes), (CUstream)s, args,
                                      nullptr);
   return r == CUDA_SUCCESS ? 0 : -1;

@@ -18,6 +18,7 @@ struct JitPlan {
   int minb = 0;   // CTAs per SM the register budget is compiled for
   int pf = 0;     // instruction prefetch pass: 0 = default (on), < 0 = off
   int mb = 0;     // > 0: mbarrier pipeline (warps drift up to NS-2 chunks) instead of a CTA barrier per chunk
+  int vec = 0;    // staging vector width request (<= 0: widest the input row allows; 1 = 4-byte copies)
   int units = 0;  // separately compiled modules the m-groups are split into (<= 0: by nnz, jit_build)
   // layer
   int C = 0, H = 0, W = 0, M = 0, K = 0, pad = 0, E = 0, F = 0, S = 1;
@@ -26,6 +27,7 @@ struct JitPlan {
   int SWs = 0;    // super-image row stride (words)
   int T = 0;      // slots per CTA
   int L = 0, Ls = 0;  // staged words per channel (and padded stride)
+  int V = 1, Lv = 0;  // staging vector width (words per cp.async) and V-chunks per channel
   int KS = 0;     // staging slots per thread
   int nmg = 0, nch = 0;
   int smem_bytes = 0;

@@ -246,10 +246,11 @@ class Csr:
         _check("escoin_csr_kernel_label", lib().escoin_csr_kernel_label(self._h, buf, 256))
         return buf.value.decode()
 
-    def jit(self, n_hint=128, Q=0, P=0, CC=0, NS=0, warps=0, minb=0, prefetch=0, mbarrier=0, units=0) -> "Csr":
+    def jit(self, n_hint=128, Q=0, P=0, CC=0, NS=0, warps=0, minb=0, prefetch=0, mbarrier=0, units=0,
+            vec=0) -> "Csr":
         """escoin_csr_jit: compile this layer's pattern-specialised kernel and select it."""
-        tun = (ctypes.c_int * 9)(Q, P, CC, NS, warps, minb, prefetch, mbarrier, units)
-        _check("escoin_csr_jit", lib().escoin_csr_jit(self._h, n_hint, tun, 9))
+        tun = (ctypes.c_int * 10)(Q, P, CC, NS, warps, minb, prefetch, mbarrier, units, vec)
+        _check("escoin_csr_jit", lib().escoin_csr_jit(self._h, n_hint, tun, 10))
         return self
 
     def jit_info(self):

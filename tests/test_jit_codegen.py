@@ -189,7 +189,7 @@ def test_units_partition_groups_and_union_is_the_csr(units):
 
 
 def test_default_unit_split_balances_nonzeros():
-    # about one unit per 24k nonzeros, contiguous ranges of about equal work (ResNet res5: 472k)
+    # about one unit per 200k nonzeros, contiguous ranges of about equal work (ResNet res5: 472k)
     L = [l for l in workloads.workload("resnet50").layers if l.name == "res5a_branch2b"][0]
     w = inputs.layer_weights("resnet50", L, 800)
     csr = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad)
@@ -202,8 +202,8 @@ def test_default_unit_split_balances_nonzeros():
                                         0, 0) == 0
     rowptr = csr.host_arrays()[0]
     nnz = [int(rowptr[min(L.M, rng[2 * u + 1] * 32)] - rowptr[rng[2 * u] * 32]) for u in range(cnt.value)]
-    assert cnt.value == 16  # 16 groups of 32 rows, 472k nonzeros: one group per unit
-    assert max(nnz) < 1.2 * (sum(nnz) / len(nnz))
+    assert cnt.value == 3  # 472k nonzeros, about 200k per unit
+    assert max(nnz) < 1.25 * (sum(nnz) / len(nnz))
 
 
 @pytest.mark.parametrize("units", [1, 3])

@@ -303,3 +303,31 @@ def test_autotune_ex_flushed_jit_only_and_label():
     assert kid != escoin.KERNEL_JIT
     assert not csr.label().startswith("jit_")
     assert fwd(csr, x, b, True).tobytes() == ref.tobytes()
+
+
+VEC_CASES = [  # N, C, H, W, M, K, stride, pad — rows of W % 4 == 0 / W % 2 == 0 / odd W
+    (3, 10, 16, 16, 24, 3, 1, 1), (2, 7, 12, 20, 18, 5, 1, 2), (4, 9, 14, 14, 33, 3, 1, 1), (2, 5, 10, 6, 9, 3, 2, 1),
+    (3, 6, 13, 13, 12, 3, 1, 1), (2, 12, 8, 8, 20, 1, 1, 0), (2, 4, 28, 28, 10, 3, 2, 0), (1, 3, 9, 8, 5, 3, 1, 3),
+]
+
+
+@pytest.mark.parametrize("case", VEC_CASES)
+def test_vector_staging_bitwise(case):
+    # 16/8-byte cp.async staging (per-CTA shifted, aligned buffer) vs 4-byte staging: same bits
+    N, C, H, W, M, K, st, p = case
+    rng = np.random.default_rng(abs(hash(case)) % 2**32)
+    x = rng.random((N, C, H, W)).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.3] = 0.0
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    ref, scale = oracle_ref(w, x, b, st, p, True)
+    outs = []
+    for vec in (0, 1, 2):
+        csr = escoin.Csr.stretch(w, H, W, st, p).to_device(0)
+        csr.jit(n_hint=N, Q=8, warps=4, minb=2, vec=vec)
+        outs.append(fwd(csr, x, b, True))
+        if vec == 0:
+            want = 4 if W % 4 == 0 else 2 if W % 2 == 0 else 1
+            assert csr.label().endswith("_v%d" % want)
+    check(outs[0], ref, scale, b)
+    assert outs[0].tobytes() == outs[1].tobytes() == outs[2].tobytes()
