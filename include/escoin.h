@@ -209,7 +209,7 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              instead of one CTA barrier per chunk), units (separately
  *              compiled modules the output-channel groups are split into,
  *              compiled in parallel host threads (relocatable)
- *              and linked into one kernel; <= 0: about one per 200k nonzeros,
+ *              and linked into one kernel; <= 0: one per 500k nonzeros or 1536 chunk blocks,
  *              <= 32), vec (input words per staging copy: <= 0 = the widest
  *              the input row allows, 4 / 2 / 1)};
  *              <= 0 entries take the defaults.

@@ -557,20 +557,38 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("add.s64 %%rd%d, %%rd%d, %%rd1;", rdo, rdo);
     o("add.s64 %%rd%d, %%rd%d, %%rd6;", rdo, rdo);
   }
-  for (int q = 0; q < Q; ++q) {
-    o("setp.gt.s32 %%p8, %%r19, %d;", q);
-    o("mov.f32 %%v0, 0f00000000;");
-    o("and.pred %%p9, %%p8, %%p6;");
-    o("@%%p9 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
-    for (int j = 0; j < P; ++j) {
-      const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j;
-      o("add.rn.f32 %%v1, %%a%d, %%v0;", q * P + j);
-      o("setp.gt.f32 %%p10, %%v1, 0f00000000;");
-      o("selp.f32 %%v2, %%v1, 0f00000000, %%p10;");
-      o("selp.f32 %%v1, %%v2, %%v1, %%p7;");
-      o("and.pred %%p11, %%p8, %%p%d;", pv);
-      o("@%%p11 st.global.f32 [%%rd%d+%d], %%v1;", rdo, q * EF * 4);
+  // acc + bias[m] (one fp32 add), then ReLU v > 0 ? v : 0 (R#10); relu is uniform, so the two
+  // forms are separate straight-line blocks.  Row predicates only where a group can be partial
+  // (M % Q != 0, last group); pixel predicates only matter in the tail CTA.
+  const bool full_rows = p.M % Q == 0 || g_hi * Q <= p.M;
+  for (int relu = 1; relu >= 0; --relu) {
+    if (relu) o("@!%%p7 bra.uni EPI_LIN;");
+    else o("EPI_LIN:");
+    for (int q = 0; q < Q; ++q) {
+      o("mov.f32 %%v0, 0f00000000;");
+      if (full_rows) {
+        o("@%%p6 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
+      } else {
+        o("setp.gt.s32 %%p8, %%r19, %d;", q);
+        o("and.pred %%p9, %%p8, %%p6;");
+        o("@%%p9 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
+      }
+      for (int j = 0; j < P; ++j) {
+        const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j;
+        o("add.rn.f32 %%v1, %%a%d, %%v0;", q * P + j);
+        if (relu) {
+          o("setp.gt.f32 %%p10, %%v1, 0f00000000;");
+          o("selp.f32 %%v1, %%v1, 0f00000000, %%p10;");
+        }
+        if (full_rows) {
+          o("@%%p%d st.global.f32 [%%rd%d+%d], %%v1;", pv, rdo, q * EF * 4);
+        } else {
+          o("and.pred %%p11, %%p8, %%p%d;", pv);
+          o("@%%p11 st.global.f32 [%%rd%d+%d], %%v1;", rdo, q * EF * 4);
+        }
+      }
     }
+    if (relu) o("ret;");
   }
   o("ret;");
   o("}");
@@ -860,15 +878,18 @@ std::vector<std::pair<int, int>> jit_units(const JitPlan& p, const int32_t* rowp
   // kUnitNnz each (ptxas time grows with the code: ~0.25 ms per FFMA on one host core), so
   // the largest layers compile in parallel; never more units than groups or than 32.  A linked
   // unit runs 2-12% slower than the same code compiled as one kernel (measured, r02c: function
-  // ABI around the staging code), so only layers whose single compile would exceed ~50 s split.
-  constexpr int64_t kUnitNnz = 200000;
+  // ABI around the staging code), so only layers whose single compile would take minutes split.
+  constexpr int64_t kUnitNnz = 500000;
+  constexpr int64_t kUnitBlocks = 1536;  // chunk blocks (brx targets): ptxas time also grows with these
   std::vector<int64_t> gn(p.nmg, 0);
   int64_t tot = 0;
   for (int g = 0; g < p.nmg; ++g) {
     gn[g] = int64_t(rowptr[std::min(p.M, (g + 1) * p.Q)]) - rowptr[g * p.Q];
     tot += gn[g];
   }
-  int U = p.units > 0 ? p.units : int((tot + kUnitNnz - 1) / kUnitNnz);
+  int U = p.units > 0 ? p.units
+                      : int(std::max((tot + kUnitNnz - 1) / kUnitNnz,
+                                     (int64_t(p.nmg) * p.nch + kUnitBlocks - 1) / kUnitBlocks));
   U = std::max(1, std::min(U, std::min(p.nmg, 32)));
   std::vector<std::pair<int, int>> r;
   int g = 0;
