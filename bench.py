@@ -48,6 +48,7 @@ WL_NAMES = {"alexnet": "pruned AlexNet conv2-conv5 (4 sparse CONV layers)",
             "googlenet_1x1": "pruned GoogLeNet 37 1x1 CONV layers",
             "resnet50": "pruned ResNet-50 v1 16 sparse 3x3 CONV layers",
             "resnet50_v15": "pruned ResNet-50 v1.5 16 sparse 3x3 CONV layers (3 with stride 2)",
+            "alexnet_conv1": "pruned AlexNet conv1 (11x11, stride 4; 80% sparse, NEXT-3)",
             "tiny": "tiny conv layer N=1 C=16 14x14 M=32 3x3"}
 # escoin_csr_jit tunings compiled per layer (Q,P,CC,NS,warps,CTAs/SM; 0 = the library's model pick);
 # escoin_csr_autotune_ex keeps the fastest under the bench's flushed-L2 conditions
@@ -69,6 +70,8 @@ def parse():
                         "the variants only where no specialised kernel exists)")
     p.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured graph")
     p.add_argument("--sparsity", type=int, default=800, help="per-mille (ASSUMED 800, reading R#14)")
+    p.add_argument("--skew", action="store_true",
+                   help="skewed per-row sparsity (Beta(1,b) row densities, same mean; load-balance variant)")
     p.add_argument("--kernel", type=int, default=-1, help="sconv variant id (-1 = auto)")
     p.add_argument("--no-autotune", action="store_true", help="skip escoin_csr_autotune at setup")
     p.add_argument("--no-jit", action="store_true", help="skip the pattern-specialised kernels (escoin_csr_jit)")
@@ -163,7 +166,8 @@ def setup(args, wl, device, rank, world, torch, escoin, flush):
         r = LayerRun()
         r.L = L
         if rank == 0:
-            w = inputs.layer_weights(wl.net, L, args.sparsity)
+            w = (inputs.layer_weights_skewed if getattr(args, "skew", False) else inputs.layer_weights)(
+                wl.net, L, args.sparsity)
             bias = inputs.bias(wl.net, L.name, L.M)
             src = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad)
             rp, ci, v = src.host_arrays()
@@ -313,7 +317,8 @@ def cpu_oracle_timed(wl, args, seconds, max_images):
     import oracle
     items = []
     for L in wl.layers:
-        w = inputs.layer_weights(wl.net, L, args.sparsity)
+        w = (inputs.layer_weights_skewed if getattr(args, "skew", False) else inputs.layer_weights)(
+            wl.net, L, args.sparsity)
         items.append((L, oracle.csr_stretch(w, L.H, L.W, L.stride, L.pad), inputs.bias(wl.net, L.name, L.M)))
     el = 0.0
     n = 0
@@ -532,6 +537,7 @@ def main():
             "config": {"workload": WL_NAMES[args.workload], "global_batch": images, "batch_per_gpu": B,
                        "rank0_images": [n0, n0 + B],
                        "sparsity": args.sparsity / 1000.0, "sparsity_note": "ASSUMED 80% (paper prints none)",
+                       "row_sparsity": "skewed Beta(1,b) per row" if args.skew else "uniform (magnitude pruning)",
                        "parallelism": "dp%d (batch-sharded, weights replicated)" % world,
                        "timing": "CUDA graph of the whole step" if graph is not None else "eager launches",
                        "l2": "flushed (256 MB write) before every step, outside the per-step events"},

@@ -202,7 +202,7 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
  *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
  *              forwards accept any N.
- *   tunables   NULL or ntunables (<= 10) ints {Q output channels per CTA,
+ *   tunables   NULL or ntunables (<= 11) ints {Q output channels per CTA,
  *              P pixels per lane, CC channels per stage, NS stages, warps per
  *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off),
  *              mbarrier pipeline (> 0 = on: warps drift up to NS-2 chunks
@@ -211,7 +211,12 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              compiled in parallel host threads (relocatable)
  *              and linked into one kernel; <= 0: one per 500k nonzeros or 1536 chunk blocks,
  *              <= 32), vec (input words per staging copy: <= 0 = the widest
- *              the input row allows, 4 / 2 / 1)};
+ *              the input row allows, 4 / 2 / 1), reorder (output
+ *              channels regrouped so every group of Q rows holds about the
+ *              same number of nonzeros — load balance under skewed per-row
+ *              sparsity: 0 = when the heaviest group of
+ *              consecutive rows exceeds the mean by > 5%, > 0 always, < 0
+ *              never; results are bitwise identical either way)};
  *              <= 0 entries take the defaults.
  * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
  * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE
@@ -222,8 +227,8 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  * stay compiled until escoin_csr_free, and escoin_csr_autotune times all of
  * them.  Thread-safe per handle (several tunings may compile concurrently);
  * not concurrent with forwards on the same handle.  Compile time grows with
- * nnz (about 20 s for 180k nonzeros on one host core).  Filters up to 7x7,
- * any stride and padding (K > 7 returns UNSUPPORTED).
+ * nnz (about 45 s for 180k nonzeros on one host core).  Filters up to 11x11,
+ * any stride and padding (K > 11 returns UNSUPPORTED).
  * Errors: NULL, NOT_ON_DEVICE, UNSUPPORTED (shape, tunables, compile), CUDA (load). */
 #define ESCOIN_KERNEL_JIT 1000
 int escoin_csr_jit(escoin_csr* csr, int n_hint, const int* tunables, int ntunables);

@@ -24,8 +24,7 @@ LIB = os.path.join(PKG, "libescoin.so")
 # in-process PTX compiler for the pattern-specialised kernels (jit_sconv.cpp)
 _LIB64 = os.path.join(os.path.dirname(os.path.dirname(os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc"))), "lib64")
 PTXC = os.path.join(_LIB64, "libnvptxcompiler_static.a")
-# device linker for the multi-unit specialised kernels (units compiled in parallel, linked into one)
-JITLINK = os.path.join(_LIB64, "libnvJitLink_static.a")
+# (the device linker for multi-unit specialised kernels, nvJitLink, is dlopen'ed at run time)
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -75,7 +74,7 @@ def build(jobs: int | None = None, verbose: bool = False) -> str:
     jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 4))
     with ThreadPoolExecutor(jobs) as ex:
         objs = dict(zip(srcs, ex.map(lambda s: _compile(s, headers), srcs)))
-    _link(LIB, [objs[s] for s in core + variants], [JITLINK, PTXC])
+    _link(LIB, [objs[s] for s in core + variants], [PTXC, "-ldl"])
     if verbose:
         for s in srcs:
             log = os.path.join(OBJ, os.path.basename(s) + ".o.log")

@@ -40,30 +40,15 @@ REL_D = 8  # "_x" variants: successor window of the per-case jump tables (measur
 
 VARIANTS_MASK = [
     ("m3s1_q4_4x4", 3, 1, 4, 4, 4),
-    ("m3s1_q4_1x13", 3, 1, 1, 13, 4),
     ("m5s1_q2_4x4", 5, 1, 4, 4, 2),
 ]
 # "_s": one shared dispatch site (one small jump table; pays a direct branch
 # and an exposed jump-table load per record) — better when Q*K*K is large.
 VARIANTS = [
-    ("t3s1_q4_4x4", 3, 1, 4, 4, 4),
-    ("t3s1_q4_4x4_s", 3, 1, 4, 4, 4),
-    ("t3s1_q4_4x4_x", 3, 1, 4, 4, 4),
-    ("t3s1_q4_4x4_n", 3, 1, 4, 4, 4),
     ("t3s1_q4_4x4_nx", 3, 1, 4, 4, 4),
-    ("t3s1_q3_4x4_nx", 3, 1, 4, 4, 3),
-    ("t3s1_q3_4x4_x", 3, 1, 4, 4, 3),
-    ("t3s1_q2_4x4", 3, 1, 4, 4, 2),
-    ("t3s1_q3_4x4", 3, 1, 4, 4, 3),
     ("t3s1_q4_1x13_rx", 3, 1, 1, 13, 4),
-    ("t5s1_q1_4x4", 5, 1, 4, 4, 1),
-    ("t5s1_q2_4x4_s", 5, 1, 4, 4, 2),
     ("t5s1_q2_4x4_nx", 5, 1, 4, 4, 2),
-    ("t5s1_q1_4x4_nx", 5, 1, 4, 4, 1),
-    ("t5s1_q1_5x4_nx", 5, 1, 5, 4, 1),
-    ("t3s2_q4_2x4", 3, 2, 2, 4, 4),
     ("t3s2_q4_2x4_nx", 3, 2, 2, 4, 4),
-    ("t3s2_q6_2x4_nx", 3, 2, 2, 4, 6),
 
 ]
 
@@ -492,23 +477,9 @@ int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
 # 1x1 row-block variants (mode 4, sconv_1x1.cuh): name, R rows per warp, V pixels per lane
 VARIANTS_1X1 = [
     ("d1_r4_v8", 4, 8),
-    ("d1_r4_v4", 4, 4),
-    ("d1_r3_v8", 3, 8),
-    ("d1_r2_v8", 2, 8),
-    ("d1_r6_v8", 6, 8),
-    ("d1_r8_v4", 8, 4),
     ("s1_r4_v8", 4, 8),
-    ("s1_r8_v8", 8, 8),
-    ("s1_r4_v4", 4, 4),
-    ("s1_r8_v4", 8, 4),
-    ("s1_r2_v16", 2, 16),
-    ("s1_r4_v16", 4, 16),
-    ("s1_r2_v4", 2, 4),
     ("s1_r1_v8", 1, 8),
     ("s1_r2_v2", 2, 2),
-    ("s1_r4_v2", 4, 2),
-    ("s1_r2_v1", 2, 1),
-    ("s1_r8_v2", 8, 2),
 ]
 
 TEMPLATE_1X1 = """// GENERATED by gen_sconv.py — do not edit.
@@ -528,30 +499,8 @@ int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
 # (stride 1; the "s2" entries below are stride 2)
 VARIANTS_TAP = [
     ("b3_q4_8x1", 3, 8, 4),
-    ("b3_q3_8x1", 3, 8, 3),
-    ("b3_q4_12x1", 3, 12, 4),
-    ("b3_q2_16x1", 3, 16, 2),
-    ("b3_q6_8x1", 3, 8, 6),
-    ("b3_q1_32x1", 3, 32, 1),
-    ("b3_q1_16x1", 3, 16, 1),
-    ("b3_q2_24x1", 3, 24, 2),
-    ("b5_q1_32x1", 5, 32, 1),
     ("b5_q2_16x1", 5, 16, 2),
-    ("b5_q3_16x1", 5, 16, 3),
-    ("b5_q2_20x1", 5, 20, 2),
-    ("b5_q2_12x1", 5, 12, 2),
-    ("b3_q3_16x1", 3, 16, 3),
-    ("b3_q2_12x1", 3, 12, 2),
-    ("b5_q4_8x1", 5, 8, 4),
-    ("b5_q3_8x1", 5, 8, 3),
-    ("b3s2_q2_16x1", 3, 16, 2),
-    ("b3s2_q2_8x1", 3, 8, 2),
-    ("b3s2_q3_8x1", 3, 8, 3),
     ("b3s2_q4_8x1", 3, 8, 4),
-    ("b3s2_q6_8x1", 3, 8, 6),
-    ("b3s2_q8_8x1", 3, 8, 8),
-    ("b3s2_q4_12x1", 3, 12, 4),
-    ("b3s2_q8_4x1", 3, 4, 8),
 ]
 
 TEMPLATE_TAP = """// GENERATED by gen_sconv.py — do not edit.
@@ -570,22 +519,8 @@ int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
 # Row-record variants (mode 7, no dispatch; mosaic tiling, lanes over super-image rows,
 # PW >= the (super-)row width): name, K, PW (row pixels), Q
 VARIANTS_ROW = [
-    ("c3_q2_1x13", 3, 13, 2),
     ("c3_q4_1x13", 3, 13, 4),
-    ("c3_q3_1x13", 3, 13, 3),
-    ("c3_q2_1x14", 3, 14, 2),
-    ("c3_q4_1x14", 3, 14, 4),
-    ("c3_q4_1x7", 3, 7, 4),
-    ("c3_q8_1x7", 3, 7, 8),
-    ("c3_q2_1x28", 3, 28, 2),
-    ("c5_q2_1x27", 5, 27, 2),
     ("c5_q1_1x27", 5, 27, 1),
-    ("c5_q1_1x28", 5, 28, 1),
-    ("c5_q1_1x14", 5, 14, 1),
-    ("c5_q2_1x14", 5, 14, 2),
-    ("c5_q2_1x28", 5, 28, 2),
-    ("c5_q4_1x14", 5, 14, 4),
-    ("c5_q4_1x7", 5, 7, 4),
 ]
 
 TEMPLATE_ROW = """// GENERATED by gen_sconv.py — do not edit.
@@ -602,9 +537,7 @@ int launch_{name}(const TiledArgs& a, cudaStream_t s) {{
 """
 
 VARIANTS_F2 = [
-    ("f3s1_q1_4x4", 3, 1, 4, 4, 1),
     ("f3s1_q3_4x4", 3, 1, 4, 4, 3),
-    ("f5s1_q2_4x4", 5, 1, 4, 4, 2),
 ]
 
 

@@ -49,6 +49,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <thread>
+#include <dlfcn.h>
 #include <unistd.h>
 #include <string>
 #include <vector>
@@ -99,6 +100,8 @@ const Driver& driver() {
 }
 
 int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+constexpr int kMaxK = 11;  // largest filter with a specialised form (AlexNet conv1)
 
 // ---------------------------------------------------------------- geometry
 void plan_geometry(JitPlan& p, int /*n_hint*/) {
@@ -171,6 +174,50 @@ struct Nz {
   uint32_t bits;
 };
 
+// Output-channel order of the m-groups (slot g*Q + q -> CSR row, -1 = empty slot).  Identity unless
+// p.reorder > 0, or p.reorder == 0 and the heaviest group of consecutive rows holds > 5% more
+// nonzeros than the mean (skewed per-row sparsity, "adaptively tile the output channel"):
+// then rows are dealt longest-first to the group with the fewest nonzeros so far (LPT), so every
+// group's CTAs do about the same work.  Only the grouping changes: each channel still accumulates
+// its own CSR row in ascending (c, kh, kw) order, so the output bits are identical.
+std::vector<int> row_order(const JitPlan& p, const int32_t* rowptr, bool* reordered) {
+  const int Q = p.Q, G = p.nmg;
+  std::vector<int> ord(size_t(G) * Q, -1);
+  for (int m = 0; m < p.M; ++m) ord[m] = m;
+  *reordered = false;
+  if (p.reorder < 0 || G < 2) return ord;
+  std::vector<int64_t> gn(G, 0);
+  int64_t tot = 0;
+  for (int m = 0; m < p.M; ++m) {
+    gn[m / Q] += rowptr[m + 1] - rowptr[m];
+    tot += rowptr[m + 1] - rowptr[m];
+  }
+  const int64_t mx = *std::max_element(gn.begin(), gn.end());
+  if (p.reorder == 0 && (tot == 0 || double(mx) * G <= 1.05 * double(tot))) return ord;
+  std::vector<int> rows(p.M);
+  for (int m = 0; m < p.M; ++m) rows[m] = m;
+  std::stable_sort(rows.begin(), rows.end(), [&](int a, int b) {
+    return rowptr[a + 1] - rowptr[a] > rowptr[b + 1] - rowptr[b];
+  });
+  std::vector<int64_t> load(G, 0);
+  std::vector<std::vector<int>> members(G);
+  for (int m : rows) {
+    int best = -1;
+    for (int g = 0; g < G; ++g) {
+      const int cap = g < G - 1 ? Q : p.M - (G - 1) * Q;
+      if (int(members[g].size()) < cap && (best < 0 || load[g] < load[best])) best = g;
+    }
+    members[best].push_back(m);
+    load[best] += rowptr[m + 1] - rowptr[m];
+  }
+  for (int g = 0; g < G; ++g) {
+    std::sort(members[g].begin(), members[g].end());
+    for (size_t q = 0; q < members[g].size(); ++q) ord[size_t(g) * Q + q] = members[g][q];
+  }
+  *reordered = true;
+  return ord;
+}
+
 // PTX of the m-groups [g_lo, g_hi).  unit < 0: a complete kernel `escoin_jit_sconv` (blockIdx.y =
 // g - g_lo).  unit >= 0: the device function `escoin_unit_<unit>` of a linked multi-unit kernel
 // (gen_entry below calls it with the local group index), compiled relocatable on its own.
@@ -182,9 +229,13 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   const int hp = p.H + p.pad;
   const int HW = p.H * p.W, EF = p.E * p.F;
   // nonzeros per (m-group, channel), ascending tap then row
+  bool reordered = false;
+  const std::vector<int> ord = row_order(p, rowptr, &reordered);
   std::vector<std::vector<Nz>> lists(size_t(ng) * p.C);
-  for (int m = g_lo * Q; m < std::min(p.M, g_hi * Q); ++m) {
-    const int g = m / Q - g_lo, q = m % Q;
+  for (int slot = g_lo * Q; slot < g_hi * Q; ++slot) {
+    const int m = ord[slot];
+    if (m < 0) continue;
+    const int g = slot / Q - g_lo, q = slot % Q;
     for (int j = rowptr[m]; j < rowptr[m + 1]; ++j) {
       const int col = colidx[j];
       const int c = col / (Hpd * Wpd), r = col % (Hpd * Wpd);
@@ -509,18 +560,29 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
         if (c >= p.C) break;
         const auto& l = lists[size_t(g) * p.C + c];
         if (l.empty()) continue;
-        bool used[64] = {};
+        bool used[kMaxK * kMaxK] = {};
         for (const Nz& z : l) used[z.t] = true;
-        for (int t = 0; t < KK; ++t) {
-          if (!used[t]) continue;
-          const int kh = t / p.K, kw = t % p.K;
-          for (int j = 0; j < P; ++j)
-            o("ld.shared.f32 %%x%d, [%%r%d+%d];", t * P + j, 40 + j,
-              ((buf * p.CC + cc) * p.Ls + kh * p.SWs + kw) * 4);
+        // K <= 5: every used tap of the channel is loaded, then its FFMAs (ptxas schedules); larger
+        // filters (AlexNet conv1 11x11) row by row — load a filter row's taps, run their FFMAs —
+        // so at most one row of taps is live.  Either way the list is sorted by tap, so every
+        // accumulator still receives its terms in ascending (kh, kw) order.
+        const int rows_per_pass = p.K <= 5 ? p.K : 1;
+        size_t zi = 0;
+        for (int kh0 = 0; kh0 < p.K; kh0 += rows_per_pass) {
+          const int t_end = std::min(p.K, kh0 + rows_per_pass) * p.K;
+          for (int t = kh0 * p.K; t < t_end; ++t) {
+            if (!used[t]) continue;
+            const int kh = t / p.K, kw = t % p.K;
+            for (int j = 0; j < P; ++j)
+              o("ld.shared.f32 %%x%d, [%%r%d+%d];", t * P + j, 40 + j,
+                ((buf * p.CC + cc) * p.Ls + kh * p.SWs + kw) * 4);
+          }
+          for (; zi < l.size() && l[zi].t < t_end; ++zi) {
+            const Nz& z = l[zi];
+            for (int j = 0; j < P; ++j)
+              o("fma.rn.f32 %%a%d, %%x%d, 0f%08X, %%a%d;", z.q * P + j, z.t * P + j, z.bits, z.q * P + j);
+          }
         }
-        for (const Nz& z : l)
-          for (int j = 0; j < P; ++j)
-            o("fma.rn.f32 %%a%d, %%x%d, 0f%08X, %%a%d;", z.q * P + j, z.t * P + j, z.bits, z.q * P + j);
       }
       o("bra.uni NEXT;");
     }
@@ -534,61 +596,109 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("setp.lt.u32 %%p5, %%r15, %%r21;");
   o("@%%p5 bra.uni LOOP;");
   o("EPI:");
-  // epilogue
-  o("setp.ne.u64 %%p6, %%rd2, 0;");
-  o("setp.ne.u32 %%p7, %%r0, 0;");
-  o("add.u32 %%r18, %%r4, %d;", g_lo);          // global m-group
-  o("mul.lo.u32 %%r18, %%r18, %d;", Q);          // m0
-  o("mul.wide.u32 %%rd5, %%r18, 4;");
-  o("add.s64 %%rd5, %%rd5, %%rd2;");             // bias + m0
-  o("mul.wide.u32 %%rd6, %%r18, %d;", EF * 4);   // m0 * EF bytes
-  o("sub.s32 %%r19, %d, %%r18;", p.M);           // rows left
-  for (int j = 0; j < P; ++j) {
-    const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j, t0 = 64 + 4 * p.KS + 8 * j;
-    o("add.u32 %%r%d, %%r9, %d;", t0, 32 * j);                // g
-    o("setp.le.u32 %%p%d, %%r%d, %%r29;", pv, t0);
-    o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, EF);           // n
-    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, EF);
-    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 2, t0, t0 + 2);    // oh*F + ow
-    o("mul.wide.u32 %%rd%d, %%r%d, %d;", rdo, t0 + 1, p.M * EF);
-    o("cvt.u64.u32 %%rd7, %%r%d;", t0 + 2);
-    o("add.s64 %%rd%d, %%rd%d, %%rd7;", rdo, rdo);
-    o("shl.b64 %%rd%d, %%rd%d, 2;", rdo, rdo);
-    o("add.s64 %%rd%d, %%rd%d, %%rd1;", rdo, rdo);
-    o("add.s64 %%rd%d, %%rd%d, %%rd6;", rdo, rdo);
-  }
-  // acc + bias[m] (one fp32 add), then ReLU v > 0 ? v : 0 (R#10); relu is uniform, so the two
-  // forms are separate straight-line blocks.  Row predicates only where a group can be partial
-  // (M % Q != 0, last group); pixel predicates only matter in the tail CTA.
-  const bool full_rows = p.M % Q == 0 || g_hi * Q <= p.M;
-  for (int relu = 1; relu >= 0; --relu) {
-    if (relu) o("@!%%p7 bra.uni EPI_LIN;");
-    else o("EPI_LIN:");
-    for (int q = 0; q < Q; ++q) {
-      o("mov.f32 %%v0, 0f00000000;");
-      if (full_rows) {
-        o("@%%p6 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
-      } else {
-        o("setp.gt.s32 %%p8, %%r19, %d;", q);
-        o("and.pred %%p9, %%p8, %%p6;");
-        o("@%%p9 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
-      }
-      for (int j = 0; j < P; ++j) {
-        const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j;
-        o("add.rn.f32 %%v1, %%a%d, %%v0;", q * P + j);
-        if (relu) {
-          o("setp.gt.f32 %%p10, %%v1, 0f00000000;");
-          o("selp.f32 %%v1, %%v1, 0f00000000, %%p10;");
+  if (reordered) {
+    // per-group epilogues: each group's rows are scattered output channels, so the channel of
+    // (group, q) is an immediate (bias + 4m, out + 4m*EF); one brx on the group picks the block
+    o("setp.ne.u64 %%p6, %%rd2, 0;");
+    o("setp.ne.u32 %%p7, %%r0, 0;");
+    for (int j = 0; j < P; ++j) {
+      const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j, t0 = 64 + 4 * p.KS + 8 * j;
+      o("add.u32 %%r%d, %%r9, %d;", t0, 32 * j);                // g
+      o("setp.le.u32 %%p%d, %%r%d, %%r29;", pv, t0);
+      o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, EF);           // n
+      o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, EF);
+      o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 2, t0, t0 + 2);    // oh*F + ow
+      o("mul.wide.u32 %%rd%d, %%r%d, %d;", rdo, t0 + 1, p.M * EF);
+      o("cvt.u64.u32 %%rd7, %%r%d;", t0 + 2);
+      o("add.s64 %%rd%d, %%rd%d, %%rd7;", rdo, rdo);
+      o("shl.b64 %%rd%d, %%rd%d, 2;", rdo, rdo);
+      o("add.s64 %%rd%d, %%rd%d, %%rd1;", rdo, rdo);
+    }
+    std::string et = "te: .branchtargets ";
+    for (int g = 0; g < ng; ++g) et += std::string(g ? ", " : "") + "EG" + std::to_string(g);
+    o("%s;", et.c_str());
+    o("brx.idx.uni %%r4, te;");
+    for (int g = 0; g < ng; ++g) {
+      o("EG%d:", g);
+      for (int relu = 1; relu >= 0; --relu) {
+        if (relu) o("@!%%p7 bra.uni EG%d_LIN;", g);
+        else o("EG%d_LIN:", g);
+        for (int q = 0; q < Q; ++q) {
+          const int m = ord[size_t(g_lo + g) * Q + q];
+          if (m < 0) continue;
+          o("mov.f32 %%v0, 0f00000000;");
+          o("@%%p6 ld.global.nc.f32 %%v0, [%%rd2+%d];", m * 4);
+          for (int j = 0; j < P; ++j) {
+            const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j;
+            o("add.rn.f32 %%v1, %%a%d, %%v0;", q * P + j);
+            if (relu) {
+              o("setp.gt.f32 %%p10, %%v1, 0f00000000;");
+              o("selp.f32 %%v1, %%v1, 0f00000000, %%p10;");
+            }
+            o("@%%p%d st.global.f32 [%%rd%d+%lld], %%v1;", pv, rdo, (long long)m * EF * 4);
+          }
         }
-        if (full_rows) {
-          o("@%%p%d st.global.f32 [%%rd%d+%d], %%v1;", pv, rdo, q * EF * 4);
-        } else {
-          o("and.pred %%p11, %%p8, %%p%d;", pv);
-          o("@%%p11 st.global.f32 [%%rd%d+%d], %%v1;", rdo, q * EF * 4);
-        }
+        o("ret;");
       }
     }
-    if (relu) o("ret;");
+  } else {
+    // epilogue
+    o("setp.ne.u64 %%p6, %%rd2, 0;");
+    o("setp.ne.u32 %%p7, %%r0, 0;");
+    o("add.u32 %%r18, %%r4, %d;", g_lo);          // global m-group
+    o("mul.lo.u32 %%r18, %%r18, %d;", Q);          // m0
+    o("mul.wide.u32 %%rd5, %%r18, 4;");
+    o("add.s64 %%rd5, %%rd5, %%rd2;");             // bias + m0
+    o("mul.wide.u32 %%rd6, %%r18, %d;", EF * 4);   // m0 * EF bytes
+    o("sub.s32 %%r19, %d, %%r18;", p.M);           // rows left
+    for (int j = 0; j < P; ++j) {
+      const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j, t0 = 64 + 4 * p.KS + 8 * j;
+      o("add.u32 %%r%d, %%r9, %d;", t0, 32 * j);                // g
+      o("setp.le.u32 %%p%d, %%r%d, %%r29;", pv, t0);
+      o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, EF);           // n
+      o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, EF);
+      o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 2, t0, t0 + 2);    // oh*F + ow
+      o("mul.wide.u32 %%rd%d, %%r%d, %d;", rdo, t0 + 1, p.M * EF);
+      o("cvt.u64.u32 %%rd7, %%r%d;", t0 + 2);
+      o("add.s64 %%rd%d, %%rd%d, %%rd7;", rdo, rdo);
+      o("shl.b64 %%rd%d, %%rd%d, 2;", rdo, rdo);
+      o("add.s64 %%rd%d, %%rd%d, %%rd1;", rdo, rdo);
+      o("add.s64 %%rd%d, %%rd%d, %%rd6;", rdo, rdo);
+    }
+    // acc + bias[m] (one fp32 add), then ReLU v > 0 ? v : 0 (R#10); relu is uniform, so the two
+    // forms are separate straight-line blocks.  Row predicates only where a group can be partial
+    // (M % Q != 0, last group); pixel predicates only matter in the tail CTA.
+    const bool full_rows = p.M % Q == 0 || g_hi * Q <= p.M;
+    for (int relu = 1; relu >= 0; --relu) {
+      if (relu) o("@!%%p7 bra.uni EPI_LIN;");
+      else o("EPI_LIN:");
+      for (int q = 0; q < Q; ++q) {
+        o("mov.f32 %%v0, 0f00000000;");
+        if (full_rows) {
+          o("@%%p6 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
+        } else {
+          o("setp.gt.s32 %%p8, %%r19, %d;", q);
+          o("and.pred %%p9, %%p8, %%p6;");
+          o("@%%p9 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
+        }
+        for (int j = 0; j < P; ++j) {
+          const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j;
+          o("add.rn.f32 %%v1, %%a%d, %%v0;", q * P + j);
+          if (relu) {
+            o("setp.gt.f32 %%p10, %%v1, 0f00000000;");
+            o("selp.f32 %%v1, %%v1, 0f00000000, %%p10;");
+          }
+          if (full_rows) {
+            o("@%%p%d st.global.f32 [%%rd%d+%d], %%v1;", pv, rdo, q * EF * 4);
+          } else {
+            o("and.pred %%p11, %%p8, %%p%d;", pv);
+            o("@%%p11 st.global.f32 [%%rd%d+%d], %%v1;", rdo, q * EF * 4);
+          }
+        }
+      }
+      if (relu) o("ret;");
+    }
+
   }
   o("ret;");
   o("}");
@@ -655,7 +765,7 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   // Any stride and padding: the stacked layout shares `pad` zero rows between neighbouring
   // images (image n's bottom padding is image n+1's top padding) and every window an output
   // reads lies inside its own image's padded extent, rows [oh*S, oh*S + K) of H + 2*pad.
-  if (stride < 1 || pad < 0 || K > 7) return -1;
+  if (stride < 1 || pad < 0 || K > kMaxK) return -1;
   const int E = (H + 2 * pad - K) / stride + 1, F = (W + 2 * pad - K) / stride + 1;
   if (H + 2 * pad < K || W + 2 * pad < K || E < 1 || F < 1) return -1;
   p.C = C; p.H = H; p.W = W; p.M = M; p.K = K; p.pad = pad;
@@ -684,7 +794,8 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
       for (const auto& sh : shapes) {
         const int wc = sh[0], mb = sh[1];
         const int regs = std::min(255, 65536 / (wc * 32 * mb)) & ~7;
-        if (std::min(Qc, M) + K * K + 20 > regs && !(Qc == 32 && wc == 32 && K <= 5)) continue;
+        const int tap_regs = K <= 5 ? K * K : 2 * K;  // live taps (row-wise passes above 5x5)
+        if (std::min(Qc, M) + tap_regs + 20 > regs && !(Qc == 32 && wc == 32 && K <= 5)) continue;
         JitPlan t = keep;
         t.Q = std::min(Qc, M); t.warps = wc; t.minb = mb;
         if (!plan_fit(t, n_hint)) continue;
@@ -841,33 +952,79 @@ int compile_ptx(const std::string& ptx, const Opts& opts, std::vector<char>* cub
   return rc;
 }
 
+// nvJitLink, loaded at first use from the CUDA toolkit by path (its static archive would add
+// ~100 MB to the library; a process may also hold an older libnvJitLink.so.12 of its own, e.g.
+// torch's, so the library is opened by full path, RTLD_LOCAL, and the 12.9 entry points used).
+struct JitLinkApi {
+  nvJitLinkResult (*create)(nvJitLinkHandle*, uint32_t, const char**) = nullptr;
+  nvJitLinkResult (*destroy)(nvJitLinkHandle*) = nullptr;
+  nvJitLinkResult (*add)(nvJitLinkHandle, nvJitLinkInputType, const void*, size_t, const char*) = nullptr;
+  nvJitLinkResult (*complete)(nvJitLinkHandle) = nullptr;
+  nvJitLinkResult (*cubin_size)(nvJitLinkHandle, size_t*) = nullptr;
+  nvJitLinkResult (*cubin)(nvJitLinkHandle, void*) = nullptr;
+  nvJitLinkResult (*log_size)(nvJitLinkHandle, size_t*) = nullptr;
+  nvJitLinkResult (*log)(nvJitLinkHandle, char*) = nullptr;
+  bool ok = false;
+};
+
+const JitLinkApi& jitlink() {
+  static JitLinkApi a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    std::vector<std::string> cands;
+    if (const char* e = std::getenv("ESCOIN_NVJITLINK")) cands.push_back(e);
+    cands.push_back("/usr/local/cuda/lib64/libnvJitLink.so.12");
+    cands.push_back("libnvJitLink.so.12");
+    for (const std::string& c : cands) {
+      void* h = dlopen(c.c_str(), RTLD_NOW | RTLD_LOCAL);
+      if (!h) continue;
+      auto sym = [&](const char* n) { return dlsym(h, n); };
+      a.create = reinterpret_cast<decltype(a.create)>(sym("__nvJitLinkCreate_12_9"));
+      a.destroy = reinterpret_cast<decltype(a.destroy)>(sym("__nvJitLinkDestroy_12_9"));
+      a.add = reinterpret_cast<decltype(a.add)>(sym("__nvJitLinkAddData_12_9"));
+      a.complete = reinterpret_cast<decltype(a.complete)>(sym("__nvJitLinkComplete_12_9"));
+      a.cubin_size = reinterpret_cast<decltype(a.cubin_size)>(sym("__nvJitLinkGetLinkedCubinSize_12_9"));
+      a.cubin = reinterpret_cast<decltype(a.cubin)>(sym("__nvJitLinkGetLinkedCubin_12_9"));
+      a.log_size = reinterpret_cast<decltype(a.log_size)>(sym("__nvJitLinkGetErrorLogSize_12_9"));
+      a.log = reinterpret_cast<decltype(a.log)>(sym("__nvJitLinkGetErrorLog_12_9"));
+      a.ok = a.create && a.destroy && a.add && a.complete && a.cubin_size && a.cubin && a.log_size && a.log;
+      if (a.ok) return;
+      dlclose(h);
+    }
+  });
+  return a;
+}
+
 // Link relocatable objects (the units + the entry) into one cubin; 0 = OK.
 int link_objects(const std::vector<std::vector<char>>& objs, std::vector<char>* cubin, std::string* log) {
+  const JitLinkApi& L = jitlink();
+  if (!L.ok) {
+    if (log) *log = "nvJitLink (libnvJitLink.so.12, CUDA 12.9) not found: set ESCOIN_NVJITLINK";
+    return -2;
+  }
   nvJitLinkHandle h = nullptr;
   const char* lo[] = {"-arch=sm_100a"};
-  if (nvJitLinkCreate(&h, 1, lo) != NVJITLINK_SUCCESS) return -2;
+  if (L.create(&h, 1, lo) != NVJITLINK_SUCCESS) return -2;
   int rc = 0;
   for (size_t i = 0; i < objs.size() && rc == 0; ++i) {
     const std::string name = "unit" + std::to_string(i);
-    if (nvJitLinkAddData(h, NVJITLINK_INPUT_CUBIN, objs[i].data(), objs[i].size(), name.c_str()) !=
-        NVJITLINK_SUCCESS)
-      rc = -2;
+    if (L.add(h, NVJITLINK_INPUT_CUBIN, objs[i].data(), objs[i].size(), name.c_str()) != NVJITLINK_SUCCESS) rc = -2;
   }
-  if (rc == 0 && nvJitLinkComplete(h) != NVJITLINK_SUCCESS) rc = -2;
+  if (rc == 0 && L.complete(h) != NVJITLINK_SUCCESS) rc = -2;
   if (rc != 0 && log) {
     size_t n = 0;
-    nvJitLinkGetErrorLogSize(h, &n);
+    L.log_size(h, &n);
     std::string e(n, '\0');
-    if (n) nvJitLinkGetErrorLog(h, &e[0]);
+    if (n) L.log(h, &e[0]);
     *log = e;
   }
   if (rc == 0) {
     size_t n = 0;
-    nvJitLinkGetLinkedCubinSize(h, &n);
+    L.cubin_size(h, &n);
     cubin->resize(n);
-    nvJitLinkGetLinkedCubin(h, cubin->data());
+    L.cubin(h, cubin->data());
   }
-  nvJitLinkDestroy(&h);
+  L.destroy(&h);
   return rc;
 }
 
@@ -883,8 +1040,13 @@ std::vector<std::pair<int, int>> jit_units(const JitPlan& p, const int32_t* rowp
   constexpr int64_t kUnitBlocks = 1536;  // chunk blocks (brx targets): ptxas time also grows with these
   std::vector<int64_t> gn(p.nmg, 0);
   int64_t tot = 0;
+  bool reordered = false;
+  const std::vector<int> ord = row_order(p, rowptr, &reordered);
   for (int g = 0; g < p.nmg; ++g) {
-    gn[g] = int64_t(rowptr[std::min(p.M, (g + 1) * p.Q)]) - rowptr[g * p.Q];
+    for (int q = 0; q < p.Q; ++q) {
+      const int m = ord[size_t(g) * p.Q + q];
+      if (m >= 0) gn[g] += rowptr[m + 1] - rowptr[m];
+    }
     tot += gn[g];
   }
   int U = p.units > 0 ? p.units
@@ -907,6 +1069,7 @@ std::vector<std::pair<int, int>> jit_units(const JitPlan& p, const int32_t* rowp
 int jit_cubin(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value,
               std::vector<char>* cubin_out, std::string* log) {
   jm.plan = p;
+  row_order(p, rowptr, &jm.reordered);
   const auto ranges = jit_units(p, rowptr);
   const int U = int(ranges.size());
   jm.units.assign(U, JitUnit());
@@ -926,10 +1089,10 @@ int jit_cubin(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int3
     JitUnit& ju = jm.units[u];
     ju.g_lo = ranges[u].first;
     ju.g_hi = ranges[u].second;
-    ju.nnz = int64_t(rowptr[std::min(p.M, ju.g_hi * p.Q)]) - rowptr[ju.g_lo * p.Q];
     const std::string ptx = gen_ptx(p, rowptr, colidx, value, ju.g_lo, ju.g_hi, U > 1 ? u : -1);
     ju.ptx_bytes = ptx.size();
     rcs[u] = compile_ptx(ptx, uopts, &objs[u], &logs[u], &ju.cache_hit);
+    (void)ju;
     ju.cubin_bytes = objs[u].size();
   };
   if (U == 1) {
@@ -1017,8 +1180,8 @@ std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t*
 std::string jit_label(const JitModule& jm) {
   const JitPlan& p = jm.plan;
   char b[160];
-  snprintf(b, sizeof b, "jit_q%d_p%d_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d_v%d", p.Q, p.P, p.CC, p.NS, p.warps,
-           p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V);
+  snprintf(b, sizeof b, "jit_q%d_p%d_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d_v%d%s", p.Q, p.P, p.CC, p.NS, p.warps,
+           p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V, jm.reordered ? "_ro" : "");
   return b;
 }
 

@@ -18,6 +18,7 @@ struct JitPlan {
   int minb = 0;   // CTAs per SM the register budget is compiled for
   int pf = 0;     // instruction prefetch pass: 0 = default (on), < 0 = off
   int mb = 0;     // > 0: mbarrier pipeline (warps drift up to NS-2 chunks) instead of a CTA barrier per chunk
+  int reorder = 0;  // output-channel grouping: 0 = balance groups by nonzeros if skewed, > 0 always, < 0 never
   int vec = 0;    // staging vector width request (<= 0: widest the input row allows; 1 = 4-byte copies)
   int units = 0;  // separately compiled modules the m-groups are split into (<= 0: by nnz, jit_build)
   // layer
@@ -52,6 +53,7 @@ struct JitModule {
   size_t ptx_bytes = 0, cubin_bytes = 0;
   double compile_s = 0.0;          // wall time of jit_build (all units, parallel)
   int cache_hits = 0;              // units loaded from ESCOIN_JIT_CACHE instead of compiled
+  bool reordered = false;          // output channels regrouped for load balance (row_order)
 };
 
 // 0 = supported (plan filled), < 0 = this layer has no JIT form (stride != 1, 2*pad != K-1, smem).

@@ -142,3 +142,31 @@ def layer_weights(net: str, layer, sparsity_permille: int, exact: bool = False) 
     """Pruned, group-expanded dense weights [M][C][K][K] for a workloads.Layer."""
     wg = weights(net, layer.name, layer.M, layer.C // layer.groups, layer.K, exact=exact)
     return expand_groups(prune_by_magnitude(wg, sparsity_permille), layer.groups)
+
+
+def skewed_row_density(net: str, layer: str, M: int, mean_density: float) -> np.ndarray:
+    """Per-output-channel densities d_m ~ Beta(1, b) with mean 1/(1+b) = mean_density (SURVEY §8(d),
+    the optional "skewed" variant for load balance): inverse CDF d = 1 - (1-u)^(1/b), so most rows
+    are sparser than the mean and a few are much denser."""
+    assert 0.0 < mean_density < 1.0
+    b = 1.0 / mean_density - 1.0
+    u = u01(stream_u64(key(net, layer, "skew"), M)).astype(np.float64)
+    return 1.0 - np.power(1.0 - u, 1.0 / b)
+
+
+def prune_rows_by_magnitude(w: np.ndarray, density: np.ndarray) -> np.ndarray:
+    """Row m keeps its round(d_m * T_row) largest-|w| entries (ties: lower index pruned first)."""
+    out = np.array(w, dtype=np.float32, copy=True).reshape(w.shape[0], -1)
+    T = out.shape[1]
+    for m in range(out.shape[0]):
+        zeros = T - int(round(float(density[m]) * T))
+        order = np.argsort(np.abs(out[m]), kind="stable")
+        out[m, order[:zeros]] = 0.0
+    return out.reshape(w.shape)
+
+
+def layer_weights_skewed(net: str, layer, sparsity_permille: int) -> np.ndarray:
+    """As layer_weights, but with per-row densities drawn from Beta(1, b) (mean 1 - sparsity)."""
+    wg = weights(net, layer.name, layer.M, layer.C // layer.groups, layer.K)
+    d = skewed_row_density(net, layer.name, layer.M, 1.0 - sparsity_permille / 1000.0)
+    return expand_groups(prune_rows_by_magnitude(wg, d), layer.groups)

@@ -156,6 +156,10 @@ def workload(name: str) -> Workload:
                         [l for l in googlenet_full() if l.kind == "conv" and l.K == 1])
     if name == "resnet50":
         return Workload("resnet50", "resnet50", [l for l in resnet50_full() if l.sparse])
+    if name == "alexnet_conv1":  # NEXT-3: the 11x11 / stride-4 first layer on the sparse path (80%, R#14)
+        c1 = alexnet_full()[0]
+        return Workload("alexnet_conv1", "alexnet", [Layer(c1.name, c1.C, c1.H, c1.W, c1.M, c1.K, c1.stride, c1.pad,
+                                                           c1.groups, sparse=True)])
     if name == "resnet50_v15":  # NEXT-3: three of the 16 sparse 3x3 layers have stride 2
         return Workload("resnet50_v15", "resnet50_v15", [l for l in resnet50_full(v15=True) if l.sparse])
     raise KeyError(name)

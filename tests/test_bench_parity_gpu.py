@@ -33,7 +33,8 @@ def _setup(wl_name):
     return W, runs
 
 
-@pytest.mark.parametrize("wl_name", ["alexnet", "resnet50", "googlenet", "googlenet_1x1", "resnet50_v15"])
+@pytest.mark.parametrize("wl_name", ["alexnet", "resnet50", "googlenet", "googlenet_1x1", "resnet50_v15",
+                                     "alexnet_conv1"])
 def test_bench_setup_every_output_vs_oracle(wl_name):
     W, runs = _setup(wl_name)
     tunings = [[int(v) for v in t.split(",")] if t.strip() not in ("", "0") else []

@@ -134,7 +134,7 @@ def test_generated_ptx_compiles_for_sm100a():
 
 
 def test_unsupported_shapes_have_no_specialised_form():
-    w = np.ones((4, 3, 9, 9), np.float32)  # K > 7
+    w = np.ones((4, 3, 13, 13), np.float32)  # K > 11
     csr = escoin.Csr.stretch(w, 19, 19, 2, 1)
     n = ctypes.c_int64()
     arr = (ctypes.c_int * 8)()

@@ -142,7 +142,7 @@ def test_stride_and_padding(case, tun):
 
 
 def test_unsupported_shapes_rejected():
-    w = np.ones((4, 3, 9, 9), np.float32)  # K > 7: no specialised form
+    w = np.ones((4, 3, 13, 13), np.float32)  # K > 11: no specialised form
     csr = escoin.Csr.stretch(w, 19, 19, 2, 1).to_device(0)
     with pytest.raises(escoin.EscoinError) as e:
         csr.jit()
@@ -331,3 +331,48 @@ def test_vector_staging_bitwise(case):
             assert csr.label().endswith("_v%d" % want)
     check(outs[0], ref, scale, b)
     assert outs[0].tobytes() == outs[1].tobytes() == outs[2].tobytes()
+
+
+@pytest.mark.parametrize("case", [(2, 3, 35, 35, 16, 11, 4, 0), (3, 4, 31, 29, 10, 11, 4, 2), (2, 5, 19, 19, 9, 9, 2, 4),
+                                  (1, 3, 227, 227, 24, 11, 4, 0)])
+def test_large_filters_row_wise(case):
+    # K up to 11 (AlexNet conv1, 11x11 / stride 4): taps loaded and consumed filter row by row
+    N, C, H, W, M, K, st, p = case
+    rng = np.random.default_rng(K * 100 + H)
+    x = rng.random((N, C, H, W)).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.2] = 0.0
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    ref, scale = oracle_ref(w, x, b, st, p, True)
+    csr = escoin.Csr.stretch(w, H, W, st, p).to_device(0)
+    csr.jit(n_hint=N)
+    assert csr.kernel() == escoin.KERNEL_JIT
+    out = fwd(csr, x, b, True)
+    check(out, ref, scale, b)
+    csr.set_kernel(0)
+    assert out.tobytes() == fwd(csr, x, b, True).tobytes()
+
+
+@pytest.mark.parametrize("reorder", [1, 0])
+def test_row_reordering_for_skewed_rows_bitwise(reorder):
+    # skewed per-row sparsity (Beta(1, b) row densities): output channels regrouped so every group of
+    # Q rows holds about the same nonzeros (load balance) — same bits, epilogue scatters
+    from paper_1802_10280_b200.workloads import Layer
+    L = Layer("skew", 48, 14, 14, 100, 3, 1, 1)
+    w = inputs.layer_weights_skewed("skewtest", L, 800)
+    rng = np.random.default_rng(4)
+    x = rng.random((3, L.C, L.H, L.W)).astype(np.float32)
+    b = (rng.random(L.M) * 0.2 - 0.1).astype(np.float32)
+    ref, scale = oracle_ref(w, x, b, 1, 1, True)
+    c0 = escoin.Csr.stretch(w, L.H, L.W, 1, 1).to_device(0)
+    c0.jit(n_hint=3, Q=16, warps=8, reorder=-1)
+    assert not c0.label().endswith("_ro")
+    c1 = escoin.Csr.stretch(w, L.H, L.W, 1, 1).to_device(0)
+    c1.jit(n_hint=3, Q=16, warps=8, reorder=reorder)
+    assert c1.label().endswith("_ro")  # skewed enough that auto (0) regroups too
+    o0, o1 = fwd(c0, x, b, True), fwd(c1, x, b, False)
+    o1r = fwd(c1, x, b, True)
+    check(o1r, ref, scale, b)
+    assert o0.tobytes() == o1r.tobytes()
+    ref_lin, scale_lin = oracle_ref(w, x, b, 1, 1, False)
+    check(o1, ref_lin, scale_lin, b)

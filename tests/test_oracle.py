@@ -408,3 +408,25 @@ def test_resnet50_v15_macs():
     assert sum(l.weights for l in full) == sum(l.weights for l in workloads.resnet50_full())
     sparse = [l for l in full if l.sparse]
     assert len(sparse) == 16 and sum(l.stride == 2 for l in sparse) == 3
+
+
+def test_skewed_generator_contract():
+    # SURVEY §8(d) skewed variant: per-row densities Beta(1, b) with the requested mean, each row pruned
+    # to round(d_m * T_row) by magnitude; deterministic (counter-based keys)
+    L = workloads.workload("resnet50").layers[10]
+    w = inputs.layer_weights_skewed("resnet50", L, 800)
+    w2 = inputs.layer_weights_skewed("resnet50", L, 800)
+    assert w.tobytes() == w2.tobytes()
+    d = inputs.skewed_row_density("resnet50", L.name, L.M, 0.2)
+    T = L.C * L.K * L.K
+    per_row = np.count_nonzero(w.reshape(L.M, -1), axis=1)
+    assert np.array_equal(per_row, np.round(d * T).astype(int))
+    assert abs(per_row.sum() / w.size - 0.2) < 0.03          # mean density ~ 0.2
+    assert per_row.max() > 2.5 * per_row.mean()               # skewed: a heavy tail
+    # surviving entries are the largest |w| of their row
+    dense = inputs.weights("resnet50", L.name, L.M, L.C, L.K)
+    for m in [0, 7, 100]:
+        kept = np.abs(dense[m].reshape(-1))[w[m].reshape(-1) != 0]
+        dropped = np.abs(dense[m].reshape(-1))[w[m].reshape(-1) == 0]
+        if kept.size and dropped.size:
+            assert kept.min() >= dropped.max()

@@ -33,7 +33,8 @@ def main():
     from concurrent.futures import ThreadPoolExecutor
     handles = []
     for L in layers:
-        w = inputs.layer_weights(wl.net, L, wl.sparsity_permille)
+        w = (inputs.layer_weights_skewed if os.environ.get("AB_SKEW") else inputs.layer_weights)(
+            wl.net, L, wl.sparsity_permille)
         b = torch.from_numpy(inputs.bias(wl.net, L.name, L.M)).to(dev)
         x = torch.from_numpy(inputs.activations(wl.net, L.name, 0, N, L.C, L.H, L.W)).to(dev)
         out = torch.empty((N, L.M, L.E, L.F), device=dev)
