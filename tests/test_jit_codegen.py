@@ -24,12 +24,14 @@ def _lib():
 
 
 def gen_ptx(csr, n_hint=16, **tun):
-    keys = ["Q", "P", "CC", "NS", "warps", "minb", "prefetch", "mbarrier"]
-    arr = (ctypes.c_int * 8)(*[tun.get(k, 0) for k in keys])
+    # reorder defaults to -1 here (identity grouping: accumulator (g, q) is row g*Q + q)
+    keys = ["Q", "P", "CC", "NS", "warps", "minb", "prefetch", "mbarrier", "units", "vec", "reorder"]
+    tun.setdefault("reorder", -1)
+    arr = (ctypes.c_int * 11)(*[tun.get(k, 0) for k in keys])
     L, n = _lib(), ctypes.c_int64()
-    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 8, None, 0, ctypes.byref(n)) == 0
+    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 11, None, 0, ctypes.byref(n)) == 0
     buf = ctypes.create_string_buffer(n.value + 1)
-    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 8, buf, n.value + 1, ctypes.byref(n)) == 0
+    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 11, buf, n.value + 1, ctypes.byref(n)) == 0
     return buf.value.decode()
 
 
@@ -52,7 +54,7 @@ def fma_stream(ptx):
     return out
 
 
-def check_rows(csr, ptx, Q, P, stream=None):
+def check_rows(csr, ptx, Q, P, stream=None, order=None):
     info = csr.info()
     M, K, H, W, pad = info["M"], info["K"], info["H"], info["W"], info["pad"]
     Hp, Wp = H + 2 * pad, W + 2 * pad
@@ -62,8 +64,9 @@ def check_rows(csr, ptx, Q, P, stream=None):
     per_acc = {}
     for g, a, x, bits in stream:
         per_acc.setdefault((g, a), []).append((x, bits))
+    slot_of = {m: divmod(m, Q) for m in range(M)} if order is None else {m: gq for gq, m in order.items()}
     for m in range(M):
-        g, q = divmod(m, Q)
+        g, q = slot_of[m]
         r0, r1 = rowptr[m], rowptr[m + 1]
         bits = value[r0:r1].view(np.uint32).tolist()
         rem = colidx[r0:r1] % (Hp * Wp)
@@ -142,8 +145,9 @@ def test_unsupported_shapes_have_no_specialised_form():
 
 
 def unit_split(csr, n_hint=16, **tun):
-    keys = ["Q", "P", "CC", "NS", "warps", "minb", "prefetch", "mbarrier", "units"]
-    arr = (ctypes.c_int * 9)(*[tun.get(k, 0) for k in keys])
+    keys = ["Q", "P", "CC", "NS", "warps", "minb", "prefetch", "mbarrier", "units", "vec", "reorder"]
+    tun.setdefault("reorder", -1)
+    arr = (ctypes.c_int * 11)(*[tun.get(k, 0) for k in keys])
     L = _lib()
     L.escoin_internal_jit_units.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                                             ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
@@ -151,16 +155,16 @@ def unit_split(csr, n_hint=16, **tun):
                                             ctypes.c_int, ctypes.c_int]
     rng = (ctypes.c_int * 64)()
     cnt = ctypes.c_int()
-    assert L.escoin_internal_jit_units(csr.handle, n_hint, arr, 9, rng, 64, ctypes.byref(cnt), None, 0, None,
+    assert L.escoin_internal_jit_units(csr.handle, n_hint, arr, 11, rng, 64, ctypes.byref(cnt), None, 0, None,
                                        0, 0) == 0
     ranges = [(rng[2 * u], rng[2 * u + 1]) for u in range(cnt.value)]
     ptxs = []
     for lo, hi in ranges:
         n = ctypes.c_int64()
-        assert L.escoin_internal_jit_units(csr.handle, n_hint, arr, 9, None, 0, ctypes.byref(cnt), None, 0,
+        assert L.escoin_internal_jit_units(csr.handle, n_hint, arr, 11, None, 0, ctypes.byref(cnt), None, 0,
                                            ctypes.byref(n), lo, hi) == 0
         buf = ctypes.create_string_buffer(n.value + 1)
-        assert L.escoin_internal_jit_units(csr.handle, n_hint, arr, 9, None, 0, ctypes.byref(cnt), buf,
+        assert L.escoin_internal_jit_units(csr.handle, n_hint, arr, 11, None, 0, ctypes.byref(cnt), buf,
                                            n.value + 1, ctypes.byref(n), lo, hi) == 0
         ptxs.append(buf.value.decode())
     return ranges, ptxs
@@ -229,3 +233,36 @@ def test_multi_unit_compile_and_link_on_host(units):
     rc = L_.escoin_internal_jit_cubin(csr.handle, 4, arr, 9, ctypes.byref(u), ctypes.byref(nb), log, 4096)
     assert rc == 0, log.value.decode()
     assert u.value == units and nb.value > 0
+
+
+def test_reordered_groups_fma_stream_and_epilogue():
+    # reorder=1: output channels regrouped (LPT by nonzeros); the per-group epilogue stores accumulator
+    # (g, q) at channel m (offset 4*m*E*F): decode that map from the PTX, then every channel's FFMA
+    # stream must still be exactly its CSR row, and every channel must be stored exactly once
+    rng = np.random.default_rng(9)
+    M, C, H, K, Q = 40, 6, 9, 3, 8
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    dens = rng.beta(1.0, 4.0, M)
+    w[rng.random(w.shape) >= dens[:, None, None, None]] = 0.0
+    csr = escoin.Csr.stretch(w, H, H, 1, 1)
+    ptx = gen_ptx(csr, Q=Q, reorder=1)
+    order, g = {}, None
+    for line in ptx.splitlines():
+        m = re.match(r"^EG(\d+):", line)
+        if m:
+            g, acc = int(m.group(1)), None
+            continue
+        m = re.search(r"add\.rn\.f32 %v1, %a(\d+), %v0;", line)
+        if m and g is not None:
+            acc = int(m.group(1))
+            continue
+        m = re.search(r"st\.global\.f32 \[%rd\d+\+(\d+)\], %v1;", line)
+        if m and g is not None and acc is not None:
+            order.setdefault((g, acc), int(m.group(1)) // (4 * H * H))
+    assert sorted(order.values()) == list(range(M))
+    assert order != {divmod(m, Q): m for m in range(M)}  # actually regrouped
+    check_rows(csr, ptx, Q, 1, order=order)
+    # groups hold about equal nonzeros after regrouping
+    rowptr = csr.host_arrays()[0]
+    loads = [sum(int(rowptr[m + 1] - rowptr[m]) for (gg, _), m in order.items() if gg == gi) for gi in range(M // Q)]
+    assert max(loads) <= 1.1 * (sum(loads) / len(loads))
