@@ -49,6 +49,8 @@ WL_NAMES = {"alexnet": "pruned AlexNet conv2-conv5 (4 sparse CONV layers)",
             "resnet50": "pruned ResNet-50 v1 16 sparse 3x3 CONV layers",
             "resnet50_v15": "pruned ResNet-50 v1.5 16 sparse 3x3 CONV layers (3 with stride 2)",
             "alexnet_conv1": "pruned AlexNet conv1 (11x11, stride 4; 80% sparse, NEXT-3)",
+            "alexnet_convs": "AlexNet all 5 CONV layers: conv1 dense (unpruned), conv2-5 pruned (NEXT-2 stack)",
+            "resnet50_convs": "ResNet-50 v1 all 53 CONV layers: 16 pruned 3x3, 37 dense (NEXT-2 stack)",
             "tiny": "tiny conv layer N=1 C=16 14x14 M=32 3x3"}
 # escoin_csr_jit tunings compiled per layer (Q,P,CC,NS,warps,CTAs/SM; 0 = the library's model pick);
 # escoin_csr_autotune_ex keeps the fastest under the bench's flushed-L2 conditions
@@ -69,6 +71,8 @@ def parse():
                    help="autotune also over the compiled interpreter variants (default: specialised kernels only, "
                         "the variants only where no specialised kernel exists)")
     p.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured graph")
+    p.add_argument("--engine", default="auto", choices=["auto", "sparse", "dense"],
+                   help="per-layer engine: auto = escoin_select_engine (sparsity >= threshold -> sparse), or forced")
     p.add_argument("--sparsity", type=int, default=800, help="per-mille (ASSUMED 800, reading R#14)")
     p.add_argument("--skew", action="store_true",
                    help="skewed per-row sparsity (Beta(1,b) row densities, same mean; load-balance variant)")
@@ -165,9 +169,10 @@ def setup(args, wl, device, rank, world, torch, escoin, flush):
     for L in wl.layers:
         r = LayerRun()
         r.L = L
+        sp = args.sparsity if L.sparse else 0  # whole-stack workloads: layers the paper leaves dense
         if rank == 0:
-            w = (inputs.layer_weights_skewed if getattr(args, "skew", False) else inputs.layer_weights)(
-                wl.net, L, args.sparsity)
+            w = (inputs.layer_weights_skewed if getattr(args, "skew", False) and L.sparse else inputs.layer_weights)(
+                wl.net, L, sp)
             bias = inputs.bias(wl.net, L.name, L.M)
             src = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad)
             rp, ci, v = src.host_arrays()
@@ -190,6 +195,13 @@ def setup(args, wl, device, rank, world, torch, escoin, flush):
             r.csr.to_device(device.index, torch.cuda.current_stream().cuda_stream)
             r.bias = torch.from_numpy(bias).to(device)
         r.nnz = int(r.csr.info()["nnz"])
+        # NEXT-1 engine selection: the dense tcgen05 engine below the measured sparsity crossover
+        eng = getattr(args, "engine", "auto")
+        if eng == "dense" or (eng == "auto" and escoin.select_engine(L.M, L.C, L.K, r.nnz) == escoin.ENGINE_DENSE_TC):
+            r.csr.set_kernel(escoin.KERNEL_DENSE_TC)
+            r.engine = "dense_tc"
+        else:
+            r.engine = "sparse"
         x = inputs.activations(wl.net, L.name, n0, B, L.C, L.H, L.W)
         r.h_x = torch.from_numpy(x).pin_memory()
         r.x = r.h_x.to(device)
@@ -211,6 +223,8 @@ def setup(args, wl, device, rank, world, torch, escoin, flush):
 
         def jit(task):
             r, tun = task
+            if r.engine != "sparse":
+                return None
             try:
                 r.csr.jit(B, *tun)
             except escoin.EscoinError as e:
@@ -237,7 +251,7 @@ def setup(args, wl, device, rank, world, torch, escoin, flush):
             torch.distributed.barrier()
     t0 = time.time()
     for r in runs:
-        if args.kernel == -1 and not args.no_autotune:
+        if args.kernel == -1 and not args.no_autotune and r.engine == "sparse":
             # kernel customization (paper §3.4): measured once at setup, untimed, each candidate
             # timed alone after an L2 flush like the timed steps (escoin_csr_autotune_ex)
             flags = escoin.TUNE_JIT
@@ -517,12 +531,18 @@ def main():
     dom = int(np.argmax(layer_ms))
     rd = runs[dom]
     achieved = rd.flops / (layer_ms[dom] / 1e3) / 1e12
+    bound, peak_used, peak_basis = "alu", peak_tf, "FP32 FFMA %d SMs x 128 lanes x 2 x %.0f MHz (derived, DESIGN.md)" % (
+        nsm, sm_max)
+    if rd.engine == "dense_tc":  # 3xTF32 on tcgen05: three TF32 MMAs per FP32-accurate product
+        tf32 = (peaks.get("bf16_tflops") or 2250.0) * 0.5
+        bound, peak_used = "tensor", tf32 / 3.0
+        peak_basis = "TF32 dense = 0.5 x measured BF16 %.0f TFLOP/s (nominal ratio), / 3 for 3xTF32" % (2 * tf32)
     traffic = load_traffic(args.workload).get(rd.L.name)
     layers_out = []
     for r, ms, mn, md in zip(runs, layer_ms, layer_ms_min, layer_ms_med):
         layers_out.append({"layer": r.L.name, "ms": round(float(ms), 5), "ms_min": round(float(mn), 5),
                            "ms_median": round(float(md), 5), "kernel": r.kernel, "nnz": r.nnz,
-                           "jit_compile_s": getattr(r, "jit_s", None), "units": r.units,
+                           "jit_compile_s": getattr(r, "jit_s", None), "units": r.units, "engine": r.engine,
                            "autotune_ms": (r.tune or {}).get("ms"),
                            "gflop": round(r.flops / 1e9, 4),
                            "tflops": round(r.flops / (ms / 1e3) / 1e12, 3),
@@ -541,11 +561,10 @@ def main():
                        "parallelism": "dp%d (batch-sharded, weights replicated)" % world,
                        "timing": "CUDA graph of the whole step" if graph is not None else "eager launches",
                        "l2": "flushed (256 MB write) before every step, outside the per-step events"},
-            "roofline": {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak_tf, 2),
-                         "unit": "TFLOP/s", "frac": round(achieved / peak_tf, 4), "traffic": traffic,
+            "roofline": {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak_used, 2),
+                         "unit": "TFLOP/s", "frac": round(achieved / peak_used, 4), "traffic": traffic,
                          "kernel": "sconv %s (%s)" % (rd.kernel, rd.L.name),
-                         "peak_basis": "FP32 FFMA %d SMs x 128 lanes x 2 x %.0f MHz (derived, DESIGN.md)" % (
-                             nsm, sm_max),
+                         "peak_basis": peak_basis,
                          "hbm_view": {"alg_gbs": round(rd.alg_bytes / (layer_ms[dom] / 1e3) / 1e9, 1),
                                       "peak_gbs": peaks.get("hbm_gbs")},
                          "measured_ffma_peak": load_ffma_peak(),

@@ -202,7 +202,7 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
  *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
  *              forwards accept any N.
- *   tunables   NULL or ntunables (<= 11) ints {Q output channels per CTA,
+ *   tunables   NULL or ntunables (<= 12) ints {Q output channels per CTA,
  *              P pixels per lane, CC channels per stage, NS stages, warps per
  *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off),
  *              mbarrier pipeline (> 0 = on: warps drift up to NS-2 chunks
@@ -216,7 +216,10 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              same number of nonzeros — load balance under skewed per-row
  *              sparsity: 0 = when the heaviest group of
  *              consecutive rows exceeds the mean by > 5%, > 0 always, < 0
- *              never; results are bitwise identical either way)};
+ *              never; results are bitwise identical either way), sws (row
+ *              stride of the staged input in words: <= 0 = the bank-conflict
+ *              model's pick; larger strides spread a warp's lanes over the
+ *              32 shared-memory banks)};
  *              <= 0 entries take the defaults.
  * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
  * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE

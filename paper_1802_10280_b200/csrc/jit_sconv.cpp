@@ -104,46 +104,101 @@ int cdiv(int a, int b) { return (a + b - 1) / b; }
 constexpr int kMaxK = 11;  // largest filter with a specialised form (AlexNet conv1)
 
 // ---------------------------------------------------------------- geometry
+// Stacked staging layout: images one above the other, separated by `pad` shared zero rows, row
+// stride SWs >= W + 2*pad (extra columns are zeros too); output pixel g = (n*E + oh)*F + ow has
+// its window origin at pos(g) = (n*(H+pad) + oh*S)*SWs + ow*S and reads tap (kh, kw) at
+// pos(g) + kh*SWs + kw — the stretched offset f(0, kh, kw) of P:428 with the stacked row stride.
+int64_t stacked_pos(const JitPlan& p, int sws, int64_t g) {
+  const int64_t EF = int64_t(p.E) * p.F, n = g / EF, r = g % EF;
+  return (n * (p.H + p.pad) + (r / p.F) * p.S) * sws + (r % p.F) * p.S;
+}
+
+// Shared-memory wavefronts per warp-wide LDS (1 = conflict-free) of the lane -> pixel mapping
+// (warp w, slot j, lane l -> pixel g0 + (w*P + j)*32 + l) for row stride sws: the mean over the
+// first tiles of the n_hint-image grid of the largest number of lanes on one bank.
+double lds_wavefronts(const JitPlan& p, int sws, int n_hint) {
+  const int64_t EF = int64_t(p.E) * p.F, total = int64_t(std::max(1, n_hint)) * EF;
+  const int64_t tiles = std::min<int64_t>((total + p.T - 1) / p.T, 12);
+  double sum = 0;
+  int64_t groups = 0;
+  for (int64_t t = 0; t < tiles; ++t)
+    for (int grp = 0; grp < p.T / 32; ++grp) {
+      int cnt[32] = {};
+      int mx = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int64_t g = std::min(total - 1, t * p.T + grp * 32 + l);
+        mx = std::max(mx, ++cnt[stacked_pos(p, sws, g) & 31]);
+      }
+      sum += mx;
+      ++groups;
+    }
+  return groups ? sum / groups : 1.0;
+}
+
 void plan_geometry(JitPlan& p, int /*n_hint*/) {
-  // Dense pixel mapping: a CTA owns T consecutive output pixels g = (n*E + oh)*F + ow (no
-  // idle lanes); the input is staged in the stacked layout (images one above the other,
-  // separated by `pad` shared zero rows, row stride SWs = W + 2*pad), where pixel g sits at
-  // pos(g) = (n*(H+pad) + oh)*SWs + ow and reads tap (kh, kw) at pos(g) + kh*SWs + kw.
   const int T = p.warps * 32 * p.P;
   const int EF = p.E * p.F;
   p.mos = 1;
   p.T = T;
   // Staging vector width: V input words per cp.async when an input row is a whole number of
-  // V-word (16 / 8 byte) chunks (W % V == 0): every chunk of the stacked window is then either
-  // all data or all padding, and with a row stride SWs that is a multiple of V and a per-CTA
-  // shift of the buffer (bo, below) the data chunks are aligned in global AND shared memory.
+  // V-word (16 / 8 byte) chunks (W % V == 0); with a row stride that is a multiple of V and a
+  // per-CTA shift of the buffer (bo, gen_ptx) the data chunks are aligned in global AND shared
+  // memory.  Only data chunks are copied: the padding words of the stage buffers are zeroed once
+  // per CTA (they are the same positions for every channel and chunk).
   if (p.vec <= 0) p.V = p.W % 4 == 0 ? 4 : p.W % 2 == 0 ? 2 : 1;
   else p.V = (p.vec >= 4 && p.W % 4 == 0) ? 4 : (p.vec >= 2 && p.W % 2 == 0) ? 2 : 1;
-  p.SWs = (p.W + 2 * p.pad + p.V - 1) / p.V * p.V;
-  auto pos = [&](int64_t g) {
-    const int64_t n = g / EF, r = g % EF;
-    return (n * (p.H + p.pad) + (r / p.F) * p.S) * p.SWs + (r % p.F) * p.S;
-  };
+  const int base = (p.W + 2 * p.pad + p.V - 1) / p.V * p.V;
+  p.SWs = p.sws > 0 ? std::max(base, (p.sws + p.V - 1) / p.V * p.V) : base;
   int64_t span = 0;  // max pos(g0 + T - 1) - pos(g0); periodic in g0 with period EF
-  for (int64_t g0 = 0; g0 < EF; ++g0) span = std::max(span, pos(g0 + T - 1) - pos(g0));
+  for (int64_t g0 = 0; g0 < EF; ++g0)
+    span = std::max(span, stacked_pos(p, p.SWs, g0 + T - 1) - stacked_pos(p, p.SWs, g0));
   p.L = int(span + int64_t(p.K - 1) * (p.SWs + 1) + 1);
   p.Lv = cdiv(p.L + p.V - 1, p.V);  // V-word chunks per channel (the window shifted by bo < V)
   p.Ls = (p.Lv * p.V + 3) & ~3;
   p.nmg = cdiv(p.M, p.Q);
   p.nch = cdiv(p.C, p.CC);
-  p.KS = cdiv(p.Lv, p.warps * 32);
+  p.cpr = p.W / p.V;                                  // data chunks per input row
+  p.rows_win = (p.Lv * p.V + p.SWs - 1) / p.SWs + 1;  // stacked rows the window can touch
+  p.KS = cdiv(p.rows_win * p.cpr, p.warps * 32);     // data-chunk slots per thread
   p.smem_bytes = p.NS * p.CC * p.Ls * 4 + (p.mb ? 128 : 0);
 }
 
 // Geometry with the channel chunk halved until the stage ring fits shared memory (strided
 // layers stage S*S times more input per output pixel).
-bool plan_fit(JitPlan& p, int n_hint) {
+bool plan_fit_sws(JitPlan& p, int n_hint) {
   for (;;) {
     plan_geometry(p, n_hint);
     if (p.smem_bytes <= 227 * 1024 / p.minb) return true;
     if (p.CC == 1) return false;
     p.CC = (p.CC + 1) / 2;
   }
+}
+
+// Row stride by the bank-conflict model: a warp's 32 pixels wrap across row ends of the stacked
+// layout, and with SWs = W + 2*pad two of them land 32 words apart (2-way conflicts on every LDS,
+// ncu r01z/r02b).  Among SWs = base .. base + 48 (multiples of V) take the fewest modelled
+// wavefronts (ties: the smaller stride) that fits shared memory at the requested channel chunk;
+// if none fits, the base stride with the chunk halved as needed.
+bool plan_fit(JitPlan& p, int n_hint) {
+  if (p.sws > 0) return plan_fit_sws(p, n_hint);
+  JitPlan t = p;
+  plan_geometry(t, n_hint);
+  const int base = t.SWs;
+  std::vector<std::pair<double, int>> cands;
+  for (int sws = base; sws <= base + 48; sws += t.V)
+    cands.emplace_back(std::round(lds_wavefronts(t, sws, n_hint) * 100.0) / 100.0, sws);
+  std::sort(cands.begin(), cands.end());
+  for (const auto& c : cands) {
+    JitPlan q = p;
+    q.sws = c.second;
+    plan_geometry(q, n_hint);
+    if (q.smem_bytes <= 227 * 1024 / q.minb) {
+      q.sws = 0;  // keep the request "model" (plan equality compares SWs itself)
+      p = q;
+      return true;
+    }
+  }
+  return plan_fit_sws(p, n_hint);
 }
 
 // ---------------------------------------------------------------- PTX text
@@ -338,40 +393,64 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("shl.b32 %%r34, %%r34, 2;");
     o("add.u32 %%r%d, %%r34, %%r6;", 40 + j);
   }
-  // staging slots: k < KS (V-word chunk i = tid + k*NT of the window); regs: rd(32+k) src ptr,
-  // r(64+k) dst, r(64+KS+k) size (4V bytes, 0 = zero-fill: the virtual padding R#9), p(16+k) i < Lv
+  // Data-chunk staging slots k < KS: chunk d = tid + k*NT of the window's rows x (W/V) chunks;
+  // d -> stacked row R = R_lo + d / cpr, chunk c = d % cpr, buffer word R*SWs + pad + c*V - q0 + bo.
+  // Valid (predicate p(16+k)) iff R is an image row of an image < N and the V words lie inside the
+  // buffer; only valid chunks are ever copied (the padding words were zeroed once).  regs: rd(32+k)
+  // source pointer, r(64+k) buffer byte offset.
+  o("sub.s32 %%r37, %%r5, %%r10;");                   // q0 - bo (>= -3)
+  o("add.s32 %%r38, %%r37, %d;", p.SWs);
+  o("div.s32 %%r38, %%r38, %d;", p.SWs);
+  o("sub.s32 %%r38, %%r38, 1;");                      // R_lo = floor((q0 - bo) / SWs)
   for (int k = 0; k < p.KS; ++k) {
-    const int rs = 64 + k, rz = 64 + p.KS + k, t0 = 64 + 2 * p.KS;  // t0.. scratch
-    o("add.u32 %%r%d, %%r2, %d;", t0, k * NT);                // i
-    o("setp.lt.u32 %%p%d, %%r%d, %d;", 16 + k, t0, p.Lv);
-    o("shl.b32 %%r%d, %%r%d, %d;", rs, t0, p.V == 4 ? 4 : p.V == 2 ? 3 : 2);
-    o("add.u32 %%r%d, %%r%d, %%r6;", rs, rs);                 // dst
-    if (p.V > 1) o("shl.b32 %%r%d, %%r%d, %d;", t0, t0, p.V == 4 ? 2 : 1);
-    o("add.u32 %%r%d, %%r%d, %%r5;", t0 + 1, t0);
-    o("sub.s32 %%r%d, %%r%d, %%r10;", t0 + 1, t0 + 1);        // flat (may be < 0 before image 0)
-    o("div.s32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, p.SWs);    // R'
-    o("mul.lo.s32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 2, p.SWs);
-    o("sub.s32 %%r%d, %%r%d, %%r%d;", t0 + 3, t0 + 1, t0 + 3);  // X'
-    o("sub.s32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 2, p.pad);    // rr
-    o("sub.s32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 3, p.pad);    // x
-    o("setp.ge.s32 %%p0, %%r%d, 0;", t0 + 1);
-    o("setp.ge.and.s32 %%p0, %%r%d, 0, %%p0;", t0 + 2);
+    const int rs = 64 + k, t0 = 64 + 2 * p.KS;  // t0.. scratch
+    o("add.u32 %%r%d, %%r2, %d;", t0, k * NT);                 // d
+    o("setp.lt.u32 %%p0, %%r%d, %d;", t0, p.rows_win * p.cpr);
+    o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, p.cpr);         // row in window
+    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, p.cpr);
+    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 2, t0, t0 + 2);     // c
+    o("add.s32 %%r%d, %%r%d, %%r38;", t0 + 1, t0 + 1);         // R
+    o("mul.lo.s32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 1, p.SWs);
+    o("mad.lo.s32 %%r%d, %%r%d, %d, %%r%d;", t0 + 3, t0 + 2, p.V, t0 + 3);
+    o("add.s32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 3, p.pad);
+    o("sub.s32 %%r%d, %%r%d, %%r37;", t0 + 3, t0 + 3);         // buffer word
     o("setp.ge.and.s32 %%p0, %%r%d, 0, %%p0;", t0 + 3);
-    o("max.s32 %%r%d, %%r%d, 0;", t0 + 2, t0 + 2);
-    o("max.s32 %%r%d, %%r%d, 0;", t0 + 3, t0 + 3);
-    o("div.u32 %%r%d, %%r%d, %d;", t0 + 4, t0 + 2, hp);       // n
+    o("setp.le.and.s32 %%p0, %%r%d, %d, %%p0;", t0 + 3, p.Lv * p.V - p.V);
+    o("sub.s32 %%r%d, %%r%d, %d;", t0 + 1, t0 + 1, p.pad);     // rr
+    o("setp.ge.and.s32 %%p0, %%r%d, 0, %%p0;", t0 + 1);
+    o("max.s32 %%r%d, %%r%d, 0;", t0 + 1, t0 + 1);
+    o("div.u32 %%r%d, %%r%d, %d;", t0 + 4, t0 + 1, hp);        // n
     o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 5, t0 + 4, hp);
-    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 5, t0 + 2, t0 + 5);  // y
+    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 5, t0 + 1, t0 + 5); // y
     o("setp.lt.and.u32 %%p0, %%r%d, %d, %%p0;", t0 + 5, p.H);
-    o("setp.lt.and.u32 %%p0, %%r%d, %d, %%p0;", t0 + 3, p.W);
     o("setp.lt.and.u32 %%p0, %%r%d, %%r1, %%p0;", t0 + 4);
+    o("selp.b32 %%r%d, 1, 0, %%p0;", 64 + p.KS + k);            // slot valid (kept as a register)
+    o("max.s32 %%r%d, %%r%d, 0;", t0 + 3, t0 + 3);
+    o("shl.b32 %%r%d, %%r%d, 2;", rs, t0 + 3);
+    o("add.u32 %%r%d, %%r%d, %%r6;", rs, rs);                  // dst
     o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 4, t0 + 4, p.C * HW);
     o("mad.lo.u32 %%r%d, %%r%d, %d, %%r%d;", t0 + 4, t0 + 5, p.W, t0 + 4);
-    o("add.u32 %%r%d, %%r%d, %%r%d;", t0 + 4, t0 + 4, t0 + 3);  // src element (x = 0 mod V)
+    o("mad.lo.u32 %%r%d, %%r%d, %d, %%r%d;", t0 + 4, t0 + 2, p.V, t0 + 4);  // src element
     o("selp.u32 %%r%d, %%r%d, 0, %%p0;", t0 + 4, t0 + 4);
-    o("selp.u32 %%r%d, %d, 0, %%p0;", rz, 4 * p.V);
     o("mul.wide.u32 %%rd%d, %%r%d, 4;", 32 + k, t0 + 4);
     o("add.s64 %%rd%d, %%rd%d, %%rd0;", 32 + k, 32 + k);
+    o("setp.ne.u32 %%p%d, %%r%d, 0;", 16 + k, 64 + p.KS + k);
+  }
+  // the padding words of every stage buffer: zero once (16-byte stores), before any copy lands
+  {
+    const int words = p.NS * p.CC * p.Ls;  // multiple of 4
+    o("shl.b32 %%r39, %%r2, 4;");
+    o("add.u32 %%r39, %%r39, %%r6;");
+    o("mov.b32 %%r23, 0;");
+    for (int w0 = 0; w0 < words; w0 += 4 * NT) {
+      if (w0 + 4 * NT > words) {
+        o("setp.lt.u32 %%p2, %%r2, %d;", (words - w0) / 4);
+        o("@%%p2 st.shared.v4.b32 [%%r39+%d], {%%r23, %%r23, %%r23, %%r23};", w0 * 4);
+      } else {
+        o("st.shared.v4.b32 [%%r39+%d], {%%r23, %%r23, %%r23, %%r23};", w0 * 4);
+      }
+    }
+    o("bar.sync 0;");
   }
   // stage(chunk register rc, buffer byte offset register rb): r11 = chunk, r12 = buffer offset
   // Per (channel, slot) one cp.async; the channel offset and the stage offset are immediates
@@ -390,18 +469,13 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     for (int cc = 0; cc < p.CC; ++cc) {
       if (ragged_c) o("setp.gt.s32 %%p1, %%r13, %d;", cc);
       for (int k = 0; k < p.KS; ++k) {
-        const bool ragged_k = (k + 1) * NT > p.Lv;
-        std::string pred;
-        if (ragged_c && ragged_k) {
+        std::string pred = "@%p" + std::to_string(16 + k) + " ";
+        if (ragged_c) {
           o("and.pred %%p2, %%p1, %%p%d;", 16 + k);
           pred = "@%p2 ";
-        } else if (ragged_c) {
-          pred = "@%p1 ";
-        } else if (ragged_k) {
-          pred = "@%p" + std::to_string(16 + k) + " ";
         }
-        o("%scp.async.%s.shared.global [%%r%d+%d], [%%rd%d+%d], %d, %%r%d;", pred.c_str(), p.V == 4 ? "cg" : "ca",
-          64 + 2 * p.KS + k, cc * p.Ls * 4, 32 + p.KS + P + k, cc * HW * 4, 4 * p.V, 64 + p.KS + k);
+        o("%scp.async.%s.shared.global [%%r%d+%d], [%%rd%d+%d], %d;", pred.c_str(), p.V == 4 ? "cg" : "ca",
+          64 + 2 * p.KS + k, cc * p.Ls * 4, 32 + p.KS + P + k, cc * HW * 4, 4 * p.V);
       }
     }
   };

@@ -156,6 +156,10 @@ def workload(name: str) -> Workload:
                         [l for l in googlenet_full() if l.kind == "conv" and l.K == 1])
     if name == "resnet50":
         return Workload("resnet50", "resnet50", [l for l in resnet50_full() if l.sparse])
+    if name == "alexnet_convs":  # NEXT-2 whole conv stack: conv1 dense (unpruned) + conv2-5 sparse
+        return Workload("alexnet_convs", "alexnet", conv_layers(alexnet_full()))
+    if name == "resnet50_convs":  # NEXT-2 whole conv stack: 53 convs, the 16 3x3 sparse, the rest dense
+        return Workload("resnet50_convs", "resnet50", conv_layers(resnet50_full()))
     if name == "alexnet_conv1":  # NEXT-3: the 11x11 / stride-4 first layer on the sparse path (80%, R#14)
         c1 = alexnet_full()[0]
         return Workload("alexnet_conv1", "alexnet", [Layer(c1.name, c1.C, c1.H, c1.W, c1.M, c1.K, c1.stride, c1.pad,
