@@ -346,6 +346,16 @@ def cpu_oracle_timed(wl, args, seconds, max_images):
     return n, el, oracle.num_threads()
 
 
+def cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def sm_peak_tflops(torch, device, sm_max_mhz):
     props = torch.cuda.get_device_properties(device)
     # FP32 FFMA: 128 lanes/SM x 2 flop x clock (B200_PROFILING / blackwell guide unit counts)
@@ -585,7 +595,13 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         n, el, cores = cpu_oracle_timed(wl, args, args.cpu_seconds, B)
         line["cpu_baseline"] = {"value": n / el, "unit": "images/s", "cores": cores, "kind": "oracle",
-                                "sample": "%d image(s) x %d layers, fp64 oracle (OpenMP over (n,m))" % (n, len(runs))}
+                                "sample": "%d image(s) x %d layers, fp64 oracle (OpenMP over (n,m))" % (n, len(runs)),
+                                "cpu_model": cpu_model()}
+        import oracle
+        oracle.set_threads(1)  # per-core rate: one image through the stack on one thread
+        n1, el1, _ = cpu_oracle_timed(wl, args, max(2.0, args.cpu_seconds / 4), 1)
+        oracle.set_threads(cores)
+        line["cpu_baseline"]["one_thread"] = {"value": n1 / el1, "unit": "images/s", "sample": "%d image(s)" % n1}
     if rank == 0:
         s = json.dumps(line)
         print(s, flush=True)

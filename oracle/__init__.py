@@ -51,6 +51,8 @@ def lib():
             L.oracle_layout_f.argtypes = [cl, cl, cl, cl, cl]
             L.oracle_layout_f.restype = cl
             L.oracle_num_threads.restype = ci
+            L.oracle_set_threads.argtypes = [ci]
+            L.oracle_set_threads.restype = None
             L.oracle_csr_stretch.argtypes = [f32p, ci, ci, ci, ci, ci, ci, ci, i32p, i32p, f32p, cl,
                                              ctypes.POINTER(cl)]
             L.oracle_csr_stretch.restype = ci
@@ -83,6 +85,11 @@ def layout_f(c: int, y: int, x: int, Hin: int, Win: int) -> int:
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's loops (timing only; results do not depend on it)."""
+    lib().oracle_set_threads(int(n))
 
 
 def csr_stretch(w: np.ndarray, H: int, W: int, stride: int, pad: int):

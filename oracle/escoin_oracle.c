@@ -46,6 +46,11 @@ int64_t oracle_layout_f(int64_t c, int64_t y, int64_t x, int64_t Hin, int64_t Wi
   return (c * Hin + y) * Win + x;
 }
 
+/* Thread count of the parallel loops (timing only: the per-output arithmetic does not depend on it). */
+void oracle_set_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

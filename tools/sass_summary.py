@@ -1,8 +1,10 @@
 """Aggregate an ncu `--page source --csv --print-source sass` export by SASS opcode.
 
-usage: python tools/sass_summary.py SOURCE.csv > summary.txt
-Prints, per kernel section, executed warp-instructions per opcode (share of total) and the
-columns found, so a multi-MB per-instruction export becomes a few lines (gpurun_out is capped).
+usage: python tools/sass_summary.py SOURCE.csv [kernel-substring] > summary.txt
+Only the sections of kernels whose name contains the substring (default escoin_jit_sconv) are
+counted.  Prints executed warp-instructions per opcode (share of total) with the warp-stall
+samples attributed to that opcode split by reason, then the 12 instructions with the most stall
+samples — so a multi-MB per-instruction export becomes a few dozen lines (gpurun_out is capped).
 """
 import collections
 import csv
@@ -10,42 +12,54 @@ import re
 import sys
 
 
-def main(path):
-    rows = list(csv.reader(open(path, errors="replace")))
-    hdr_i = next(i for i, r in enumerate(rows) if any("Source" == c.strip() for c in r))
-    hdr = [c.strip() for c in rows[hdr_i]]
-    src = hdr.index("Source")
-    cand = [i for i, c in enumerate(hdr) if re.search(r"Instructions Executed|inst_executed", c, re.I)
-            and "Predicated" not in c]
-    ex = cand[0] if cand else None
-    stall_cols = [i for i, c in enumerate(hdr) if "Sampling" in c or "stall" in c.lower()]
-    print("columns:", hdr)
+def num(x):
+    try:
+        return float(x.replace(",", "") or 0)
+    except ValueError:
+        return 0.0
+
+
+def main(path, want="escoin_jit_sconv"):
     agg = collections.Counter()
-    samp = collections.Counter()
-    tot = 0.0
-    for r in rows[hdr_i + 1:]:
-        if len(r) <= src or ex is None:
+    stall = collections.defaultdict(collections.Counter)
+    top = []
+    hdr = None
+    keep = False
+    kernels = 0
+    for r in csv.reader(open(path, errors="replace")):
+        if r and r[0] == "Kernel Name":
+            keep = want in (r[1] if len(r) > 1 else "")
+            kernels += keep
+            hdr = None
+            continue
+        if r and r[0] == "Address":
+            hdr = r
+            src, ex = r.index("Source"), r.index("Instructions Executed")
+            scols = [(i, c) for i, c in enumerate(r) if c.startswith("stall_") and "Not Issued" not in c]
+            continue
+        if not keep or hdr is None or len(r) != len(hdr):
             continue
         s = r[src].strip()
         m = re.match(r"^(@!?U?P\w+\s+)?([A-Z0-9_]+)", s)
         if not m:
             continue
         op = m.group(2)
-        try:
-            v = float(r[ex].replace(",", "") or 0)
-        except ValueError:
-            continue
-        agg[op] += v
-        tot += v
-        for i in stall_cols[:1]:
-            try:
-                samp[op] += float(r[i].replace(",", "") or 0)
-            except ValueError:
-                pass
-    print("total executed warp instructions: %.0f (column %s)" % (tot, hdr[ex] if ex is not None else None))
-    for op, v in agg.most_common(25):
-        print("%-12s %14.0f %6.2f%%  samples %8.0f" % (op, v, 100.0 * v / max(tot, 1), samp[op]))
+        agg[op] += num(r[ex])
+        tot_s = 0.0
+        for i, c in scols:
+            v = num(r[i])
+            stall[op][c[6:]] += v
+            tot_s += v
+        top.append((tot_s, s[:60], {c[6:]: num(r[i]) for i, c in scols if num(r[i]) > 0}))
+    tot = sum(agg.values())
+    print("kernels: %d  executed warp instructions: %.0f" % (kernels, tot))
+    for op, v in agg.most_common(18):
+        st = ", ".join("%s %d" % (k, n) for k, n in stall[op].most_common(3) if n > 0)
+        print("%-10s %13.0f %6.2f%%   stalls: %s" % (op, v, 100.0 * v / max(tot, 1), st))
+    print("instructions with the most stall samples:")
+    for t, s, d in sorted(top, key=lambda x: -x[0])[:12]:
+        print("  %7d  %-60s %s" % (t, s, ", ".join("%s %d" % kv for kv in sorted(d.items(), key=lambda x: -x[1])[:3])))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(*sys.argv[1:])
