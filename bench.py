@@ -54,7 +54,7 @@ WL_NAMES = {"alexnet": "pruned AlexNet conv2-conv5 (4 sparse CONV layers)",
             "tiny": "tiny conv layer N=1 C=16 14x14 M=32 3x3"}
 # escoin_csr_jit tunings compiled per layer (Q,P,CC,NS,warps,CTAs/SM; 0 = the library's model pick);
 # escoin_csr_autotune_ex keeps the fastest under the bench's flushed-L2 conditions
-DEFAULT_JIT_TUNINGS = "0;32,1,0,0,24,1;32,1,0,0,16,2;64,1,0,0,16,1;32,1,16,3,24,1"
+DEFAULT_JIT_TUNINGS = "0;32,1,0,0,24,1;32,1,0,0,16,2;32,1,16,3,24,1;32,1,0,0,32,1"
 METRIC = "sparse-conv images/s (whole stack of sparse layers, global batch 128)"
 
 

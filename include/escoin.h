@@ -217,9 +217,9 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              sparsity: 0 = when the heaviest group of
  *              consecutive rows exceeds the mean by > 5%, > 0 always, < 0
  *              never; results are bitwise identical either way), sws (row
- *              stride of the staged input in words: <= 0 = the bank-conflict
- *              model's pick; larger strides spread a warp's lanes over the
- *              32 shared-memory banks)};
+ *              stride of the staged input in words: 0 = W + 2*pad, < 0 =
+ *              the bank-conflict model's pick (larger strides spread a
+ *              warp's lanes over the 32 shared-memory banks), > 0 = this)};
  *              <= 0 entries take the defaults.
  * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
  * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE

@@ -174,13 +174,15 @@ bool plan_fit_sws(JitPlan& p, int n_hint) {
   }
 }
 
-// Row stride by the bank-conflict model: a warp's 32 pixels wrap across row ends of the stacked
-// layout, and with SWs = W + 2*pad two of them land 32 words apart (2-way conflicts on every LDS,
-// ncu r01z/r02b).  Among SWs = base .. base + 48 (multiples of V) take the fewest modelled
-// wavefronts (ties: the smaller stride) that fits shared memory at the requested channel chunk;
-// if none fits, the base stride with the chunk halved as needed.
+// Row stride: the base W + 2*pad (rounded to V) unless requested.  sws < 0 asks for the
+// bank-conflict model: a warp's 32 pixels wrap across row ends of the stacked layout, and with the
+// base stride two of them land 32 words apart (2-way conflicts on most LDS, ncu r01z/r02b); among
+// SWs = base .. base + 48 (multiples of V) take the fewest modelled wavefronts (ties: the smaller
+// stride) that fits shared memory at the requested channel chunk.  Measured (r02f A/B): -4% time on
+// ResNet res3 at 24 warps, +4% on res2 (the larger stage ring), neutral on res4/res5 — so it is an
+// autotune candidate, not the default.
 bool plan_fit(JitPlan& p, int n_hint) {
-  if (p.sws > 0) return plan_fit_sws(p, n_hint);
+  if (p.sws >= 0) return plan_fit_sws(p, n_hint);
   JitPlan t = p;
   plan_geometry(t, n_hint);
   const int base = t.SWs;
@@ -193,12 +195,15 @@ bool plan_fit(JitPlan& p, int n_hint) {
     q.sws = c.second;
     plan_geometry(q, n_hint);
     if (q.smem_bytes <= 227 * 1024 / q.minb) {
-      q.sws = 0;  // keep the request "model" (plan equality compares SWs itself)
+      q.sws = -1;  // keep the request "model" (plan equality compares SWs itself)
       p = q;
       return true;
     }
   }
-  return plan_fit_sws(p, n_hint);
+  p.sws = 0;
+  if (!plan_fit_sws(p, n_hint)) return false;
+  p.sws = -1;
+  return true;
 }
 
 // ---------------------------------------------------------------- PTX text

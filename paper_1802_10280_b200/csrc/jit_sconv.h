@@ -19,7 +19,7 @@ struct JitPlan {
   int pf = 0;     // instruction prefetch pass: 0 = default (on), < 0 = off
   int mb = 0;     // > 0: mbarrier pipeline (warps drift up to NS-2 chunks) instead of a CTA barrier per chunk
   int reorder = 0;  // output-channel grouping: 0 = balance groups by nonzeros if skewed, > 0 always, < 0 never
-  int sws = 0;    // staged row stride request (<= 0: the bank-conflict model's pick, plan_fit)
+  int sws = 0;    // staged row stride request (0: W + 2*pad rounded to V; < 0: bank-conflict model; > 0: this)
   int vec = 0;    // staging vector width request (<= 0: widest the input row allows; 1 = 4-byte copies)
   int units = 0;  // separately compiled modules the m-groups are split into (<= 0: by nnz, jit_build)
   // layer
