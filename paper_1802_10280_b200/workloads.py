@@ -126,6 +126,11 @@ def resnet50_full(v15: bool = False) -> List[Layer]:
     return L
 
 
+def _sparse(l: Layer) -> Layer:
+    """The same layer marked as pruned (workloads that benchmark a normally-dense layer group)."""
+    return Layer(l.name, l.C, l.H, l.W, l.M, l.K, l.stride, l.pad, l.groups, sparse=True, kind=l.kind)
+
+
 def conv_layers(layers: List[Layer]) -> List[Layer]:
     return [l for l in layers if l.kind == "conv"]
 
@@ -151,9 +156,9 @@ def workload(name: str) -> Workload:
         return Workload("alexnet", "alexnet", [l for l in alexnet_full() if l.sparse])
     if name == "googlenet":
         return Workload("googlenet", "googlenet", [l for l in googlenet_full() if l.sparse])
-    if name == "googlenet_1x1":
+    if name == "googlenet_1x1":  # R#19: the 37 1x1 layers benchmarked as their own pruned group
         return Workload("googlenet_1x1", "googlenet",
-                        [l for l in googlenet_full() if l.kind == "conv" and l.K == 1])
+                        [_sparse(l) for l in googlenet_full() if l.kind == "conv" and l.K == 1])
     if name == "resnet50":
         return Workload("resnet50", "resnet50", [l for l in resnet50_full() if l.sparse])
     if name == "alexnet_convs":  # NEXT-2 whole conv stack: conv1 dense (unpruned) + conv2-5 sparse
@@ -161,9 +166,7 @@ def workload(name: str) -> Workload:
     if name == "resnet50_convs":  # NEXT-2 whole conv stack: 53 convs, the 16 3x3 sparse, the rest dense
         return Workload("resnet50_convs", "resnet50", conv_layers(resnet50_full()))
     if name == "alexnet_conv1":  # NEXT-3: the 11x11 / stride-4 first layer on the sparse path (80%, R#14)
-        c1 = alexnet_full()[0]
-        return Workload("alexnet_conv1", "alexnet", [Layer(c1.name, c1.C, c1.H, c1.W, c1.M, c1.K, c1.stride, c1.pad,
-                                                           c1.groups, sparse=True)])
+        return Workload("alexnet_conv1", "alexnet", [_sparse(alexnet_full()[0])])
     if name == "resnet50_v15":  # NEXT-3: three of the 16 sparse 3x3 layers have stride 2
         return Workload("resnet50_v15", "resnet50_v15", [l for l in resnet50_full(v15=True) if l.sparse])
     raise KeyError(name)

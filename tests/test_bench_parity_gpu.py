@@ -34,7 +34,7 @@ def _setup(wl_name):
 
 
 @pytest.mark.parametrize("wl_name", ["alexnet", "resnet50", "googlenet", "googlenet_1x1", "resnet50_v15",
-                                     "alexnet_conv1"])
+                                     "alexnet_conv1", "alexnet_convs"])
 def test_bench_setup_every_output_vs_oracle(wl_name):
     W, runs = _setup(wl_name)
     tunings = [[int(v) for v in t.split(",")] if t.strip() not in ("", "0") else []
@@ -47,7 +47,7 @@ def test_bench_setup_every_output_vs_oracle(wl_name):
         torch.cuda.synchronize()
         out = r.out.cpu().numpy()
         label = r.csr.label()
-        w = inputs.layer_weights(W.net, L, 800)
+        w = inputs.layer_weights(W.net, L, 800 if L.sparse else 0)  # bench.setup's rule (R#25)
         b = inputs.bias(W.net, L.name, L.M)
         x = r.h_x.numpy()
         rp, ci, v = oracle.csr_stretch(w, L.H, L.W, L.stride, L.pad)
