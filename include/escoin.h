@@ -202,7 +202,7 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
  *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
  *              forwards accept any N.
- *   tunables   NULL or ntunables (<= 12) ints {Q output channels per CTA,
+ *   tunables   NULL or ntunables (<= 13) ints {Q output channels per CTA,
  *              P pixels per lane, CC channels per stage, NS stages, warps per
  *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off),
  *              mbarrier pipeline (> 0 = on: warps drift up to NS-2 chunks
@@ -219,7 +219,11 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              never; results are bitwise identical either way), sws (row
  *              stride of the staged input in words: 0 = W + 2*pad, < 0 =
  *              the bank-conflict model's pick (larger strides spread a
- *              warp's lanes over the 32 shared-memory banks), > 0 = this)};
+ *              warp's lanes over the 32 shared-memory banks), > 0 = this),
+ *              perm (> 0: lanes take the tile's pixels dealt by shared-
+ *              memory bank instead of consecutively — conflict-free window
+ *              loads — and the accumulators are transposed through shared
+ *              memory for coalesced stores; same bits)};
  *              <= 0 entries take the defaults.
  * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
  * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE

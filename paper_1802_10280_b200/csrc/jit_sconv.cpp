@@ -161,6 +161,14 @@ void plan_geometry(JitPlan& p, int /*n_hint*/) {
   p.rows_win = (p.Lv * p.V + p.SWs - 1) / p.SWs + 1;  // stacked rows the window can touch
   p.KS = cdiv(p.rows_win * p.cpr, p.warps * 32);     // data-chunk slots per thread
   p.smem_bytes = p.NS * p.CC * p.Ls * 4 + (p.mb ? 128 : 0);
+  // lane -> pixel deal (perm > 0): the bank pattern of a tile repeats every EF / gcd(T, EF) tiles
+  p.nphase = 0;
+  if (p.perm > 0) {
+    int a = T, b = EF;
+    while (b) { const int t = a % b; a = b; b = t; }
+    const int64_t nph = EF / a;
+    if (nph * T <= (int64_t(1) << 22) && T <= 65536) p.nphase = int(nph);
+  }
 }
 
 // Geometry with the channel chunk halved until the stage ring fits shared memory (strided
@@ -234,6 +242,30 @@ struct Nz {
   uint32_t bits;
 };
 
+// Lane -> pixel deal of the tiles (perm > 0), per tile phase ph (tile mod nphase): the T pixels of
+// the tile sorted by the shared-memory bank of their window origin (pos(g) mod 32; every tap adds
+// the same offset to all lanes, so the banks of any LDS are this pattern shifted) and dealt
+// round-robin to the T/32 (warp, slot) groups: a group receives at most one pixel per bank unless a
+// bank holds more than T/32 of the tile's pixels (row ends of the stacked layout make the
+// consecutive-pixel assignment 2-way conflicted, ncu r01z/r02b).  table[ph*T + s*32 + l] = pixel
+// offset in the tile of slot s = warp*P + j, lane l.
+std::vector<uint16_t> perm_table(const JitPlan& p) {
+  const int T = p.T, G = T / 32;
+  std::vector<uint16_t> tab(size_t(p.nphase) * T);
+  std::vector<int> idx(T);
+  std::vector<int> bank(T);
+  for (int ph = 0; ph < p.nphase; ++ph) {
+    const int64_t g0 = int64_t(ph) * T;
+    for (int i = 0; i < T; ++i) {
+      idx[i] = i;
+      bank[i] = int(stacked_pos(p, p.SWs, g0 + i) & 31);
+    }
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return bank[a] < bank[b]; });
+    for (int i = 0; i < T; ++i) tab[size_t(i % G) * 32 + i / G + size_t(ph) * T] = uint16_t(idx[i]);
+  }
+  return tab;
+}
+
 // Output-channel order of the m-groups (slot g*Q + q -> CSR row, -1 = empty slot).  Identity unless
 // p.reorder > 0, or p.reorder == 0 and the heaviest group of consecutive rows holds > 5% more
 // nonzeros than the mean (skewed per-row sparsity, "adaptively tile the output channel"):
@@ -291,6 +323,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   // nonzeros per (m-group, channel), ascending tap then row
   bool reordered = false;
   const std::vector<int> ord = row_order(p, rowptr, &reordered);
+  const bool permuted = p.perm > 0 && !reordered && p.nphase > 0;  // lane -> pixel deal (perm_table)
   std::vector<std::vector<Nz>> lists(size_t(ng) * p.C);
   for (int slot = g_lo * Q; slot < g_hi * Q; ++slot) {
     const int m = ord[slot];
@@ -318,12 +351,12 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   const std::string mgr = unit < 0 ? std::string("mgr") : "mgr" + std::to_string(unit);
   if (unit < 0) {
     o(".visible .entry escoin_jit_sconv(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
-      ".param .u32 p_relu, .param .u32 p_N)");
+      ".param .u32 p_relu, .param .u32 p_N, .param .u64 p_perm)");
     o(".maxntid %d, 1, 1", NT);
     o(".minnctapersm %d", p.minb);
   } else {
     o(".visible .func escoin_unit_%d(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
-      ".param .u32 p_relu, .param .u32 p_N, .param .u32 p_gy)", unit);
+      ".param .u32 p_relu, .param .u32 p_N, .param .u32 p_gy, .param .u64 p_perm)", unit);
   }
   o("{");
   o(".reg .pred %%p<%d>;", 16 + 2 * p.KS + P);
@@ -332,6 +365,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o(".reg .f32 %%a<%d>;", Q * P);
   o(".reg .f32 %%x<%d>;", KK * P);
   o(".reg .f32 %%v<8>;");
+  o(".reg .b16 %%rs<2>;");
   // params, ids
   o("ld.param.u64 %%rd0, [p_in];");
   o("cvta.to.global.u64 %%rd0, %%rd0;");
@@ -340,6 +374,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("ld.param.u64 %%rd2, [p_bias];");
   o("ld.param.u32 %%r0, [p_relu];");
   o("ld.param.u32 %%r1, [p_N];");
+  o("ld.param.u64 %%rd11, [p_perm];");
   o("mov.u32 %%r2, %%tid.x;");
   // grid = (m-groups, pixel tiles): the m-groups of one tile are consecutive CTAs, so they run
   // together and read the tile's input from L2 instead of re-reading it from HBM
@@ -378,8 +413,26 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("mul.lo.u32 %%r9, %%r8, %d;", 32 * P);
   o("add.u32 %%r9, %%r9, %%r7;");
   o("add.u32 %%r9, %%r9, %%r28;");        // pixel g of j = 0 (j adds 32 j)
+  if (permuted) {
+    // lane -> pixel deal (perm_table): slot (warp*P + j, lane) of tile phase ph = tile mod nphase
+    // takes pixel g0 + perm[ph][(warp*P + j)*32 + lane]; r(56+j) = that offset
+    o("rem.u32 %%r54, %%r3, %d;", p.nphase);
+    o("mul.lo.u32 %%r55, %%r54, %d;", p.T);
+    o("mad.lo.u32 %%r55, %%r8, %d, %%r55;", 32 * P);
+    o("add.u32 %%r55, %%r55, %%r7;");
+    for (int j = 0; j < P; ++j) {
+      o("add.u32 %%r54, %%r55, %d;", 32 * j);
+      o("mul.wide.u32 %%rd12, %%r54, 2;");
+      o("add.s64 %%rd12, %%rd12, %%rd11;");
+      o("ld.global.nc.u16 %%rs0, [%%rd12];");
+      o("cvt.u32.u16 %%r%d, %%rs0;", 56 + j);
+    }
+  }
   for (int j = 0; j < P; ++j) {          // lane smem base of pixel j: smem + 4 (pos(g) - q0)
-    o("add.u32 %%r35, %%r9, %d;", 32 * j);
+    if (permuted)
+      o("add.u32 %%r35, %%r28, %%r%d;", 56 + j);
+    else
+      o("add.u32 %%r35, %%r9, %d;", 32 * j);
     o("min.u32 %%r35, %%r35, %%r29;");     // tail lanes read in range, never store
     o("div.u32 %%r30, %%r35, %d;", EF);
     o("mul.lo.u32 %%r31, %%r30, %d;", EF);
@@ -732,7 +785,12 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("sub.s32 %%r19, %d, %%r18;", p.M);           // rows left
     for (int j = 0; j < P; ++j) {
       const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j, t0 = 64 + 4 * p.KS + 8 * j;
-      o("add.u32 %%r%d, %%r9, %d;", t0, 32 * j);                // g
+      if (permuted) {  // stores in natural pixel order g0 + tid + j*NT (the accumulators go through smem)
+        o("add.u32 %%r%d, %%r28, %%r2;", t0);
+        o("add.u32 %%r%d, %%r%d, %d;", t0, t0, j * NT);
+      } else {
+        o("add.u32 %%r%d, %%r9, %d;", t0, 32 * j);              // g
+      }
       o("setp.le.u32 %%p%d, %%r%d, %%r29;", pv, t0);
       o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, EF);           // n
       o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, EF);
@@ -748,7 +806,60 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     // forms are separate straight-line blocks.  Row predicates only where a group can be partial
     // (M % Q != 0, last group); pixel predicates only matter in the tail CTA.
     const bool full_rows = p.M % Q == 0 || g_hi * Q <= p.M;
-    for (int relu = 1; relu >= 0; --relu) {
+    if (permuted) {
+      // Lanes hold dealt (non-consecutive) pixels: the accumulators are transposed through the
+      // (now idle) stage ring, QB channels at a time, and stored in natural pixel order — every
+      // warp store still writes 32 consecutive pixels of one channel (128 B).
+      const int QB = std::max(1, std::min(Q, p.NS * p.CC * p.Ls / p.T));
+      o("bar.sync 0;");                                 // every warp is done with the stage ring
+      for (int j = 0; j < P; ++j) {
+        o("shl.b32 %%r%d, %%r%d, 2;", 56 + j, 56 + j);
+        o("add.u32 %%r%d, %%r%d, %%r6;", 56 + j, 56 + j);  // smem byte address of this slot's pixel
+      }
+      o("shl.b32 %%r54, %%r2, 2;");
+      o("add.u32 %%r54, %%r54, %%r6;");                // natural pixel tid of the tile
+      for (int b0 = 0; b0 < Q; b0 += QB) {
+        const int qb = std::min(QB, Q - b0);
+        for (int q = b0; q < b0 + qb; ++q)
+          for (int j = 0; j < P; ++j)
+            o("st.shared.f32 [%%r%d+%d], %%a%d;", 56 + j, (q - b0) * p.T * 4, q * P + j);
+        o("bar.sync 0;");
+        for (int relu = 1; relu >= 0; --relu) {
+          if (relu) o("@!%%p7 bra.uni EPB%d_LIN;", b0);
+          else o("EPB%d_LIN:", b0);
+          for (int q = b0; q < b0 + qb; ++q) {
+            o("mov.f32 %%v0, 0f00000000;");
+            if (full_rows) {
+              o("@%%p6 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
+            } else {
+              o("setp.gt.s32 %%p8, %%r19, %d;", q);
+              o("and.pred %%p9, %%p8, %%p6;");
+              o("@%%p9 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
+            }
+            for (int j = 0; j < P; ++j) {
+              const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j;
+              o("ld.shared.f32 %%v1, [%%r54+%d];", ((q - b0) * p.T + j * NT) * 4);
+              o("add.rn.f32 %%v1, %%v1, %%v0;");
+              if (relu) {
+                o("setp.gt.f32 %%p10, %%v1, 0f00000000;");
+                o("selp.f32 %%v1, %%v1, 0f00000000, %%p10;");
+              }
+              if (full_rows) {
+                o("@%%p%d st.global.f32 [%%rd%d+%d], %%v1;", pv, rdo, q * EF * 4);
+              } else {
+                o("and.pred %%p11, %%p8, %%p%d;", pv);
+                o("@%%p11 st.global.f32 [%%rd%d+%d], %%v1;", rdo, q * EF * 4);
+              }
+            }
+          }
+          if (relu) o("bra.uni EPB%d_END;", b0);
+        }
+        o("EPB%d_END:", b0);
+        o("bar.sync 0;");
+      }
+      o("ret;");
+    }
+    for (int relu = 1; relu >= 0 && !permuted; --relu) {
       if (relu) o("@!%%p7 bra.uni EPI_LIN;");
       else o("EPI_LIN:");
       for (int q = 0; q < Q; ++q) {
@@ -793,10 +904,10 @@ std::string gen_entry(const JitPlan& p, const std::vector<std::pair<int, int>>& 
   o(".target sm_100a");
   o(".address_size 64");
   const char* sig = "(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, .param .u32 p_relu, "
-                    ".param .u32 p_N, .param .u32 p_gy)";
+                    ".param .u32 p_N, .param .u32 p_gy, .param .u64 p_perm)";
   for (size_t u = 0; u < ranges.size(); ++u) o(".extern .func escoin_unit_%d%s;", int(u), sig);
   o(".visible .entry escoin_jit_sconv(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
-    ".param .u32 p_relu, .param .u32 p_N)");
+    ".param .u32 p_relu, .param .u32 p_N, .param .u64 p_perm)");
   o(".maxntid %d, 1, 1", p.warps * 32);
   o(".minnctapersm %d", p.minb);
   o("{");
@@ -808,6 +919,7 @@ std::string gen_entry(const JitPlan& p, const std::vector<std::pair<int, int>>& 
   o("ld.param.u64 %%rd2, [p_bias];");
   o("ld.param.u32 %%r0, [p_relu];");
   o("ld.param.u32 %%r1, [p_N];");
+  o("ld.param.u64 %%rd3, [p_perm];");
   o("mov.u32 %%r2, %%ctaid.x;");
   for (size_t u = 0; u < ranges.size(); ++u) {
     o("setp.lt.u32 %%p0, %%r2, %d;", ranges[u].second);
@@ -824,13 +936,15 @@ std::string gen_entry(const JitPlan& p, const std::vector<std::pair<int, int>>& 
     o(".param .u32 a3;");
     o(".param .u32 a4;");
     o(".param .u32 a5;");
+    o(".param .u64 a6;");
     o("st.param.u64 [a0], %%rd0;");
     o("st.param.u64 [a1], %%rd1;");
     o("st.param.u64 [a2], %%rd2;");
     o("st.param.u32 [a3], %%r0;");
     o("st.param.u32 [a4], %%r1;");
     o("st.param.u32 [a5], %%r3;");
-    o("call.uni escoin_unit_%d, (a0, a1, a2, a3, a4, a5);", int(u));
+    o("st.param.u64 [a6], %%rd3;");
+    o("call.uni escoin_unit_%d, (a0, a1, a2, a3, a4, a5, a6);", int(u));
     o("}");
     o("ret;");
   }
@@ -1236,6 +1350,14 @@ int jit_build(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int3
     return -3;
   }
   jm.func = f;
+  if (p.perm > 0 && !jm.reordered && p.nphase > 0) {
+    const std::vector<uint16_t> tab = perm_table(p);
+    if (cudaMalloc(&jm.d_perm, tab.size() * 2) != cudaSuccess ||
+        cudaMemcpy(jm.d_perm, tab.data(), tab.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess) {
+      jit_free(jm);
+      return -3;
+    }
+  }
   d.getattr(&jm.regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f);
   d.getattr(&jm.local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, f);
   jm.compile_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1259,12 +1381,15 @@ std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t*
 std::string jit_label(const JitModule& jm) {
   const JitPlan& p = jm.plan;
   char b[160];
-  snprintf(b, sizeof b, "jit_q%d_p%d_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d_v%d%s", p.Q, p.P, p.CC, p.NS, p.warps,
-           p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V, jm.reordered ? "_ro" : "");
+  snprintf(b, sizeof b, "jit_q%d_p%d_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d_v%d%s%s", p.Q, p.P, p.CC, p.NS, p.warps,
+           p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V, jm.reordered ? "_ro" : "",
+           (p.perm > 0 && !jm.reordered && p.nphase > 0) ? "_dl" : "");
   return b;
 }
 
 void jit_free(JitModule& jm) {
+  if (jm.d_perm) cudaFree(jm.d_perm);
+  jm.d_perm = nullptr;
   if (jm.module && driver().ok) driver().unload(static_cast<CUmodule>(jm.module));
   jm.module = nullptr;
   jm.func = nullptr;
@@ -1283,7 +1408,8 @@ int jit_launch(const JitModule& jm, const float* in, float* out, const float* bi
   const void* a_in = in;
   void* a_out = out;
   const void* a_bias = bias;
-  void* args[] = {&a_in, &a_out, &a_bias, &relu_u, &n_u};
+  const void* a_perm = jm.d_perm;
+  void* args[] = {&a_in, &a_out, &a_bias, &relu_u, &n_u, &a_perm};
   const CUresult r = driver().launch(static_cast<CUfunction>(jm.func), unsigned(p.nmg), unsigned(tiles), 1,
                                      unsigned(p.warps * 32), 1, 1, unsigned(p.smem_bytes), (CUstream)s, args,
                                      nullptr);

@@ -376,3 +376,35 @@ def test_row_reordering_for_skewed_rows_bitwise(reorder):
     assert o0.tobytes() == o1r.tobytes()
     ref_lin, scale_lin = oracle_ref(w, x, b, 1, 1, False)
     check(o1, ref_lin, scale_lin, b)
+
+
+PERM_CASES = [  # N, C, H, W, M, K, stride, pad, tunables
+    (3, 12, 13, 13, 40, 3, 1, 1, dict(Q=16, warps=4)), (5, 9, 7, 7, 33, 3, 1, 1, dict(Q=8, warps=8, P=2)),
+    (2, 7, 14, 14, 24, 5, 1, 2, dict(Q=8, warps=4, minb=2)), (4, 6, 27, 27, 20, 5, 1, 2, dict(Q=16, warps=8)),
+    (2, 8, 15, 11, 17, 3, 2, 1, dict(Q=8, warps=4)), (3, 10, 13, 13, 48, 3, 1, 1, dict(Q=16, warps=4, units=3)),
+]
+
+
+@pytest.mark.parametrize("relu", [True, False])
+@pytest.mark.parametrize("case", PERM_CASES)
+def test_lane_pixel_deal_bitwise(case, relu):
+    # perm=1: lanes take the tile's pixels dealt by shared-memory bank; accumulators transposed through
+    # shared memory before the (coalesced) stores — same bits as every other kernel, ragged tails included
+    N, C, H, W, M, K, st, p, tun = case
+    rng = np.random.default_rng(abs(hash(case[:8])) % 2**32)
+    x = rng.random((N, C, H, W)).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.25] = 0.0
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    ref, scale = oracle_ref(w, x, b, st, p, relu)
+    csr = escoin.Csr.stretch(w, H, W, st, p).to_device(0)
+    csr.jit(n_hint=N, perm=1, reorder=-1, **tun)
+    assert "_dl" in csr.label()
+    out = fwd(csr, x, b, relu)
+    check(out, ref, scale, b)
+    csr.set_kernel(0)
+    assert out.tobytes() == fwd(csr, x, b, relu).tobytes()
+    for n0, n1 in [(1, N), (0, 1)]:  # other batch sizes (other tile phases / tails)
+        csr2 = escoin.Csr.stretch(w, H, W, st, p).to_device(0)
+        csr2.jit(n_hint=N, perm=1, reorder=-1, **tun)
+        assert fwd(csr2, x[n0:n1], b, relu).tobytes() == out[n0:n1].tobytes()
