@@ -615,15 +615,25 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("add.u32 %%r24, %%r23, %%r22;");
     o("sub.u32 %%r24, %%r24, 1;");
     o("div.u32 %%r24, %%r24, %%r22;");             // warps needed so the group's CTAs cover every chunk
+    o("mov.u32 %%r27, 0;");
     o("setp.ge.u32 %%p14, %%r8, %%r24;");
     o("@%%p14 bra.uni PF_DONE;");
     o("mad.lo.u32 %%r26, %%r8, %%r22, %%r3;");     // tile + warp * tiles
     o("rem.u32 %%r26, %%r26, %%r23;");
     o("add.u32 %%r26, %%r26, %%r20;");
+    // The block reads stage buffer (k - k_lo) mod NS; shift the lane bases so it reads buffer NS-1
+    // instead: that one holds only the zeros of the padding fill until the main loop's first
+    // refill (after a CTA barrier), so the pass never reads words the prologue's copies are writing.
+    o("sub.u32 %%r27, %%r26, %%r20;");
+    o("rem.u32 %%r27, %%r27, %d;", p.NS);
+    o("sub.u32 %%r27, %d, %%r27;", p.NS - 1);
+    o("mul.lo.u32 %%r27, %%r27, %d;", p.CC * p.Ls * 4);
+    for (int j = 0; j < P; ++j) o("add.u32 %%r%d, %%r%d, %%r27;", 40 + j, 40 + j);
     o("mad.lo.u32 %%r17, %%r4, %d, %%r26;", p.nch);
     o("%s", tp.c_str());
     o("brx.idx.uni %%r17, tp;");
     o("PF_DONE:");
+    for (int j = 0; j < P; ++j) o("sub.u32 %%r%d, %%r%d, %%r27;", 40 + j, 40 + j);
     o("setp.ne.u32 %%p12, %%r1, 0;");              // true from here on
     for (int q = 0; q < Q * P; ++q) o("mov.f32 %%a%d, 0f00000000;", q);
   }
@@ -969,8 +979,10 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   // +5% over 8 x 3), 3x3 and 1x1 with 8 x 3 (conv3 -14% with 4 x 4).
   if (p.CC <= 0) p.CC = K >= 5 ? 4 : 8;
   if (p.NS <= 1) p.NS = K >= 5 ? 4 : 3;
-  p.pf = p.pf < 0 ? 0 : 1;
   p.mb = p.mb > 0 ? 1 : 0;
+  // the instruction-prefetch pass reads the last stage buffer, free until the first CTA barrier of
+  // the main loop; the mbarrier pipeline has no such barrier, so it runs without the pass
+  p.pf = (p.pf < 0 || p.mb) ? 0 : 1;
   n_hint = std::max(1, n_hint);
   if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0) {
     // Shape choice by a small model (escoin_csr_autotune_ex measures the real choice among the

@@ -1,0 +1,9 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+TAG=r02i
+timeout 900 python -m pytest tests/test_jit_gpu.py -x -q > gpurun_out/${TAG}_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/${TAG}_tests.log
+L=res2a_branch2b,res3a_branch2b,res4a_branch2b,res5a_branch2b
+timeout 1500 python tools/ab.py resnet50 $L "32,1,0,0,24,1;32,1,0,0,24,1,0,0,0,0,-1,0,1;32,1,0,0,16,2;32,1,0,0,16,2,0,0,0,0,-1,0,1;32,1,16,3,24,1;32,1,16,3,24,1,0,0,0,0,-1,0,1;32,1,0,0,32,1;32,1,0,0,32,1,0,0,0,0,-1,0,1" 20 > gpurun_out/${TAG}_ab.jsonl 2> gpurun_out/${TAG}_ab.err
+timeout 900 python tools/ab.py alexnet all "32,1,0,0,32,1;32,1,0,0,32,1,0,0,0,0,-1,0,1;0;0,0,0,0,0,0,0,0,0,0,-1,0,1" 20 > gpurun_out/${TAG}_ab_alexnet.jsonl 2>> gpurun_out/${TAG}_ab.err
+timeout 900 python tools/ab.py googlenet inception_4a/5x5,inception_5a/3x3,inception_5a/5x5,inception_4e/3x3 "0;0,0,0,0,0,0,0,0,0,0,-1,0,1;32,1,0,0,8,2;32,1,0,0,8,2,0,0,0,0,-1,0,1;16,1,0,0,8,4" 20 > gpurun_out/${TAG}_ab_googlenet.jsonl 2>> gpurun_out/${TAG}_ab.err

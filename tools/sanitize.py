@@ -43,7 +43,8 @@ def main():
         b = torch.from_numpy((rng.random(M) * 0.2 - 0.1).astype(np.float32)).to(dev)
         ref = None
         tunings = [dict(), dict(mbarrier=1, NS=4), dict(vec=1), dict(Q=8, units=3), dict(Q=8, reorder=1),
-                   dict(Q=16, warps=4, minb=2, P=2)]
+                   dict(Q=16, warps=4, minb=2, P=2), dict(Q=8, perm=1, reorder=-1), dict(Q=8, P=2, warps=4, perm=1,
+                                                                                      reorder=-1), dict(sws=-1)]
         for tun in tunings:
             csr = escoin.Csr.stretch(w, H, W, st, pad).to_device(0)
             try:
