@@ -267,8 +267,8 @@ std::vector<uint16_t> perm_table(const JitPlan& p) {
 }
 
 // Output-channel order of the m-groups (slot g*Q + q -> CSR row, -1 = empty slot).  Identity unless
-// p.reorder > 0, or p.reorder == 0 and the heaviest group of consecutive rows holds > 5% more
-// nonzeros than the mean (skewed per-row sparsity, "adaptively tile the output channel"):
+// p.reorder > 0, or p.reorder == 0 and the densest group of consecutive rows holds > 5% more
+// nonzeros per row than the layer's mean (skewed per-row sparsity, "adaptively tile the output channel"):
 // then rows are dealt longest-first to the group with the fewest nonzeros so far (LPT), so every
 // group's CTAs do about the same work.  Only the grouping changes: each channel still accumulates
 // its own CSR row in ascending (c, kh, kw) order, so the output bits are identical.
@@ -284,8 +284,11 @@ std::vector<int> row_order(const JitPlan& p, const int32_t* rowptr, bool* reorde
     gn[m / Q] += rowptr[m + 1] - rowptr[m];
     tot += rowptr[m + 1] - rowptr[m];
   }
-  const int64_t mx = *std::max_element(gn.begin(), gn.end());
-  if (p.reorder == 0 && (tot == 0 || double(mx) * G <= 1.05 * double(tot))) return ord;
+  // imbalance = the densest group's nonzeros per row over the layer's mean (a partial last group
+  // has fewer rows, not less work per row)
+  double mx = 0.0;
+  for (int g = 0; g < G; ++g) mx = std::max(mx, double(gn[g]) / double(std::min(Q, p.M - g * Q)));
+  if (p.reorder == 0 && (tot == 0 || mx <= 1.05 * double(tot) / p.M)) return ord;
   std::vector<int> rows(p.M);
   for (int m = 0; m < p.M; ++m) rows[m] = m;
   std::stable_sort(rows.begin(), rows.end(), [&](int a, int b) {
