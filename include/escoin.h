@@ -202,7 +202,7 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
  *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
  *              forwards accept any N.
- *   tunables   NULL or ntunables (<= 13) ints {Q output channels per CTA,
+ *   tunables   NULL or ntunables (<= 14) ints {Q output channels per CTA,
  *              P pixels per lane, CC channels per stage, NS stages, warps per
  *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off),
  *              mbarrier pipeline (> 0 = on: warps drift up to NS-2 chunks
@@ -223,7 +223,11 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              perm (> 0: lanes take the tile's pixels dealt by shared-
  *              memory bank instead of consecutively — conflict-free window
  *              loads — and the accumulators are transposed through shared
- *              memory for coalesced stores; same bits)};
+ *              memory for coalesced stores; same bits), split (> 1: the
+ *              CTA's warps form that many independent sub-tiles, each with
+ *              its own stage ring and named barrier, all running the same
+ *              m-group's code — one sub-tile's barrier wait is covered by the
+ *              others' work)};
  *              <= 0 entries take the defaults.
  * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
  * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE

@@ -140,6 +140,10 @@ void plan_geometry(JitPlan& p, int /*n_hint*/) {
   const int EF = p.E * p.F;
   p.mos = 1;
   p.T = T;
+  // split > 1: the CTA's warps form `split` independent sub-tiles of T/split pixels (own stage
+  // ring, own named barrier) running the same m-group's code
+  p.sp = (p.split > 1 && !p.mb && p.perm <= 0 && p.warps % p.split == 0) ? p.split : 1;
+  const int Th = T / p.sp;
   // Staging vector width: V input words per cp.async when an input row is a whole number of
   // V-word (16 / 8 byte) chunks (W % V == 0); with a row stride that is a multiple of V and a
   // per-CTA shift of the buffer (bo, gen_ptx) the data chunks are aligned in global AND shared
@@ -149,9 +153,9 @@ void plan_geometry(JitPlan& p, int /*n_hint*/) {
   else p.V = (p.vec >= 4 && p.W % 4 == 0) ? 4 : (p.vec >= 2 && p.W % 2 == 0) ? 2 : 1;
   const int base = (p.W + 2 * p.pad + p.V - 1) / p.V * p.V;
   p.SWs = p.sws > 0 ? std::max(base, (p.sws + p.V - 1) / p.V * p.V) : base;
-  int64_t span = 0;  // max pos(g0 + T - 1) - pos(g0); periodic in g0 with period EF
+  int64_t span = 0;  // max pos(g0 + Th - 1) - pos(g0); periodic in g0 with period EF
   for (int64_t g0 = 0; g0 < EF; ++g0)
-    span = std::max(span, stacked_pos(p, p.SWs, g0 + T - 1) - stacked_pos(p, p.SWs, g0));
+    span = std::max(span, stacked_pos(p, p.SWs, g0 + Th - 1) - stacked_pos(p, p.SWs, g0));
   p.L = int(span + int64_t(p.K - 1) * (p.SWs + 1) + 1);
   p.Lv = cdiv(p.L + p.V - 1, p.V);  // V-word chunks per channel (the window shifted by bo < V)
   p.Ls = (p.Lv * p.V + 3) & ~3;
@@ -159,8 +163,8 @@ void plan_geometry(JitPlan& p, int /*n_hint*/) {
   p.nch = cdiv(p.C, p.CC);
   p.cpr = p.W / p.V;                                  // data chunks per input row
   p.rows_win = (p.Lv * p.V + p.SWs - 1) / p.SWs + 1;  // stacked rows the window can touch
-  p.KS = cdiv(p.rows_win * p.cpr, p.warps * 32);     // data-chunk slots per thread
-  p.smem_bytes = p.NS * p.CC * p.Ls * 4 + (p.mb ? 128 : 0);
+  p.KS = cdiv(p.rows_win * p.cpr, p.warps * 32 / p.sp);  // data-chunk slots per thread
+  p.smem_bytes = p.sp * p.NS * p.CC * p.Ls * 4 + (p.mb ? 128 : 0);
   // lane -> pixel deal (perm > 0): the bank pattern of a tile repeats every EF / gcd(T, EF) tiles
   p.nphase = 0;
   if (p.perm > 0) {
@@ -386,7 +390,23 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("mov.u32 %%r4, %%ctaid.x;");
   else
     o("ld.param.u32 %%r4, [p_gy];");     // local m-group (the entry subtracted g_lo)
+  const int NTh = NT / p.sp, WH = p.warps / p.sp;
+  o("and.b32 %%r7, %%r2, 31;");           // lane
+  o("shr.u32 %%r8, %%r2, 5;");            // warp
+  if (p.sp > 1) {  // sub-tile h = warp / WH; r56 = tid in the sub-tile, r58 = warp in the sub-tile
+    o("div.u32 %%r57, %%r8, %d;", WH);
+    o("mul.lo.u32 %%r56, %%r57, %d;", NTh);
+    o("sub.u32 %%r56, %%r2, %%r56;");
+    o("mul.lo.u32 %%r58, %%r57, %d;", WH);
+    o("sub.u32 %%r58, %%r8, %%r58;");
+    o("add.u32 %%r61, %%r57, 1;");         // the sub-tile's named barrier
+  } else {
+    o("mov.u32 %%r56, %%r2;");
+    o("mov.u32 %%r57, 0;");
+    o("mov.u32 %%r58, %%r8;");
+  }
   o("mul.lo.u32 %%r28, %%r3, %d;", p.T);  // g0: first output pixel of the tile
+  if (p.sp > 1) o("mad.lo.u32 %%r28, %%r57, %d, %%r28;", p.T / p.sp);  // ... of the sub-tile
   o("mul.lo.u32 %%r29, %%r1, %d;", EF);
   o("sub.u32 %%r29, %%r29, 1;");           // last pixel N*E*F - 1
   // q0 = pos(g0): staged window start
@@ -407,13 +427,13 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("add.u32 %%r10, %%r5, %d;", p.V - p.pad % p.V);
   o("and.b32 %%r10, %%r10, %d;", p.V - 1);
   o("mov.u32 %%r6, smem;");
+  o("mov.u32 %%r60, %%r6;");              // whole stage area (all sub-tiles), for the padding fill
+  if (p.sp > 1) o("mad.lo.u32 %%r6, %%r57, %d, %%r6;", p.NS * p.CC * p.Ls * 4);  // this sub-tile's ring
   if (p.mb) {  // mbarriers full[NS], empty[NS] in the first 128 bytes, stage buffers after
     o("mov.u32 %%r36, %%r6;");
     o("add.u32 %%r6, %%r6, 128;");
   }
-  o("and.b32 %%r7, %%r2, 31;");           // lane
-  o("shr.u32 %%r8, %%r2, 5;");            // warp
-  o("mul.lo.u32 %%r9, %%r8, %d;", 32 * P);
+  o("mul.lo.u32 %%r9, %%r58, %d;", 32 * P);
   o("add.u32 %%r9, %%r9, %%r7;");
   o("add.u32 %%r9, %%r9, %%r28;");        // pixel g of j = 0 (j adds 32 j)
   if (permuted) {
@@ -465,7 +485,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("sub.s32 %%r38, %%r38, 1;");                      // R_lo = floor((q0 - bo) / SWs)
   for (int k = 0; k < p.KS; ++k) {
     const int rs = 64 + k, t0 = 64 + 2 * p.KS;  // t0.. scratch
-    o("add.u32 %%r%d, %%r2, %d;", t0, k * NT);                 // d
+    o("add.u32 %%r%d, %%r56, %d;", t0, k * NTh);               // d
     o("setp.lt.u32 %%p0, %%r%d, %d;", t0, p.rows_win * p.cpr);
     o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, p.cpr);         // row in window
     o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, p.cpr);
@@ -499,9 +519,9 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   }
   // the padding words of every stage buffer: zero once (16-byte stores), before any copy lands
   {
-    const int words = p.NS * p.CC * p.Ls;  // multiple of 4
+    const int words = p.sp * p.NS * p.CC * p.Ls;  // multiple of 4
     o("shl.b32 %%r39, %%r2, 4;");
-    o("add.u32 %%r39, %%r39, %%r6;");
+    o("add.u32 %%r39, %%r39, %%r60;");
     o("mov.b32 %%r23, 0;");
     for (int w0 = 0; w0 < words; w0 += 4 * NT) {
       if (w0 + 4 * NT > words) {
@@ -643,7 +663,10 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("LOOP:");
   if (!p.mb) {
     o("cp.async.wait_group %d;", p.NS - 2);
-    o("bar.sync 0;");
+    if (p.sp > 1)
+      o("bar.sync %%r61, %d;", NTh);        // only this sub-tile's warps
+    else
+      o("bar.sync 0;");
   }
   o("add.u32 %%r11, %%r15, %d;", D);
   o("setp.ge.u32 %%p3, %%r11, %%r21;");
@@ -1396,9 +1419,9 @@ std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t*
 std::string jit_label(const JitModule& jm) {
   const JitPlan& p = jm.plan;
   char b[160];
-  snprintf(b, sizeof b, "jit_q%d_p%d_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d_v%d%s%s", p.Q, p.P, p.CC, p.NS, p.warps,
-           p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V, jm.reordered ? "_ro" : "",
-           (p.perm > 0 && !jm.reordered && p.nphase > 0) ? "_dl" : "");
+  snprintf(b, sizeof b, "jit_q%d_p%d_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d_v%d%s%s%s", p.Q, p.P, p.CC, p.NS,
+           p.warps, p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V, jm.reordered ? "_ro" : "",
+           (p.perm > 0 && !jm.reordered && p.nphase > 0) ? "_dl" : "", p.sp > 1 ? ("_s" + std::to_string(p.sp)).c_str() : "");
   return b;
 }
 

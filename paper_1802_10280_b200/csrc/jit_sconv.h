@@ -18,6 +18,7 @@ struct JitPlan {
   int minb = 0;   // CTAs per SM the register budget is compiled for
   int pf = 0;     // instruction prefetch pass: 0 = default (on), < 0 = off
   int mb = 0;     // > 0: mbarrier pipeline (warps drift up to NS-2 chunks) instead of a CTA barrier per chunk
+  int split = 0;    // > 1: CTA = `split` independent sub-tiles (own stage ring + named barrier), same m-group
   int perm = 0;     // > 0: lane -> pixel deal by shared-memory bank (perm_table), accumulators transposed via smem
   int reorder = 0;  // output-channel grouping: 0 = balance groups by nonzeros if skewed, > 0 always, < 0 never
   int sws = 0;    // staged row stride request (0: W + 2*pad rounded to V; < 0: bank-conflict model; > 0: this)
@@ -32,6 +33,7 @@ struct JitPlan {
   int L = 0, Ls = 0;  // staged words per channel (and padded stride)
   int V = 1, Lv = 0;  // staging vector width (words per cp.async) and V-chunks per channel
   int nphase = 0;     // tile phases of the lane -> pixel deal (0 = off)
+  int sp = 1;         // sub-tiles per CTA in effect (split)
   int cpr = 0, rows_win = 0;  // data chunks per input row, stacked rows a window touches
   int KS = 0;     // staging slots per thread
   int nmg = 0, nch = 0;

@@ -408,3 +408,30 @@ def test_lane_pixel_deal_bitwise(case, relu):
         csr2 = escoin.Csr.stretch(w, H, W, st, p).to_device(0)
         csr2.jit(n_hint=N, perm=1, reorder=-1, **tun)
         assert fwd(csr2, x[n0:n1], b, relu).tobytes() == out[n0:n1].tobytes()
+
+
+SPLIT_CASES = [  # N, C, H, W, M, K, stride, pad, tunables
+    (3, 12, 13, 13, 40, 3, 1, 1, dict(Q=16, warps=8, split=2)), (5, 9, 7, 7, 33, 3, 1, 1, dict(Q=8, warps=6, split=3)),
+    (2, 7, 14, 14, 24, 5, 1, 2, dict(Q=8, warps=4, split=2, P=2)), (4, 6, 28, 28, 20, 3, 1, 1, dict(Q=16, warps=8, split=4)),
+    (2, 8, 15, 11, 17, 3, 2, 1, dict(Q=8, warps=4, split=2)), (3, 10, 13, 13, 48, 3, 1, 1, dict(Q=16, warps=4, split=2,
+                                                                                             units=3)),
+]
+
+
+@pytest.mark.parametrize("case", SPLIT_CASES)
+def test_split_subtiles_bitwise(case):
+    # split > 1: independent sub-tiles (own ring, own named barrier) inside one CTA — same bits
+    N, C, H, W, M, K, st, p, tun = case
+    rng = np.random.default_rng(abs(hash(case[:8])) % 2**32 + 1)
+    x = rng.random((N, C, H, W)).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.25] = 0.0
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    ref, scale = oracle_ref(w, x, b, st, p, True)
+    csr = escoin.Csr.stretch(w, H, W, st, p).to_device(0)
+    csr.jit(n_hint=N, **tun)
+    assert "_s%d" % tun["split"] in csr.label()
+    out = fwd(csr, x, b, True)
+    check(out, ref, scale, b)
+    csr.set_kernel(0)
+    assert out.tobytes() == fwd(csr, x, b, True).tobytes()
