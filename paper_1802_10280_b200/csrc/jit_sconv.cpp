@@ -373,6 +373,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o(".reg .f32 %%x<%d>;", KK * P);
   o(".reg .f32 %%v<8>;");
   o(".reg .b16 %%rs<2>;");
+  o(".reg .b32 %%s<5>;");
   // params, ids
   o("ld.param.u64 %%rd0, [p_in];");
   o("cvta.to.global.u64 %%rd0, %%rd0;");
@@ -393,20 +394,22 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   const int NTh = NT / p.sp, WH = p.warps / p.sp;
   o("and.b32 %%r7, %%r2, 31;");           // lane
   o("shr.u32 %%r8, %%r2, 5;");            // warp
-  if (p.sp > 1) {  // sub-tile h = warp / WH; r56 = tid in the sub-tile, r58 = warp in the sub-tile
-    o("div.u32 %%r57, %%r8, %d;", WH);
-    o("mul.lo.u32 %%r56, %%r57, %d;", NTh);
-    o("sub.u32 %%r56, %%r2, %%r56;");
-    o("mul.lo.u32 %%r58, %%r57, %d;", WH);
-    o("sub.u32 %%r58, %%r8, %%r58;");
-    o("add.u32 %%r61, %%r57, 1;");         // the sub-tile's named barrier
+  // sub-tile registers: %s0 = tid in the sub-tile, %s1 = sub-tile h = warp / WH, %s2 = warp in the
+  // sub-tile, %s3 = its named barrier, %s4 = base of the whole stage area
+  if (p.sp > 1) {
+    o("div.u32 %%s1, %%r8, %d;", WH);
+    o("mul.lo.u32 %%s0, %%s1, %d;", NTh);
+    o("sub.u32 %%s0, %%r2, %%s0;");
+    o("mul.lo.u32 %%s2, %%s1, %d;", WH);
+    o("sub.u32 %%s2, %%r8, %%s2;");
+    o("add.u32 %%s3, %%s1, 1;");
   } else {
-    o("mov.u32 %%r56, %%r2;");
-    o("mov.u32 %%r57, 0;");
-    o("mov.u32 %%r58, %%r8;");
+    o("mov.u32 %%s0, %%r2;");
+    o("mov.u32 %%s1, 0;");
+    o("mov.u32 %%s2, %%r8;");
   }
   o("mul.lo.u32 %%r28, %%r3, %d;", p.T);  // g0: first output pixel of the tile
-  if (p.sp > 1) o("mad.lo.u32 %%r28, %%r57, %d, %%r28;", p.T / p.sp);  // ... of the sub-tile
+  if (p.sp > 1) o("mad.lo.u32 %%r28, %%s1, %d, %%r28;", p.T / p.sp);  // ... of the sub-tile
   o("mul.lo.u32 %%r29, %%r1, %d;", EF);
   o("sub.u32 %%r29, %%r29, 1;");           // last pixel N*E*F - 1
   // q0 = pos(g0): staged window start
@@ -427,13 +430,13 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("add.u32 %%r10, %%r5, %d;", p.V - p.pad % p.V);
   o("and.b32 %%r10, %%r10, %d;", p.V - 1);
   o("mov.u32 %%r6, smem;");
-  o("mov.u32 %%r60, %%r6;");              // whole stage area (all sub-tiles), for the padding fill
-  if (p.sp > 1) o("mad.lo.u32 %%r6, %%r57, %d, %%r6;", p.NS * p.CC * p.Ls * 4);  // this sub-tile's ring
+  o("mov.u32 %%s4, %%r6;");               // whole stage area (all sub-tiles), for the padding fill
+  if (p.sp > 1) o("mad.lo.u32 %%r6, %%s1, %d, %%r6;", p.NS * p.CC * p.Ls * 4);  // this sub-tile's ring
   if (p.mb) {  // mbarriers full[NS], empty[NS] in the first 128 bytes, stage buffers after
     o("mov.u32 %%r36, %%r6;");
     o("add.u32 %%r6, %%r6, 128;");
   }
-  o("mul.lo.u32 %%r9, %%r58, %d;", 32 * P);
+  o("mul.lo.u32 %%r9, %%s2, %d;", 32 * P);
   o("add.u32 %%r9, %%r9, %%r7;");
   o("add.u32 %%r9, %%r9, %%r28;");        // pixel g of j = 0 (j adds 32 j)
   if (permuted) {
@@ -485,7 +488,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("sub.s32 %%r38, %%r38, 1;");                      // R_lo = floor((q0 - bo) / SWs)
   for (int k = 0; k < p.KS; ++k) {
     const int rs = 64 + k, t0 = 64 + 2 * p.KS;  // t0.. scratch
-    o("add.u32 %%r%d, %%r56, %d;", t0, k * NTh);               // d
+    o("add.u32 %%r%d, %%s0, %d;", t0, k * NTh);                // d
     o("setp.lt.u32 %%p0, %%r%d, %d;", t0, p.rows_win * p.cpr);
     o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, p.cpr);         // row in window
     o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, p.cpr);
@@ -521,7 +524,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   {
     const int words = p.sp * p.NS * p.CC * p.Ls;  // multiple of 4
     o("shl.b32 %%r39, %%r2, 4;");
-    o("add.u32 %%r39, %%r39, %%r60;");
+    o("add.u32 %%r39, %%r39, %%s4;");
     o("mov.b32 %%r23, 0;");
     for (int w0 = 0; w0 < words; w0 += 4 * NT) {
       if (w0 + 4 * NT > words) {
@@ -664,7 +667,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   if (!p.mb) {
     o("cp.async.wait_group %d;", p.NS - 2);
     if (p.sp > 1)
-      o("bar.sync %%r61, %d;", NTh);        // only this sub-tile's warps
+      o("bar.sync %%s3, %d;", NTh);         // only this sub-tile's warps
     else
       o("bar.sync 0;");
   }
