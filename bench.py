@@ -468,7 +468,7 @@ def main():
             fwd(escoin, runs[i], s_)
 
     graph = None if args.no_graph else capture_step(torch, step_fn)
-    launches_per_step = sum(r.units for r in runs)
+    launches_per_step = len(runs)  # one kernel launch per layer (linked units are one kernel)
 
     # ---------------- device-timed region (K steps, barrier + sync both sides)
     if world > 1:
