@@ -430,12 +430,12 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("add.u32 %%r10, %%r5, %d;", p.V - p.pad % p.V);
   o("and.b32 %%r10, %%r10, %d;", p.V - 1);
   o("mov.u32 %%r6, smem;");
-  o("mov.u32 %%s4, %%r6;");               // whole stage area (all sub-tiles), for the padding fill
-  if (p.sp > 1) o("mad.lo.u32 %%r6, %%s1, %d, %%r6;", p.NS * p.CC * p.Ls * 4);  // this sub-tile's ring
   if (p.mb) {  // mbarriers full[NS], empty[NS] in the first 128 bytes, stage buffers after
     o("mov.u32 %%r36, %%r6;");
     o("add.u32 %%r6, %%r6, 128;");
   }
+  o("mov.u32 %%s4, %%r6;");               // whole stage area (all sub-tiles), for the padding fill
+  if (p.sp > 1) o("mad.lo.u32 %%r6, %%s1, %d, %%r6;", p.NS * p.CC * p.Ls * 4);  // this sub-tile's ring
   o("mul.lo.u32 %%r9, %%s2, %d;", 32 * P);
   o("add.u32 %%r9, %%r9, %%r7;");
   o("add.u32 %%r9, %%r9, %%r28;");        // pixel g of j = 0 (j adds 32 j)
