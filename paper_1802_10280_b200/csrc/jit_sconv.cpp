@@ -663,109 +663,154 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("setp.ne.u32 %%p12, %%r1, 0;");              // true from here on
     for (int q = 0; q < Q * P; ++q) o("mov.f32 %%a%d, 0f00000000;", q);
   }
-  o("LOOP:");
-  if (!p.mb) {
-    o("cp.async.wait_group %d;", p.NS - 2);
-    if (p.sp > 1)
-      o("bar.sync %%s3, %d;", NTh);         // only this sub-tile's warps
-    else
-      o("bar.sync 0;");
-  }
-  o("add.u32 %%r11, %%r15, %d;", D);
-  o("setp.ge.u32 %%p3, %%r11, %%r21;");
-  o("@%%p3 bra.uni NOSTAGE;");
-  if (p.mb) {
-    // buffer b = (j + D) % NS (byte offset r16); before refilling it, every warp must have
-    // finished chunk j + D - NS: wait empty[b] with parity ((j + D) / NS + 1) & 1
-    o("sub.u32 %%r48, %%r11, %%r20;");             // jj = j + D
-    o("setp.lt.u32 %%p3, %%r48, %d;", p.NS);       // first use of the buffer: nothing to wait for
-    o("@%%p3 bra.uni EMPTY_OK;");
-    o("rem.u32 %%r49, %%r48, %d;", p.NS);
-    o("div.u32 %%r50, %%r48, %d;", p.NS);
-    o("add.u32 %%r50, %%r50, 1;");
-    o("and.b32 %%r50, %%r50, 1;");
-    o("mad.lo.u32 %%r51, %%r49, 8, %%r36;");
-    o("add.u32 %%r51, %%r51, %d;", 8 * p.NS);
-    o("WAIT_EMPTY:");
-    o("mbarrier.try_wait.parity.shared::cta.b64 %%p15, [%%r51], %%r50;");
-    o("@!%%p15 bra WAIT_EMPTY;");
-    o("EMPTY_OK:");
-  }
-  stage("%r11", "%r16");
-  if (p.mb) {
-    o("sub.u32 %%r48, %%r11, %%r20;");
-    o("rem.u32 %%r49, %%r48, %d;", p.NS);
-    o("mad.lo.u32 %%r51, %%r49, 8, %%r36;");
-    o("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%%r51];");
-  }
-  o("NOSTAGE:");
-  if (!p.mb) o("cp.async.commit_group;");
-  if (p.mb) {  // data of chunk j: full[j % NS], parity (j / NS) & 1
-    o("sub.u32 %%r48, %%r15, %%r20;");
-    o("rem.u32 %%r52, %%r48, %d;", p.NS);
-    o("div.u32 %%r50, %%r48, %d;", p.NS);
-    o("and.b32 %%r50, %%r50, 1;");
-    o("mad.lo.u32 %%r51, %%r52, 8, %%r36;");
-    o("WAIT_FULL:");
-    o("mbarrier.try_wait.parity.shared::cta.b64 %%p15, [%%r51], %%r50;");
-    o("@!%%p15 bra WAIT_FULL;");
-    o("mad.lo.u32 %%r53, %%r52, 8, %%r36;");
-    o("add.u32 %%r53, %%r53, %d;", 8 * p.NS);     // empty[j % NS], arrived on after the block
-  }
-  o("add.u32 %%r16, %%r16, %d;", p.CC * p.Ls * 4);
-  o("setp.ge.u32 %%p4, %%r16, %d;", p.NS * p.CC * p.Ls * 4);
-  o("@%%p4 mov.u32 %%r16, 0;");
-  o("mad.lo.u32 %%r17, %%r4, %d, %%r15;", p.nch);
-  o("%s", tg.c_str());
-  o("brx.idx.uni %%r17, ts;");
-  for (int g = 0; g < ng; ++g)
-    for (int k = 0; k < p.nch; ++k) {
-      o("B%d_%d:", g, k);
-      if (k < klo[g] || k >= khi[g]) {  // never entered
-        o("bra.uni NEXT;");
-        continue;
-      }
-      const int buf = (k - klo[g]) % p.NS;
-      for (int cc = 0; cc < p.CC; ++cc) {
-        const int c = k * p.CC + cc;
-        if (c >= p.C) break;
-        const auto& l = lists[size_t(g) * p.C + c];
-        if (l.empty()) continue;
-        bool used[kMaxK * kMaxK] = {};
-        for (const Nz& z : l) used[z.t] = true;
-        // K <= 5: every used tap of the channel is loaded, then its FFMAs (ptxas schedules); larger
-        // filters (AlexNet conv1 11x11) row by row — load a filter row's taps, run their FFMAs —
-        // so at most one row of taps is live.  Either way the list is sorted by tap, so every
-        // accumulator still receives its terms in ascending (kh, kw) order.
-        const int rows_per_pass = p.K <= 5 ? p.K : 1;
-        size_t zi = 0;
-        for (int kh0 = 0; kh0 < p.K; kh0 += rows_per_pass) {
-          const int t_end = std::min(p.K, kh0 + rows_per_pass) * p.K;
-          for (int t = kh0 * p.K; t < t_end; ++t) {
-            if (!used[t]) continue;
-            const int kh = t / p.K, kw = t % p.K;
-            for (int j = 0; j < P; ++j)
-              o("ld.shared.f32 %%x%d, [%%r%d+%d];", t * P + j, 40 + j,
-                ((buf * p.CC + cc) * p.Ls + kh * p.SWs + kw) * 4);
-          }
-          for (; zi < l.size() && l[zi].t < t_end; ++zi) {
-            const Nz& z = l[zi];
-            for (int j = 0; j < P; ++j)
-              o("fma.rn.f32 %%a%d, %%x%d, 0f%08X, %%a%d;", z.q * P + j, z.t * P + j, z.bits, z.q * P + j);
-          }
+  // one chunk block: per channel of the chunk, the taps the group uses, then its FFMAs
+  auto block_body = [&](int g, int k) {
+    const int buf = (k - klo[g]) % p.NS;
+    for (int cc = 0; cc < p.CC; ++cc) {
+      const int c = k * p.CC + cc;
+      if (c >= p.C) break;
+      const auto& l = lists[size_t(g) * p.C + c];
+      if (l.empty()) continue;
+      bool used[kMaxK * kMaxK] = {};
+      for (const Nz& z : l) used[z.t] = true;
+      // K <= 5: every used tap of the channel is loaded, then its FFMAs (ptxas schedules); larger
+      // filters (AlexNet conv1 11x11) row by row — load a filter row's taps, run their FFMAs —
+      // so at most one row of taps is live.  Either way the list is sorted by tap, so every
+      // accumulator still receives its terms in ascending (kh, kw) order.
+      const int rows_per_pass = p.K <= 5 ? p.K : 1;
+      size_t zi = 0;
+      for (int kh0 = 0; kh0 < p.K; kh0 += rows_per_pass) {
+        const int t_end = std::min(p.K, kh0 + rows_per_pass) * p.K;
+        for (int t = kh0 * p.K; t < t_end; ++t) {
+          if (!used[t]) continue;
+          const int kh = t / p.K, kw = t % p.K;
+          for (int j = 0; j < P; ++j)
+            o("ld.shared.f32 %%x%d, [%%r%d+%d];", t * P + j, 40 + j,
+              ((buf * p.CC + cc) * p.Ls + kh * p.SWs + kw) * 4);
+        }
+        for (; zi < l.size() && l[zi].t < t_end; ++zi) {
+          const Nz& z = l[zi];
+          for (int j = 0; j < P; ++j)
+            o("fma.rn.f32 %%a%d, %%x%d, 0f%08X, %%a%d;", z.q * P + j, z.t * P + j, z.bits, z.q * P + j);
         }
       }
-      o("bra.uni NEXT;");
     }
-  o("NEXT:");
-  if (p.pf) o("@!%%p12 bra.uni PF_DONE;");
-  if (p.mb) {
-    o("setp.eq.u32 %%p15, %%r7, 0;");
-    o("@%%p15 mbarrier.arrive.shared::cta.b64 %%rd10, [%%r53];");
+  };
+  if (!p.mb) {
+    // Straight-line schedule: each m-group's chunks follow each other in the instruction stream,
+    // with the per-chunk control (wait for this chunk's copies, CTA barrier, stage chunk k + D into
+    // its buffer — both compile-time) inline between the blocks, so a group's code is one
+    // sequential stream from its entry to the epilogue: no per-chunk jump back to a shared loop
+    // head (the jumps restarted the sequential instruction prefetch three times per chunk; ncu
+    // r02l: no_instructions was the top stall of the large-code layers).
+    std::string tgg = "tgg: .branchtargets ";
+    for (int g = 0; g < ng; ++g) tgg += std::string(g ? ", " : "") + "G" + std::to_string(g);
+    o("%s;", tgg.c_str());
+    o("brx.idx.uni %%r4, tgg;");
+    for (int g = 0; g < ng; ++g) {
+      o("G%d:", g);
+      for (int k = klo[g]; k < khi[g]; ++k) {
+        o("cp.async.wait_group %d;", p.NS - 2);
+        if (p.sp > 1)
+          o("bar.sync %%s3, %d;", NTh);
+        else
+          o("bar.sync 0;");
+        if (k + D < khi[g]) {
+          o("mov.u32 %%r11, %d;", k + D);
+          o("mov.u32 %%r12, %d;", ((k + D - klo[g]) % p.NS) * p.CC * p.Ls * 4);
+          stage("%r11", "%r12");
+        }
+        o("cp.async.commit_group;");
+        o("B%d_%d:", g, k);
+        block_body(g, k);
+        if (p.pf) o("@!%%p12 bra.uni PF_DONE;");
+      }
+      o("bra.uni EPI;");
+    }
+    // entries of the prefetch table for chunks a group never runs (not taken)
+    for (int g = 0; g < ng; ++g)
+      for (int k = 0; k < p.nch; ++k)
+        if (k < klo[g] || k >= khi[g]) {
+          o("B%d_%d:", g, k);
+          o("bra.uni EPI;");
+        }
+  } else {
+    o("LOOP:");
+    if (!p.mb) {
+      o("cp.async.wait_group %d;", p.NS - 2);
+      if (p.sp > 1)
+        o("bar.sync %%s3, %d;", NTh);         // only this sub-tile's warps
+      else
+        o("bar.sync 0;");
+    }
+    o("add.u32 %%r11, %%r15, %d;", D);
+    o("setp.ge.u32 %%p3, %%r11, %%r21;");
+    o("@%%p3 bra.uni NOSTAGE;");
+    if (p.mb) {
+      // buffer b = (j + D) % NS (byte offset r16); before refilling it, every warp must have
+      // finished chunk j + D - NS: wait empty[b] with parity ((j + D) / NS + 1) & 1
+      o("sub.u32 %%r48, %%r11, %%r20;");             // jj = j + D
+      o("setp.lt.u32 %%p3, %%r48, %d;", p.NS);       // first use of the buffer: nothing to wait for
+      o("@%%p3 bra.uni EMPTY_OK;");
+      o("rem.u32 %%r49, %%r48, %d;", p.NS);
+      o("div.u32 %%r50, %%r48, %d;", p.NS);
+      o("add.u32 %%r50, %%r50, 1;");
+      o("and.b32 %%r50, %%r50, 1;");
+      o("mad.lo.u32 %%r51, %%r49, 8, %%r36;");
+      o("add.u32 %%r51, %%r51, %d;", 8 * p.NS);
+      o("WAIT_EMPTY:");
+      o("mbarrier.try_wait.parity.shared::cta.b64 %%p15, [%%r51], %%r50;");
+      o("@!%%p15 bra WAIT_EMPTY;");
+      o("EMPTY_OK:");
+    }
+    stage("%r11", "%r16");
+    if (p.mb) {
+      o("sub.u32 %%r48, %%r11, %%r20;");
+      o("rem.u32 %%r49, %%r48, %d;", p.NS);
+      o("mad.lo.u32 %%r51, %%r49, 8, %%r36;");
+      o("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%%r51];");
+    }
+    o("NOSTAGE:");
+    if (!p.mb) o("cp.async.commit_group;");
+    if (p.mb) {  // data of chunk j: full[j % NS], parity (j / NS) & 1
+      o("sub.u32 %%r48, %%r15, %%r20;");
+      o("rem.u32 %%r52, %%r48, %d;", p.NS);
+      o("div.u32 %%r50, %%r48, %d;", p.NS);
+      o("and.b32 %%r50, %%r50, 1;");
+      o("mad.lo.u32 %%r51, %%r52, 8, %%r36;");
+      o("WAIT_FULL:");
+      o("mbarrier.try_wait.parity.shared::cta.b64 %%p15, [%%r51], %%r50;");
+      o("@!%%p15 bra WAIT_FULL;");
+      o("mad.lo.u32 %%r53, %%r52, 8, %%r36;");
+      o("add.u32 %%r53, %%r53, %d;", 8 * p.NS);     // empty[j % NS], arrived on after the block
+    }
+    o("add.u32 %%r16, %%r16, %d;", p.CC * p.Ls * 4);
+    o("setp.ge.u32 %%p4, %%r16, %d;", p.NS * p.CC * p.Ls * 4);
+    o("@%%p4 mov.u32 %%r16, 0;");
+    o("mad.lo.u32 %%r17, %%r4, %d, %%r15;", p.nch);
+    o("%s", tg.c_str());
+    o("brx.idx.uni %%r17, ts;");
+    for (int g = 0; g < ng; ++g)
+      for (int k = 0; k < p.nch; ++k) {
+        o("B%d_%d:", g, k);
+        if (k < klo[g] || k >= khi[g]) {  // never entered
+          o("bra.uni NEXT;");
+          continue;
+        }
+        block_body(g, k);
+        o("bra.uni NEXT;");
+      }
+    o("NEXT:");
+    if (p.pf) o("@!%%p12 bra.uni PF_DONE;");
+    if (p.mb) {
+      o("setp.eq.u32 %%p15, %%r7, 0;");
+      o("@%%p15 mbarrier.arrive.shared::cta.b64 %%rd10, [%%r53];");
+    }
+    o("add.u32 %%r15, %%r15, 1;");
+    o("setp.lt.u32 %%p5, %%r15, %%r21;");
+    o("@%%p5 bra.uni LOOP;");
+
   }
-  o("add.u32 %%r15, %%r15, 1;");
-  o("setp.lt.u32 %%p5, %%r15, %%r21;");
-  o("@%%p5 bra.uni LOOP;");
   o("EPI:");
   if (reordered) {
     // per-group epilogues: each group's rows are scattered output channels, so the channel of

@@ -81,8 +81,9 @@ def main():
                "serialised; profiles/%s_%s_launches.csv): escoin_jit_sconv = %.1f%% of all GPU time (%d launches); the "
                "rest is the L2-flush fills and setup." % (a.tag, a.wl, 100.0 * sconv / max(tot, 1.0),
                                                           sum(1 for r in data if "escoin_jit_sconv" in r[ik])), ""]
-    md += ["Full capture (`ncu --set full --import-source on --clock-control none`, one launch per layer after an L2 "
-           "flush, `tools/prof_jit.py`):", ""]
+    md += ["Full capture (`ncu --set full --import-source on --clock-control none` of bench.py's eager per-layer pass, "
+           "NVTX range `layers`: exactly the kernels and tunings the bench times, one launch per layer after the L2 "
+           "flush):", ""]
     md.append("| metric | " + " | ".join(c[0] for c in cols) + " |")
     md.append("|---" * (len(cols) + 1) + "|")
     for m, name in METRICS:
