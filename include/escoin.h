@@ -202,7 +202,7 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
  *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
  *              forwards accept any N.
- *   tunables   NULL or ntunables (<= 14) ints {Q output channels per CTA,
+ *   tunables   NULL or ntunables (<= 16) ints {Q output channels per CTA,
  *              P pixels per lane, CC channels per stage, NS stages, warps per
  *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off),
  *              mbarrier pipeline (> 0 = on: warps drift up to NS-2 chunks
@@ -227,7 +227,17 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              CTA's warps form that many independent sub-tiles, each with
  *              its own stage ring and named barrier, all running the same
  *              m-group's code — one sub-tile's barrier wait is covered by the
- *              others' work)};
+ *              others' work), pair (> 0 or 0 = default: with P even, pixel
+ *              slots j, j+1 of a lane share one fma.rn.f32x2 per nonzero —
+ *              two exact fp32 FMAs, the weight an immediate broadcast to both
+ *              halves — halving the issued FMA instructions and the code
+ *              bytes; < 0: one fma.rn.f32 per slot; same bits either way),
+ *              hp (> 0, stride 1, K <= 5, P even, FFMA2 on: a lane's pixel
+ *              pairs are horizontal neighbours (ow, ow+1) of one output row,
+ *              whose taps of one filter row are K+1 consecutive staged words
+ *              read with 8-byte ld.shared.v2 — fewer shared-memory loads;
+ *              1 = pair alignment by rule, 2 = pairs (2i-pad%2, 2i+1-pad%2)
+ *              keeping vector staging; same bits)};
  *              <= 0 entries take the defaults.
  * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
  * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE

@@ -108,16 +108,19 @@ constexpr int kMaxK = 11;  // largest filter with a specialised form (AlexNet co
 // stride SWs >= W + 2*pad (extra columns are zeros too); output pixel g = (n*E + oh)*F + ow has
 // its window origin at pos(g) = (n*(H+pad) + oh*S)*SWs + ow*S and reads tap (kh, kw) at
 // pos(g) + kh*SWs + kw — the stretched offset f(0, kh, kw) of P:428 with the stacked row stride.
+// Items (hp): a lane slot holds item g = (n*E + oh)*Fi + i — a pixel (Fi = F, column i*S) or a horizontal
+// pixel pair (ow, ow+1) = (2i + co, 2i + co + 1) (Fi pairs per row, co = 0 or -1) — with window origin at
+// stacked column i*cs + co.
 int64_t stacked_pos(const JitPlan& p, int sws, int64_t g) {
-  const int64_t EF = int64_t(p.E) * p.F, n = g / EF, r = g % EF;
-  return (n * (p.H + p.pad) + (r / p.F) * p.S) * sws + (r % p.F) * p.S;
+  const int64_t EF = int64_t(p.E) * p.Fi, n = g / EF, r = g % EF;
+  return (n * (p.H + p.pad) + (r / p.Fi) * p.S) * sws + (r % p.Fi) * p.cs + p.co;
 }
 
 // Shared-memory wavefronts per warp-wide LDS (1 = conflict-free) of the lane -> pixel mapping
 // (warp w, slot j, lane l -> pixel g0 + (w*P + j)*32 + l) for row stride sws: the mean over the
 // first tiles of the n_hint-image grid of the largest number of lanes on one bank.
 double lds_wavefronts(const JitPlan& p, int sws, int n_hint) {
-  const int64_t EF = int64_t(p.E) * p.F, total = int64_t(std::max(1, n_hint)) * EF;
+  const int64_t EF = int64_t(p.E) * p.Fi, total = int64_t(std::max(1, n_hint)) * EF;
   const int64_t tiles = std::min<int64_t>((total + p.T - 1) / p.T, 12);
   double sum = 0;
   int64_t groups = 0;
@@ -136,8 +139,15 @@ double lds_wavefronts(const JitPlan& p, int sws, int n_hint) {
 }
 
 void plan_geometry(JitPlan& p, int /*n_hint*/) {
-  const int T = p.warps * 32 * p.P;
-  const int EF = p.E * p.F;
+  // horizontal pixel pairs: stride 1, filters up to 5x5 (one filter row of words live), P even, no deal
+  const bool hp = p.hp > 0 && p.f2 && p.S == 1 && p.K <= 5 && p.P % 2 == 0 && p.perm <= 0;
+  p.Pi = hp ? p.P / 2 : p.P;
+  p.cs = hp ? 2 : p.S;
+  const int T = p.warps * 32 * p.Pi;
+  if (!hp) {
+    p.co = 0;
+    p.Fi = p.F;
+  }
   p.mos = 1;
   p.T = T;
   // split > 1: the CTA's warps form `split` independent sub-tiles of T/split pixels (own stage
@@ -151,12 +161,25 @@ void plan_geometry(JitPlan& p, int /*n_hint*/) {
   // per CTA (they are the same positions for every channel and chunk).
   if (p.vec <= 0) p.V = p.W % 4 == 0 ? 4 : p.W % 2 == 0 ? 2 : 1;
   else p.V = (p.vec >= 4 && p.W % 4 == 0) ? 4 : (p.vec >= 2 && p.W % 2 == 0) ? 2 : 1;
-  const int base = (p.W + 2 * p.pad + p.V - 1) / p.V * p.V;
-  p.SWs = p.sws > 0 ? std::max(base, (p.sws + p.V - 1) / p.V * p.V) : base;
+  if (hp) {
+    // Pair origins must be even words of the stage buffer (ld.shared.v2).  With vector staging the
+    // first data word of a row (column pad) sits on a V-word boundary, so origins (column 2i + co)
+    // are even iff co = pad mod 2 (co = -1: pairs (-1, 0), (1, 2), ...; a phantom pixel at -1).
+    // co = 0 with an odd pad needs 4-byte staging.  hp = 1: co = 0 when F is even and the pad odd
+    // only on planes up to 28 wide (no phantom column, 4-byte copies); else co = -(pad mod 2).
+    const bool keep_v = p.pad % 2 == 0 || p.hp == 2 || p.F % 2 == 1 || p.F > 28;
+    p.co = keep_v ? -(p.pad % 2) : 0;
+    if (!keep_v) p.V = 1;
+    p.Fi = (p.F - p.co + 1) / 2;
+  }
+  const int VA = hp && p.V == 1 ? 2 : p.V;  // row stride alignment (even for pairs)
+  const int base = (p.W + 2 * p.pad + VA - 1) / VA * VA;
+  p.SWs = p.sws > 0 ? std::max(base, (p.sws + VA - 1) / VA * VA) : base;
+  const int EF = p.E * p.Fi;  // items per image
   int64_t span = 0;  // max pos(g0 + Th - 1) - pos(g0); periodic in g0 with period EF
   for (int64_t g0 = 0; g0 < EF; ++g0)
     span = std::max(span, stacked_pos(p, p.SWs, g0 + Th - 1) - stacked_pos(p, p.SWs, g0));
-  p.L = int(span + int64_t(p.K - 1) * (p.SWs + 1) + 1);
+  p.L = int(span + int64_t(p.K - 1) * (p.SWs + 1) + 1 + (hp ? 2 : 0));  // pairs: one more column (+1: v2 of K odd)
   p.Lv = cdiv(p.L + p.V - 1, p.V);  // V-word chunks per channel (the window shifted by bo < V)
   p.Ls = (p.Lv * p.V + 3) & ~3;
   p.nmg = cdiv(p.M, p.Q);
@@ -327,6 +350,10 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   const int Hpd = p.H + 2 * p.pad, Wpd = p.W + 2 * p.pad;  // stretched geometry (R#3)
   const int hp = p.H + p.pad;
   const int HW = p.H * p.W, EF = p.E * p.F;
+  // items (stacked_pos): pixels, or horizontal pixel pairs (hpair: Pi = P/2 pairs per lane, slots
+  // j = 2*ji + h are pixel h of pair ji)
+  const int EFi = p.E * p.Fi, Pi = p.Pi;
+  const bool hpair = Pi != P;
   // nonzeros per (m-group, channel), ascending tap then row
   bool reordered = false;
   const std::vector<int> ord = row_order(p, rowptr, &reordered);
@@ -371,6 +398,19 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o(".reg .b64 %%rd<%d>;", 32 + 2 * p.KS + 2 * P + p.KS);
   o(".reg .f32 %%a<%d>;", Q * P);
   o(".reg .f32 %%x<%d>;", KK * P);
+  if (hpair) o(".reg .f32 %%y<%d>;", p.K * (p.K + 2) * Pi);  // words of one filter row per pair: (kh, w, ji)
+  const int P2 = P / 2;  // slot pairs (FFMA2): %A<q*P2 + jp> = {%a<q*P + 2jp>, %a<q*P + 2jp + 1>}, same for %X
+  if (p.f2) {
+    o(".reg .b64 %%A<%d>;", Q * P2);
+    o(".reg .b64 %%X<%d>;", KK * P2);
+    o(".reg .b64 %%W;");
+  }
+  auto zero_acc = [&] {
+    if (p.f2)
+      for (int i = 0; i < Q * P2; ++i) o("mov.b64 %%A%d, 0;", i);
+    else
+      for (int q = 0; q < Q * P; ++q) o("mov.f32 %%a%d, 0f00000000;", q);
+  };
   o(".reg .f32 %%v<8>;");
   o(".reg .b16 %%rs<2>;");
   o(".reg .b32 %%s<5>;");
@@ -410,19 +450,22 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   }
   o("mul.lo.u32 %%r28, %%r3, %d;", p.T);  // g0: first output pixel of the tile
   if (p.sp > 1) o("mad.lo.u32 %%r28, %%s1, %d, %%r28;", p.T / p.sp);  // ... of the sub-tile
-  o("mul.lo.u32 %%r29, %%r1, %d;", EF);
-  o("sub.u32 %%r29, %%r29, 1;");           // last pixel N*E*F - 1
+  o("mul.lo.u32 %%r29, %%r1, %d;", EFi);
+  o("sub.u32 %%r29, %%r29, 1;");           // last item N*E*Fi - 1
+  // window origin of item (n, oh, i): stacked row oh*S, column i*cs + co (pixels: ow*S, R#1)
+  auto origin_cols = [&] {
+    if (p.S > 1) o("mul.lo.u32 %%r32, %%r32, %d;", p.S);
+    if (p.cs > 1) o("mul.lo.u32 %%r33, %%r33, %d;", p.cs);
+    if (p.co) o("add.s32 %%r33, %%r33, %d;", p.co);
+  };
   // q0 = pos(g0): staged window start
-  o("div.u32 %%r30, %%r28, %d;", EF);
-  o("mul.lo.u32 %%r31, %%r30, %d;", EF);
+  o("div.u32 %%r30, %%r28, %d;", EFi);
+  o("mul.lo.u32 %%r31, %%r30, %d;", EFi);
   o("sub.u32 %%r31, %%r28, %%r31;");
-  o("div.u32 %%r32, %%r31, %d;", p.F);
-  o("mul.lo.u32 %%r33, %%r32, %d;", p.F);
+  o("div.u32 %%r32, %%r31, %d;", p.Fi);
+  o("mul.lo.u32 %%r33, %%r32, %d;", p.Fi);
   o("sub.u32 %%r33, %%r31, %%r33;");
-  if (p.S > 1) {  // window origin of output (oh, ow): stacked row oh*S, column ow*S (R#1)
-    o("mul.lo.u32 %%r32, %%r32, %d;", p.S);
-    o("mul.lo.u32 %%r33, %%r33, %d;", p.S);
-  }
+  origin_cols();
   o("mad.lo.u32 %%r34, %%r30, %d, %%r32;", hp);
   o("mad.lo.u32 %%r5, %%r34, %d, %%r33;", p.SWs);
   // bo = (q0 - pad) mod V: word q of the window is stored at buffer word q - q0 + bo, which puts
@@ -436,9 +479,9 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   }
   o("mov.u32 %%s4, %%r6;");               // whole stage area (all sub-tiles), for the padding fill
   if (p.sp > 1) o("mad.lo.u32 %%r6, %%s1, %d, %%r6;", p.NS * p.CC * p.Ls * 4);  // this sub-tile's ring
-  o("mul.lo.u32 %%r9, %%s2, %d;", 32 * P);
+  o("mul.lo.u32 %%r9, %%s2, %d;", 32 * Pi);
   o("add.u32 %%r9, %%r9, %%r7;");
-  o("add.u32 %%r9, %%r9, %%r28;");        // pixel g of j = 0 (j adds 32 j)
+  o("add.u32 %%r9, %%r9, %%r28;");        // item g of slot j = 0 (item slot ji adds 32 ji)
   if (permuted) {
     // lane -> pixel deal (perm_table): slot (warp*P + j, lane) of tile phase ph = tile mod nphase
     // takes pixel g0 + perm[ph][(warp*P + j)*32 + lane]; r(56+j) = that offset
@@ -454,22 +497,19 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
       o("cvt.u32.u16 %%r%d, %%rs0;", 56 + j);
     }
   }
-  for (int j = 0; j < P; ++j) {          // lane smem base of pixel j: smem + 4 (pos(g) - q0)
+  for (int j = 0; j < Pi; ++j) {         // lane smem base of item slot j: smem + 4 (pos(g) - q0)
     if (permuted)
       o("add.u32 %%r35, %%r28, %%r%d;", 56 + j);
     else
       o("add.u32 %%r35, %%r9, %d;", 32 * j);
     o("min.u32 %%r35, %%r35, %%r29;");     // tail lanes read in range, never store
-    o("div.u32 %%r30, %%r35, %d;", EF);
-    o("mul.lo.u32 %%r31, %%r30, %d;", EF);
+    o("div.u32 %%r30, %%r35, %d;", EFi);
+    o("mul.lo.u32 %%r31, %%r30, %d;", EFi);
     o("sub.u32 %%r31, %%r35, %%r31;");
-    o("div.u32 %%r32, %%r31, %d;", p.F);
-    o("mul.lo.u32 %%r33, %%r32, %d;", p.F);
+    o("div.u32 %%r32, %%r31, %d;", p.Fi);
+    o("mul.lo.u32 %%r33, %%r32, %d;", p.Fi);
     o("sub.u32 %%r33, %%r31, %%r33;");
-    if (p.S > 1) {
-      o("mul.lo.u32 %%r32, %%r32, %d;", p.S);
-      o("mul.lo.u32 %%r33, %%r33, %d;", p.S);
-    }
+    origin_cols();
     o("mad.lo.u32 %%r34, %%r30, %d, %%r32;", hp);
     o("mad.lo.u32 %%r34, %%r34, %d, %%r33;", p.SWs);
     o("sub.u32 %%r34, %%r34, %%r5;");
@@ -563,7 +603,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
       }
     }
   };
-  for (int q = 0; q < Q * P; ++q) o("mov.f32 %%a%d, 0f00000000;", q);
+  zero_acc();
   // Active chunk range per m-group (grouped layers: an m-group touches only its group's
   // channels; empty groups run no chunk at all and store bias only).
   std::vector<int> klo(ng, 0), khi(ng, 0);
@@ -654,14 +694,14 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("rem.u32 %%r27, %%r27, %d;", p.NS);
     o("sub.u32 %%r27, %d, %%r27;", p.NS - 1);
     o("mul.lo.u32 %%r27, %%r27, %d;", p.CC * p.Ls * 4);
-    for (int j = 0; j < P; ++j) o("add.u32 %%r%d, %%r%d, %%r27;", 40 + j, 40 + j);
+    for (int j = 0; j < Pi; ++j) o("add.u32 %%r%d, %%r%d, %%r27;", 40 + j, 40 + j);
     o("mad.lo.u32 %%r17, %%r4, %d, %%r26;", p.nch);
     o("%s", tp.c_str());
     o("brx.idx.uni %%r17, tp;");
     o("PF_DONE:");
-    for (int j = 0; j < P; ++j) o("sub.u32 %%r%d, %%r%d, %%r27;", 40 + j, 40 + j);
+    for (int j = 0; j < Pi; ++j) o("sub.u32 %%r%d, %%r%d, %%r27;", 40 + j, 40 + j);
     o("setp.ne.u32 %%p12, %%r1, 0;");              // true from here on
-    for (int q = 0; q < Q * P; ++q) o("mov.f32 %%a%d, 0f00000000;", q);
+    zero_acc();
   }
   // one chunk block: per channel of the chunk, the taps the group uses, then its FFMAs
   auto block_body = [&](int g, int k) {
@@ -679,7 +719,47 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
       // accumulator still receives its terms in ascending (kh, kw) order.
       const int rows_per_pass = p.K <= 5 ? p.K : 1;
       size_t zi = 0;
-      for (int kh0 = 0; kh0 < p.K; kh0 += rows_per_pass) {
+      // the FFMAs of the list's taps below t_end (the list is sorted by tap)
+      auto emit_fmas = [&](int t_end) {
+        for (; zi < l.size() && l[zi].t < t_end; ++zi) {
+          const Nz& z = l[zi];
+          if (p.f2) {
+            // FFMA2: both halves x_j * w + acc_j, each rounded once (fma.rn) — the same two fp32
+            // FMAs as the scalar form; the 64-bit immediate {w, w} becomes FFMA2's broadcast
+            // 32-bit immediate operand
+            for (int jp = 0; jp < P2; ++jp)
+              o("mov.b64 %%W, 0x%08X%08X; fma.rn.f32x2 %%A%d, %%X%d, %%W, %%A%d;", z.bits, z.bits,
+                z.q * P2 + jp, z.t * P2 + jp, z.q * P2 + jp);
+          } else {
+            for (int j = 0; j < P; ++j)
+              o("fma.rn.f32 %%a%d, %%x%d, 0f%08X, %%a%d;", z.q * P + j, z.t * P + j, z.bits, z.q * P + j);
+          }
+        }
+      };
+      if (hpair) {
+        // Horizontal pairs: pixel h of the pair reads tap (kh, kw) at word kw + h of filter row kh,
+        // so a row's K taps of both pixels are the K + 1 words [0, K] — ld.shared.v2 of word pairs
+        // (2r, 2r+1) from the (even) pair origin; tap kw's operand pair is {word kw, word kw + 1}
+        // (a loaded pair for even kw, two moves for odd kw).  y index = (kh*(K+2) + w)*Pi + ji.
+        const int K = p.K, YW = K + 2;
+        for (int kh = 0; kh < K; ++kh)
+          for (int r = 0; 2 * r <= K; ++r) {
+            bool need = false;
+            for (int kw = 2 * r - 1; kw <= 2 * r + 1; ++kw) need |= kw >= 0 && kw < K && used[kh * K + kw];
+            if (!need) continue;
+            for (int ji = 0; ji < Pi; ++ji)
+              o("ld.shared.v2.f32 {%%y%d, %%y%d}, [%%r%d+%d];", (kh * YW + 2 * r) * Pi + ji,
+                (kh * YW + 2 * r + 1) * Pi + ji, 40 + ji, ((buf * p.CC + cc) * p.Ls + kh * p.SWs + 2 * r) * 4);
+          }
+        for (int t = 0; t < KK; ++t) {
+          if (!used[t]) continue;
+          const int kh = t / K, kw = t % K;
+          for (int ji = 0; ji < Pi; ++ji)
+            o("mov.b64 %%X%d, {%%y%d, %%y%d};", t * Pi + ji, (kh * YW + kw) * Pi + ji, (kh * YW + kw + 1) * Pi + ji);
+        }
+        emit_fmas(KK);
+      }
+      for (int kh0 = 0; kh0 < p.K && !hpair; kh0 += rows_per_pass) {
         const int t_end = std::min(p.K, kh0 + rows_per_pass) * p.K;
         for (int t = kh0 * p.K; t < t_end; ++t) {
           if (!used[t]) continue;
@@ -687,12 +767,10 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
           for (int j = 0; j < P; ++j)
             o("ld.shared.f32 %%x%d, [%%r%d+%d];", t * P + j, 40 + j,
               ((buf * p.CC + cc) * p.Ls + kh * p.SWs + kw) * 4);
+          for (int jp = 0; jp < P2 && p.f2; ++jp)
+            o("mov.b64 %%X%d, {%%x%d, %%x%d};", t * P2 + jp, t * P + 2 * jp, t * P + 2 * jp + 1);
         }
-        for (; zi < l.size() && l[zi].t < t_end; ++zi) {
-          const Nz& z = l[zi];
-          for (int j = 0; j < P; ++j)
-            o("fma.rn.f32 %%a%d, %%x%d, 0f%08X, %%a%d;", z.q * P + j, z.t * P + j, z.bits, z.q * P + j);
-        }
+        emit_fmas(t_end);
       }
     }
   };
@@ -812,24 +890,38 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
 
   }
   o("EPI:");
+  for (int i = 0; i < Q * P2 && p.f2; ++i)  // unpack the pairs: the epilogues below read %a
+    o("mov.b64 {%%a%d, %%a%d}, %%A%d;", 2 * i, 2 * i + 1, i);
+  // Output slot j of this lane: predicate p(pv) = stored, rd(rdo) = out + 4*(n*M*E*F + oh*F + ow) (the
+  // channel is added by the caller); t0..t0+4 scratch.  Item slot ji = j (pixels) or j / 2 (pairs,
+  // pixel h = j % 2 of the pair: ow = 2i + co + h, stored only inside the row).
+  auto slot_out = [&](int j, int pv, int rdo, int t0) {
+    const int ji = hpair ? j / 2 : j, h = hpair ? j % 2 : 0;
+    o("add.u32 %%r%d, %%r9, %d;", t0, 32 * ji);                // item g
+    o("setp.le.u32 %%p%d, %%r%d, %%r29;", pv, t0);
+    o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, EFi);          // n
+    o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, EFi);
+    o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 2, t0, t0 + 2);    // item in image (pixels: oh*F + ow)
+    if (hpair) {
+      o("div.u32 %%r%d, %%r%d, %d;", t0 + 3, t0 + 2, p.Fi);   // oh
+      o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 4, t0 + 3, p.Fi);
+      o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 4, t0 + 2, t0 + 4);  // i
+      o("mad.lo.s32 %%r%d, %%r%d, 2, %d;", t0 + 4, t0 + 4, p.co + h);  // ow (-1: phantom)
+      o("setp.lt.and.u32 %%p%d, %%r%d, %d, %%p%d;", pv, t0 + 4, p.F, pv);
+      o("mad.lo.u32 %%r%d, %%r%d, %d, %%r%d;", t0 + 2, t0 + 3, p.F, t0 + 4);  // oh*F + ow
+    }
+    o("mul.wide.u32 %%rd%d, %%r%d, %d;", rdo, t0 + 1, p.M * EF);
+    o("cvt.u64.u32 %%rd7, %%r%d;", t0 + 2);
+    o("add.s64 %%rd%d, %%rd%d, %%rd7;", rdo, rdo);
+    o("shl.b64 %%rd%d, %%rd%d, 2;", rdo, rdo);
+    o("add.s64 %%rd%d, %%rd%d, %%rd1;", rdo, rdo);
+  };
   if (reordered) {
     // per-group epilogues: each group's rows are scattered output channels, so the channel of
     // (group, q) is an immediate (bias + 4m, out + 4m*EF); one brx on the group picks the block
     o("setp.ne.u64 %%p6, %%rd2, 0;");
     o("setp.ne.u32 %%p7, %%r0, 0;");
-    for (int j = 0; j < P; ++j) {
-      const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j, t0 = 64 + 4 * p.KS + 8 * j;
-      o("add.u32 %%r%d, %%r9, %d;", t0, 32 * j);                // g
-      o("setp.le.u32 %%p%d, %%r%d, %%r29;", pv, t0);
-      o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, EF);           // n
-      o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, EF);
-      o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 2, t0, t0 + 2);    // oh*F + ow
-      o("mul.wide.u32 %%rd%d, %%r%d, %d;", rdo, t0 + 1, p.M * EF);
-      o("cvt.u64.u32 %%rd7, %%r%d;", t0 + 2);
-      o("add.s64 %%rd%d, %%rd%d, %%rd7;", rdo, rdo);
-      o("shl.b64 %%rd%d, %%rd%d, 2;", rdo, rdo);
-      o("add.s64 %%rd%d, %%rd%d, %%rd1;", rdo, rdo);
-    }
+    for (int j = 0; j < P; ++j) slot_out(j, 16 + 2 * p.KS + j, 32 + p.KS + j, 64 + 4 * p.KS + 8 * j);
     std::string et = "te: .branchtargets ";
     for (int g = 0; g < ng; ++g) et += std::string(g ? ", " : "") + "EG" + std::to_string(g);
     o("%s;", et.c_str());
@@ -872,18 +964,18 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
       if (permuted) {  // stores in natural pixel order g0 + tid + j*NT (the accumulators go through smem)
         o("add.u32 %%r%d, %%r28, %%r2;", t0);
         o("add.u32 %%r%d, %%r%d, %d;", t0, t0, j * NT);
+        o("setp.le.u32 %%p%d, %%r%d, %%r29;", pv, t0);
+        o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, EF);           // n
+        o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, EF);
+        o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 2, t0, t0 + 2);    // oh*F + ow
+        o("mul.wide.u32 %%rd%d, %%r%d, %d;", rdo, t0 + 1, p.M * EF);
+        o("cvt.u64.u32 %%rd7, %%r%d;", t0 + 2);
+        o("add.s64 %%rd%d, %%rd%d, %%rd7;", rdo, rdo);
+        o("shl.b64 %%rd%d, %%rd%d, 2;", rdo, rdo);
+        o("add.s64 %%rd%d, %%rd%d, %%rd1;", rdo, rdo);
       } else {
-        o("add.u32 %%r%d, %%r9, %d;", t0, 32 * j);              // g
+        slot_out(j, pv, rdo, t0);
       }
-      o("setp.le.u32 %%p%d, %%r%d, %%r29;", pv, t0);
-      o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, EF);           // n
-      o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, EF);
-      o("sub.u32 %%r%d, %%r%d, %%r%d;", t0 + 2, t0, t0 + 2);    // oh*F + ow
-      o("mul.wide.u32 %%rd%d, %%r%d, %d;", rdo, t0 + 1, p.M * EF);
-      o("cvt.u64.u32 %%rd7, %%r%d;", t0 + 2);
-      o("add.s64 %%rd%d, %%rd%d, %%rd7;", rdo, rdo);
-      o("shl.b64 %%rd%d, %%rd%d, 2;", rdo, rdo);
-      o("add.s64 %%rd%d, %%rd%d, %%rd1;", rdo, rdo);
       o("add.s64 %%rd%d, %%rd%d, %%rd6;", rdo, rdo);
     }
     // acc + bias[m] (one fp32 add), then ReLU v > 0 ? v : 0 (R#10); relu is uniform, so the two
@@ -1048,6 +1140,7 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   p.C = C; p.H = H; p.W = W; p.M = M; p.K = K; p.pad = pad;
   p.E = E; p.F = F; p.S = stride;
   if (p.P <= 0) p.P = 1;
+  p.f2 = (p.pair >= 0 && p.P % 2 == 0) ? 1 : 0;
   // channel chunk / stages: 5x5 (and larger) filters stage a wider halo per channel and run
   // 2.8x the FFMAs per staged word; measured best with 4 channels x 4 stages (AlexNet conv2
   // +5% over 8 x 3), 3x3 and 1x1 with 8 x 3 (conv3 -14% with 4 x 4).
@@ -1467,8 +1560,8 @@ std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t*
 std::string jit_label(const JitModule& jm) {
   const JitPlan& p = jm.plan;
   char b[160];
-  snprintf(b, sizeof b, "jit_q%d_p%d_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d_v%d%s%s%s", p.Q, p.P, p.CC, p.NS,
-           p.warps, p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V, jm.reordered ? "_ro" : "",
+  snprintf(b, sizeof b, "jit_q%d_p%d%s%s_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d_v%d%s%s%s", p.Q, p.P,
+           p.f2 ? "x2" : "", p.Pi != p.P ? (p.co ? "h1" : "h0") : "", p.CC, p.NS, p.warps, p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V, jm.reordered ? "_ro" : "",
            (p.perm > 0 && !jm.reordered && p.nphase > 0) ? "_dl" : "", p.sp > 1 ? ("_s" + std::to_string(p.sp)).c_str() : "");
   return b;
 }
@@ -1485,7 +1578,7 @@ void jit_free(JitModule& jm) {
 int jit_launch(const JitModule& jm, const float* in, float* out, const float* bias, int relu, int N,
                cudaStream_t s) {
   const JitPlan& p = jm.plan;
-  const int64_t pixels = int64_t(N) * p.E * p.F;
+  const int64_t pixels = int64_t(N) * p.E * p.Fi;  // items (pixels or horizontal pairs)
   const int64_t tiles = (pixels + p.T - 1) / p.T;
   const int64_t last_pos = (int64_t(N) * (p.H + p.pad) + p.pad) * p.SWs + p.L;  // staged positions stay int32
   if (!jm.func) return -1;

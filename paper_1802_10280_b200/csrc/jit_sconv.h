@@ -24,6 +24,11 @@ struct JitPlan {
   int sws = 0;    // staged row stride request (0: W + 2*pad rounded to V; < 0: bank-conflict model; > 0: this)
   int vec = 0;    // staging vector width request (<= 0: widest the input row allows; 1 = 4-byte copies)
   int units = 0;  // separately compiled modules the m-groups are split into (<= 0: by nnz, jit_build)
+  int pair = 0;   // > 0: slot pairs (j, j+1) share one fma.rn.f32x2 (FFMA2, weight immediate broadcast) — needs
+                  // P even; 0 = default (on when P is even), < 0 = one fma.rn.f32 per slot
+  int hp = 0;     // > 0: horizontal pixel pairs (stride 1, K <= 5, P even): a lane's pixel pair is (ow, ow+1) of one
+                  // row, its taps come from ld.shared.v2 (K+1 words per filter row instead of 2K); 1 = pair origin
+                  // parity by rule, 2 = origins at odd columns kept for vector staging
   // layer
   int C = 0, H = 0, W = 0, M = 0, K = 0, pad = 0, E = 0, F = 0, S = 1;
   // derived
@@ -34,6 +39,10 @@ struct JitPlan {
   int V = 1, Lv = 0;  // staging vector width (words per cp.async) and V-chunks per channel
   int nphase = 0;     // tile phases of the lane -> pixel deal (0 = off)
   int sp = 1;         // sub-tiles per CTA in effect (split)
+  int f2 = 0;         // FFMA2 slot pairs in effect (pair)
+  // items: what a lane slot holds — a pixel, or (hp) a horizontal pixel pair.  Item (n, oh, i) of a row of Fi
+  // items has its window origin at stacked column i*cs + co; Pi items per lane (P, or P/2 pairs)
+  int Fi = 0, cs = 1, co = 0, Pi = 1;
   int cpr = 0, rows_win = 0;  // data chunks per input row, stacked rows a window touches
   int KS = 0;     // staging slots per thread
   int nmg = 0, nch = 0;

@@ -25,22 +25,29 @@ def _lib():
 
 def gen_ptx(csr, n_hint=16, **tun):
     # reorder defaults to -1 here (identity grouping: accumulator (g, q) is row g*Q + q)
-    keys = ["Q", "P", "CC", "NS", "warps", "minb", "prefetch", "mbarrier", "units", "vec", "reorder"]
+    keys = ["Q", "P", "CC", "NS", "warps", "minb", "prefetch", "mbarrier", "units", "vec", "reorder", "sws",
+            "perm", "split", "pair", "hp"]
     tun.setdefault("reorder", -1)
-    arr = (ctypes.c_int * 11)(*[tun.get(k, 0) for k in keys])
+    arr = (ctypes.c_int * 16)(*[tun.get(k, 0) for k in keys])
     L, n = _lib(), ctypes.c_int64()
-    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 11, None, 0, ctypes.byref(n)) == 0
+    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 16, None, 0, ctypes.byref(n)) == 0
     buf = ctypes.create_string_buffer(n.value + 1)
-    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 11, buf, n.value + 1, ctypes.byref(n)) == 0
+    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 16, buf, n.value + 1, ctypes.byref(n)) == 0
     return buf.value.decode()
 
 
 FMA = re.compile(r"fma\.rn\.f32 %a(\d+), %x(\d+), 0f([0-9A-F]{8}), %a(\d+);")
+# FFMA2 slot pairs: {w, w} as a 64-bit immediate, pair registers %A (accumulators) and %X (taps)
+FMA2 = re.compile(r"mov\.b64 %W, 0x([0-9A-F]{8})([0-9A-F]{8}); fma\.rn\.f32x2 %A(\d+), %X(\d+), %W, %A(\d+);")
+PACK = re.compile(r"mov\.b64 %X(\d+), \{%x(\d+), %x(\d+)\};")
+UNPACK = re.compile(r"mov\.b64 \{%a(\d+), %a(\d+)\}, %A(\d+);")
 BLOCK = re.compile(r"^B(\d+)_(\d+):")
 
 
 def fma_stream(ptx):
-    """[(group, acc, xreg, bits)] in program order of the chunk blocks."""
+    """[(group, acc, xreg, bits)] in program order of the chunk blocks; an FFMA2 on pair registers
+    counts as its two halves (acc 2A / 2A+1 at taps 2X / 2X+1), after checking that every pair is
+    built from (and unpacked into) exactly those scalar registers."""
     g, out = None, []
     for line in ptx.splitlines():
         m = BLOCK.match(line)
@@ -51,6 +58,22 @@ def fma_stream(ptx):
         if m:
             assert m.group(1) == m.group(4), line  # accumulates in place
             out.append((g, int(m.group(1)), int(m.group(2)), int(m.group(3), 16)))
+            continue
+        m = FMA2.search(line)
+        if m:
+            assert m.group(1) == m.group(2), line  # the same weight in both halves
+            assert m.group(3) == m.group(5), line
+            a, x, bits = int(m.group(3)), int(m.group(4)), int(m.group(1), 16)
+            out.append((g, 2 * a, 2 * x, bits))
+            out.append((g, 2 * a + 1, 2 * x + 1, bits))
+            continue
+        m = PACK.search(line)
+        if m:
+            assert (int(m.group(2)), int(m.group(3))) == (2 * int(m.group(1)), 2 * int(m.group(1)) + 1), line
+            continue
+        m = UNPACK.search(line)
+        if m:
+            assert (int(m.group(1)), int(m.group(2))) == (2 * int(m.group(3)), 2 * int(m.group(3)) + 1), line
     return out
 
 
@@ -86,6 +109,9 @@ CASES = [  # C, H, W, M, K, pad, density, tunables
     (7, 9, 11, 33, 3, 1, 0.3, dict(Q=8, P=2, CC=3)),
     (6, 8, 8, 20, 5, 2, 0.25, dict(Q=16, CC=4, NS=4, mbarrier=1)),
     (12, 6, 7, 19, 1, 0, 0.4, dict(Q=4, P=3, warps=4, prefetch=-1)),
+    (9, 10, 10, 21, 3, 1, 0.25, dict(Q=8, P=2, pair=-1)),            # scalar FFMAs at P = 2
+    (10, 7, 9, 17, 3, 1, 0.3, dict(Q=8, P=4, CC=4, warps=4)),       # two FFMA2 pairs per lane
+    (5, 12, 12, 12, 5, 2, 0.3, dict(Q=4, P=2, CC=2, mbarrier=1)),   # FFMA2 in the mbarrier pipeline
 ]
 STRIDED = [  # C, H, W, M, K, stride, pad
     (6, 15, 11, 13, 3, 2, 1), (5, 9, 9, 7, 3, 1, 0), (3, 11, 11, 5, 5, 2, 2), (7, 13, 12, 6, 3, 3, 1),
@@ -130,7 +156,7 @@ def test_generated_ptx_compiles_for_sm100a():
     L = workloads.TINY
     w = inputs.layer_weights("tiny", L, 800)
     csr = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad)
-    for tun in [dict(), dict(mbarrier=1, NS=4), dict(Q=8, P=2, prefetch=-1)]:
+    for tun in [dict(), dict(mbarrier=1, NS=4), dict(Q=8, P=2, prefetch=-1), dict(Q=8, P=2), dict(Q=4, P=4, pair=1)]:
         n = ctypes.c_int64()
         assert _lib().escoin_internal_ptx_compile(gen_ptx(csr, n_hint=1, **tun).encode(), ctypes.byref(n)) == 0
         assert n.value > 0

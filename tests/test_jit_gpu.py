@@ -71,7 +71,10 @@ GRID = [  # N, C, H, W, M, K, pad, density — stride 1, "same" padding
 ]
 TUNINGS = [dict(), dict(Q=16, P=2, CC=3, NS=2), dict(Q=32, P=3, CC=5, NS=4, warps=4, minb=3),
            dict(Q=8, P=1, CC=1, NS=2, warps=2, minb=1), dict(NS=4, mbarrier=1),
-           dict(Q=16, CC=3, NS=3, warps=4, mbarrier=1, prefetch=-1), dict(Q=8, CC=1, NS=5, warps=2, mbarrier=1)]
+           dict(Q=16, CC=3, NS=3, warps=4, mbarrier=1, prefetch=-1), dict(Q=8, CC=1, NS=5, warps=2, mbarrier=1),
+           # FFMA2: slot pairs (P even, the default), scalar P = 2, horizontal pixel pairs (hp)
+           dict(Q=8, P=2, pair=-1), dict(Q=16, P=4, CC=3, warps=4), dict(Q=16, P=2, CC=3, NS=2, hp=1),
+           dict(Q=8, P=4, warps=4, hp=2), dict(Q=16, P=2, NS=4, mbarrier=1, hp=1)]
 
 
 @pytest.mark.parametrize("tun", range(len(TUNINGS)))
@@ -435,3 +438,44 @@ def test_split_subtiles_bitwise(case):
     check(out, ref, scale, b)
     csr.set_kernel(0)
     assert out.tobytes() == fwd(csr, x, b, True).tobytes()
+
+
+HP_CASES = [  # N, C, H, W, M, K, pad, tunables — horizontal pixel pairs: odd/even F, pad 0/1/2, K 1/3/5
+    (3, 12, 13, 13, 40, 3, 1, dict(Q=16, P=2, warps=4, hp=1)), (2, 9, 14, 14, 24, 3, 1, dict(Q=8, P=2, warps=4, hp=1)),
+    (2, 9, 14, 14, 24, 3, 1, dict(Q=8, P=2, warps=4, hp=2)), (2, 6, 56, 56, 16, 3, 1, dict(Q=16, P=2, warps=8, hp=1)),
+    (2, 7, 7, 7, 33, 3, 1, dict(Q=8, P=4, warps=2, hp=1)), (3, 5, 11, 9, 12, 5, 2, dict(Q=8, P=2, warps=4, hp=1)),
+    (2, 4, 12, 12, 10, 5, 2, dict(Q=4, P=2, warps=4, hp=1, CC=2, NS=4)), (4, 10, 6, 10, 9, 1, 0, dict(Q=8, P=2, hp=1)),
+    (2, 8, 9, 8, 21, 3, 0, dict(Q=8, P=2, warps=2, hp=1)), (3, 12, 13, 13, 48, 3, 1, dict(Q=16, P=2, warps=4, hp=1,
+                                                                                        units=3)),
+    (2, 8, 14, 14, 24, 3, 1, dict(Q=8, P=2, warps=8, hp=1, split=2)),
+    (5, 16, 7, 7, 64, 3, 1, dict(Q=32, P=2, warps=4, hp=1, reorder=1)),
+]
+
+
+@pytest.mark.parametrize("relu", [True, False])
+@pytest.mark.parametrize("case", HP_CASES)
+def test_horizontal_pairs_bitwise(case, relu):
+    # hp: lanes hold pixel pairs (ow, ow+1) of one output row, taps from ld.shared.v2, FFMA2 — same
+    # bits as the paper-mapping kernel, tolerance vs the oracle; phantom pixels (ow = -1 or F) never stored
+    N, C, H, W, M, K, p, tun = case
+    rng = np.random.default_rng(abs(hash(case[:7])) % 2**32 + 7)
+    x = rng.random((N, C, H, W)).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.25] = 0.0
+    w[1] = 0.0  # an empty row
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    ref, scale = oracle_ref(w, x, b, 1, p, relu)
+    csr = escoin.Csr.stretch(w, H, W, 1, p).to_device(0)
+    csr.jit(n_hint=N, **tun)
+    lab = csr.label()
+    assert "x2h" in lab, lab
+    sentinel = torch.full((N, M, H + 2 * p - K + 1, W + 2 * p - K + 1), float("nan"), device="cuda")
+    dx = torch.from_numpy(x).cuda()
+    db = torch.from_numpy(b).cuda()
+    escoin.sconv_forward(N, C, H, W, M, K, 1, p, csr, dx, sentinel, db, relu, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    out = sentinel.cpu().numpy()
+    assert not np.isnan(out).any()  # every output written
+    check(out, ref, scale, b)
+    csr.set_kernel(0)
+    assert out.tobytes() == fwd(csr, x, b, relu).tobytes()
