@@ -187,7 +187,8 @@ void plan_geometry(JitPlan& p, int /*n_hint*/) {
   p.cpr = p.W / p.V;                                  // data chunks per input row
   p.rows_win = (p.Lv * p.V + p.SWs - 1) / p.SWs + 1;  // stacked rows the window can touch
   p.KS = cdiv(p.rows_win * p.cpr, p.warps * 32 / p.sp);  // data-chunk slots per thread
-  p.smem_bytes = p.sp * p.NS * p.CC * p.Ls * 4 + (p.mb ? 128 : 0);
+  // + the m-group's Q bias values (staged once per CTA, read by the epilogue)
+  p.smem_bytes = p.sp * p.NS * p.CC * p.Ls * 4 + (p.mb ? 128 : 0) + ((p.Q * 4 + 15) & ~15);
   // lane -> pixel deal (perm > 0): the bank pattern of a tile repeats every EF / gcd(T, EF) tiles
   p.nphase = 0;
   if (p.perm > 0) {
@@ -414,6 +415,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o(".reg .f32 %%v<8>;");
   o(".reg .b16 %%rs<2>;");
   o(".reg .b32 %%s<5>;");
+  o(".reg .b32 %%bb;");  // shared-memory address of the group's staged bias
   // params, ids
   o("ld.param.u64 %%rd0, [p_in];");
   o("cvta.to.global.u64 %%rd0, %%rd0;");
@@ -573,6 +575,24 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
       } else {
         o("st.shared.v4.b32 [%%r39+%d], {%%r23, %%r23, %%r23, %%r23};", w0 * 4);
       }
+    }
+    // the group's bias values (0 past M or without bias) into shared memory behind the stage area now,
+    // so the epilogue does not wait on a global load (ncu r03b: the bias loads' long-scoreboard stalls)
+    o("add.u32 %%bb, %%s4, %d;", words * 4);
+    if (!reordered) {
+      o("setp.lt.u32 %%p13, %%r2, %d;", Q);
+      o("@%%p13 add.u32 %%r24, %%r4, %d;", g_lo);
+      o("@%%p13 mad.lo.u32 %%r24, %%r24, %d, %%r2;", Q);       // m = m0 + tid
+      o("@%%p13 setp.lt.u32 %%p13, %%r24, %d;", p.M);
+      o("mov.f32 %%v2, 0f00000000;");
+      o("setp.ne.and.u64 %%p14, %%rd2, 0, %%p13;");
+      o("@%%p14 mul.wide.u32 %%rd12, %%r24, 4;");
+      o("@%%p14 add.s64 %%rd12, %%rd12, %%rd2;");
+      o("@%%p14 ld.global.nc.f32 %%v2, [%%rd12];");
+      o("setp.lt.u32 %%p13, %%r2, %d;", Q);
+      o("shl.b32 %%r24, %%r2, 2;");
+      o("add.u32 %%r24, %%r24, %%bb;");
+      o("@%%p13 st.shared.f32 [%%r24], %%v2;");
     }
     o("bar.sync 0;");
   }
@@ -1004,14 +1024,8 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
           if (relu) o("@!%%p7 bra.uni EPB%d_LIN;", b0);
           else o("EPB%d_LIN:", b0);
           for (int q = b0; q < b0 + qb; ++q) {
-            o("mov.f32 %%v0, 0f00000000;");
-            if (full_rows) {
-              o("@%%p6 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
-            } else {
-              o("setp.gt.s32 %%p8, %%r19, %d;", q);
-              o("and.pred %%p9, %%p8, %%p6;");
-              o("@%%p9 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
-            }
+            if (!full_rows) o("setp.gt.s32 %%p8, %%r19, %d;", q);
+            o("ld.shared.f32 %%v0, [%%bb+%d];", q * 4);  // staged bias
             for (int j = 0; j < P; ++j) {
               const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j;
               o("ld.shared.f32 %%v1, [%%r54+%d];", ((q - b0) * p.T + j * NT) * 4);
@@ -1039,14 +1053,8 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
       if (relu) o("@!%%p7 bra.uni EPI_LIN;");
       else o("EPI_LIN:");
       for (int q = 0; q < Q; ++q) {
-        o("mov.f32 %%v0, 0f00000000;");
-        if (full_rows) {
-          o("@%%p6 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
-        } else {
-          o("setp.gt.s32 %%p8, %%r19, %d;", q);
-          o("and.pred %%p9, %%p8, %%p6;");
-          o("@%%p9 ld.global.nc.f32 %%v0, [%%rd5+%d];", q * 4);
-        }
+        if (!full_rows) o("setp.gt.s32 %%p8, %%r19, %d;", q);
+        o("ld.shared.f32 %%v0, [%%bb+%d];", q * 4);  // staged bias (0 past M / no bias)
         for (int j = 0; j < P; ++j) {
           const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j;
           o("add.rn.f32 %%v1, %%a%d, %%v0;", q * P + j);
@@ -1151,7 +1159,43 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   // the main loop; the mbarrier pipeline has no such barrier, so it runs without the pass
   p.pf = (p.pf < 0 || p.mb) ? 0 : 1;
   n_hint = std::max(1, n_hint);
-  if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0) {
+  if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0 && p.f2) {
+    // FFMA2 shapes (P even): a lane's work is pipe-bound by its FFMA2s (2 FMA-pipe cycles each) as long
+    // as the issue slots (FFMA2 + tap loads + pair moves) and the shared-memory wavefronts of the 4
+    // SMSPs keep up; the grid (tiles x m-groups) is sized so the last wave is nearly full — every warp
+    // count 4..32 and 1-4 CTAs per SM are candidates (waves are few at batch 128: res5 = 16 groups x
+    // 7-14 tiles), the partial last tile and group counted as lost work.
+    double best = -1;
+    JitPlan keep = p;
+    const double pixels = double(n_hint) * E * F;
+    for (int Qc : {16, 24, 32, 48, 64})
+      for (int mb = 1; mb <= 4; ++mb)
+        for (int wc = 4; wc <= 32 && wc * mb <= 64; ++wc) {
+          JitPlan t = keep;
+          t.Q = std::min(Qc, M); t.warps = wc; t.minb = mb;
+          const int regs = std::min(255, 65536 / (wc * 32 * mb)) & ~7;
+          if (!plan_fit(t, n_hint)) continue;
+          const bool hpair = t.Pi != t.P;
+          const int KK = K * K, taps_regs = hpair ? t.Pi * (K * (K + 2) + 2 * K) : KK * t.P;
+          if (t.Q * t.P + taps_regs + 24 > regs) continue;
+          const double items = double(n_hint) * E * t.Fi;
+          const double work = items / t.T * (double(M) / t.Q);  // CTA-equivalents of real work
+          const double ctas = std::ceil(items / t.T) * t.nmg, per_wave = 148.0 * mb;
+          const double wave_eff = work / (std::ceil(ctas / per_wave) * per_wave);
+          const double phantom = pixels / (items * (hpair ? 2.0 : 1.0));  // pair slots holding real pixels
+          const double fma_cyc = t.Q * KK * density * t.P;
+          const double used = 1.0 - std::pow(1.0 - density, t.Q);  // tap-use probability
+          const double lds = hpair ? t.Pi * K * ((K + 2) / 2) : KK * used * t.P;
+          const double movs = hpair ? t.Pi * K * (K / 2) * 2.0 : 0.0;
+          const double issue = fma_cyc / 2 + lds + movs + 2.0 * t.L / t.T * t.P;
+          const double wavefronts = 4.0 * lds * (hpair ? 2.0 : 1.0);
+          const double eff = fma_cyc / std::max(fma_cyc, std::max(issue / 0.85, wavefronts / 0.8));
+          const double fetch = std::pow(t.warps / 32.0, 0.25);
+          const double score = wave_eff * phantom * eff * fetch;
+          if (score > best) { best = score; p = t; }
+        }
+    if (best < 0) return -1;
+  } else if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0) {
     // Shape choice by a small model (escoin_csr_autotune_ex measures the real choice among the
     // compiled tunings).  Registers: Q accumulators + K*K taps + ~20 <= 65536 / (threads * CTAs/SM).
     // Terms: wave fill of the tiles x m-groups grid over 148 SMs x CTAs/SM (grids are often only
@@ -1184,10 +1228,41 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
     if (best < 0) return -1;
   } else {
     if (p.Q <= 0) p.Q = 64;
-    if (p.warps <= 0) p.warps = 16;
     if (p.minb <= 0) p.minb = 1;
     p.Q = std::min(p.Q, M);
+    if (p.warps <= 0) {
+      // Warps for the given Q and CTAs/SM: the tile size that fills the last wave of the (tiles x
+      // groups) grid best — time ~ waves x CTAs/SM x (rows per group) x (pixels per CTA), discounted
+      // mildly for few warps per SM (latency hiding, shared instruction fetch) — within the register
+      // budget.
+      const int G = cdiv(M, p.Q), Qb = cdiv(M, G), tap_regs = K <= 5 ? K * K * p.P : 2 * K * p.P;
+      double best = -1;
+      int bw = 16;
+      for (int wc = 8; wc <= 32 && wc * p.minb <= 64; ++wc) {
+        const int regs = std::min(255, 65536 / (wc * 32 * p.minb)) & ~7;
+        if (Qb * p.P + tap_regs / 2 + 16 > regs) continue;  // (taps are not all live at once)
+        JitPlan t = p;
+        t.warps = wc;
+        if (!plan_fit(t, n_hint)) continue;
+        const double items = double(n_hint) * E * t.Fi;
+        const double ctas = std::ceil(items / t.T) * G, waves = std::ceil(ctas / (148.0 * t.minb));
+        // minb CTAs share an SM (one's barrier wait is covered by the other's work: ~10%, r03a)
+        const double eff = std::pow(std::min(1.0, wc * t.minb / 32.0), 0.25) * (t.minb >= 2 ? 1.1 : 1.0);
+        const double time = waves * t.minb * t.T * Qb / eff;
+        if (best < 0 || time < best * 0.999) { best = time; bw = wc; }
+      }
+      p.warps = bw;
+    }
     if (!plan_fit(p, n_hint)) return -1;
+  }
+  {
+    // Balanced groups: the ceil(M/Q) m-groups take ceil(M/groups) rows each instead of Q (+ a short last
+    // group) — the CTAs of the fullest group set the layer time (ResNet res4: Q 48 -> 43, 6 groups).
+    const int G = cdiv(M, p.Q), Qb = cdiv(M, G);
+    if (Qb != p.Q) {
+      p.Q = Qb;
+      if (!plan_fit(p, n_hint)) return -1;
+    }
   }
   if (p.smem_bytes > 227 * 1024 / p.minb) return -1;
   return 0;

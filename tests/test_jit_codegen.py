@@ -104,6 +104,17 @@ def resolved_q(ptx):
     return int(re.search(r"\.reg \.f32 %a<(\d+)>;", ptx).group(1))
 
 
+def test_balanced_group_rows():
+    # Q = 48 over M = 256 rows: 6 groups of ceil(256 / 6) = 43 rows instead of 5 x 48 + 16
+    rng = np.random.default_rng(3)
+    w = rng.standard_normal((256, 4, 3, 3)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.2] = 0.0
+    csr = escoin.Csr.stretch(w, 6, 6, 1, 1)
+    ptx = gen_ptx(csr, Q=48)
+    assert resolved_q(ptx) == 43 and ".u32 mgr[12]" in ptx
+    check_rows(csr, ptx, 43, 1)
+
+
 CASES = [  # C, H, W, M, K, pad, density, tunables
     (16, 14, 14, 32, 3, 1, 0.2, dict()),
     (7, 9, 11, 33, 3, 1, 0.3, dict(Q=8, P=2, CC=3)),
@@ -126,7 +137,7 @@ def test_strided_and_padded_fma_stream(case):
     w[rng.random(w.shape) >= 0.3] = 0.0
     csr = escoin.Csr.stretch(w, H, W, st, pad)
     ptx = gen_ptx(csr, Q=8)
-    check_rows(csr, ptx, 8, 1)
+    check_rows(csr, ptx, resolved_q(ptx), 1)  # Q 8 -> ceil(M / groups) rows per group (balanced)
 
 
 @pytest.mark.parametrize("case", CASES)
