@@ -202,7 +202,7 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
  *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
  *              forwards accept any N.
- *   tunables   NULL or ntunables (<= 16) ints {Q output channels per CTA,
+ *   tunables   NULL or ntunables (<= 17) ints {Q output channels per CTA,
  *              P pixels per lane, CC channels per stage, NS stages, warps per
  *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off),
  *              mbarrier pipeline (> 0 = on: warps drift up to NS-2 chunks
@@ -237,7 +237,11 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              whose taps of one filter row are K+1 consecutive staged words
  *              read with 8-byte ld.shared.v2 — fewer shared-memory loads;
  *              1 = pair alignment by rule, 2 = pairs (2i-pad%2, 2i+1-pad%2)
- *              keeping vector staging; same bits)};
+ *              keeping vector staging; same bits), pw (> 0: one extra warp
+ *              per CTA runs the output-channel group's code one chunk ahead
+ *              of the compute warps on stale data — no copies, no stores —
+ *              so their instruction fetches hit the L1.5 cache; replaces the
+ *              prefetch pass; not with mbarrier / split / perm; same bits)};
  *              <= 0 entries take the defaults.
  * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
  * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE

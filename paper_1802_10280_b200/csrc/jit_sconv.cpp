@@ -346,7 +346,8 @@ std::vector<int> row_order(const JitPlan& p, const int32_t* rowptr, bool* reorde
 // (gen_entry below calls it with the local group index), compiled relocatable on its own.
 std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* colidx, const float* value, int g_lo,
                     int g_hi, int unit) {
-  const int KK = p.K * p.K, Q = p.Q, P = p.P, NT = p.warps * 32;
+  // NT = threads of the CTA, NTc = compute threads (the prefetch warp, if any, is warp p.warps)
+  const int KK = p.K * p.K, Q = p.Q, P = p.P, NTc = p.warps * 32, NT = NTc + (p.pw ? 32 : 0);
   const int ng = g_hi - g_lo;  // groups of this unit
   const int Hpd = p.H + 2 * p.pad, Wpd = p.W + 2 * p.pad;  // stretched geometry (R#3)
   const int hp = p.H + p.pad;
@@ -416,6 +417,10 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o(".reg .b16 %%rs<2>;");
   o(".reg .b32 %%s<5>;");
   o(".reg .b32 %%bb;");  // shared-memory address of the group's staged bias
+  if (p.pw) {
+    o(".reg .pred %%pw<2>;");
+    o(".reg .b32 %%rbid, %%rbcnt;");
+  }
   // params, ids
   o("ld.param.u64 %%rd0, [p_in];");
   o("cvta.to.global.u64 %%rd0, %%rd0;");
@@ -433,7 +438,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("mov.u32 %%r4, %%ctaid.x;");
   else
     o("ld.param.u32 %%r4, [p_gy];");     // local m-group (the entry subtracted g_lo)
-  const int NTh = NT / p.sp, WH = p.warps / p.sp;
+  const int NTh = NTc / p.sp, WH = p.warps / p.sp;
   o("and.b32 %%r7, %%r2, 31;");           // lane
   o("shr.u32 %%r8, %%r2, 5;");            // warp
   // sub-tile registers: %s0 = tid in the sub-tile, %s1 = sub-tile h = warp / WH, %s2 = warp in the
@@ -484,6 +489,15 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("mul.lo.u32 %%r9, %%s2, %d;", 32 * Pi);
   o("add.u32 %%r9, %%r9, %%r7;");
   o("add.u32 %%r9, %%r9, %%r28;");        // item g of slot j = 0 (item slot ji adds 32 ji)
+  if (p.pw) {
+    // prefetch warp (warp p.warps): items far past the last one — its lane bases clamp to valid words,
+    // none of its stores is enabled; %pw1 = compute warp
+    o("setp.eq.u32 %%pw0, %%r8, %d;", p.warps);
+    o("not.pred %%pw1, %%pw0;");
+    o("selp.b32 %%r9, %d, %%r9, %%pw0;", 0x7FFF0000);
+    o("selp.b32 %%rbid, 2, 1, %%pw0;");               // its chunk barrier: 2 (lead limiter), compute: 1
+    o("selp.b32 %%rbcnt, %d, %d, %%pw0;", NT, NTc);
+  }
   if (permuted) {
     // lane -> pixel deal (perm_table): slot (warp*P + j, lane) of tile phase ph = tile mod nphase
     // takes pixel g0 + perm[ph][(warp*P + j)*32 + lane]; r(56+j) = that offset
@@ -561,6 +575,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("mul.wide.u32 %%rd%d, %%r%d, 4;", 32 + k, t0 + 4);
     o("add.s64 %%rd%d, %%rd%d, %%rd0;", 32 + k, 32 + k);
     o("setp.ne.u32 %%p%d, %%r%d, 0;", 16 + k, 64 + p.KS + k);
+    if (p.pw) o("and.pred %%p%d, %%p%d, %%pw1;", 16 + k, 16 + k);  // the prefetch warp never copies
   }
   // the padding words of every stage buffer: zero once (16-byte stores), before any copy lands
   {
@@ -568,14 +583,16 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("shl.b32 %%r39, %%r2, 4;");
     o("add.u32 %%r39, %%r39, %%s4;");
     o("mov.b32 %%r23, 0;");
-    for (int w0 = 0; w0 < words; w0 += 4 * NT) {
-      if (w0 + 4 * NT > words) {
+    if (p.pw) o("@%%pw0 bra.uni ZF_DONE;");
+    for (int w0 = 0; w0 < words; w0 += 4 * NTc) {
+      if (w0 + 4 * NTc > words) {
         o("setp.lt.u32 %%p2, %%r2, %d;", (words - w0) / 4);
         o("@%%p2 st.shared.v4.b32 [%%r39+%d], {%%r23, %%r23, %%r23, %%r23};", w0 * 4);
       } else {
         o("st.shared.v4.b32 [%%r39+%d], {%%r23, %%r23, %%r23, %%r23};", w0 * 4);
       }
     }
+    if (p.pw) o("ZF_DONE:");
     // the group's bias values (0 past M or without bias) into shared memory behind the stage area now,
     // so the epilogue does not wait on a global load (ncu r03b: the bias loads' long-scoreboard stalls)
     o("add.u32 %%bb, %%s4, %d;", words * 4);
@@ -807,12 +824,20 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("brx.idx.uni %%r4, tgg;");
     for (int g = 0; g < ng; ++g) {
       o("G%d:", g);
+      // prefetch warp: barrier 2 pairs its wait before chunk j with the compute warps' arrival at
+      // chunk j-1 (one arrival up front, one per chunk but the last), so it runs at most one chunk
+      // ahead and the next chunk's code is in the L1.5 instruction cache when the compute warps get there
+      if (p.pw && klo[g] < khi[g]) o("@%%pw1 bar.arrive 2, %d;", NT);
       for (int k = klo[g]; k < khi[g]; ++k) {
         o("cp.async.wait_group %d;", p.NS - 2);
-        if (p.sp > 1)
+        if (p.pw) {
+          o("bar.sync %%rbid, %%rbcnt;");
+          if (k + 1 < khi[g]) o("@%%pw1 bar.arrive 2, %d;", NT);
+        } else if (p.sp > 1) {
           o("bar.sync %%s3, %d;", NTh);
-        else
+        } else {
           o("bar.sync 0;");
+        }
         if (k + D < khi[g]) {
           o("mov.u32 %%r11, %d;", k + D);
           o("mov.u32 %%r12, %d;", ((k + D - klo[g]) % p.NS) * p.CC * p.Ls * 4);
@@ -983,7 +1008,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
       const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j, t0 = 64 + 4 * p.KS + 8 * j;
       if (permuted) {  // stores in natural pixel order g0 + tid + j*NT (the accumulators go through smem)
         o("add.u32 %%r%d, %%r28, %%r2;", t0);
-        o("add.u32 %%r%d, %%r%d, %d;", t0, t0, j * NT);
+        o("add.u32 %%r%d, %%r%d, %d;", t0, t0, j * NTc);
         o("setp.le.u32 %%p%d, %%r%d, %%r29;", pv, t0);
         o("div.u32 %%r%d, %%r%d, %d;", t0 + 1, t0, EF);           // n
         o("mul.lo.u32 %%r%d, %%r%d, %d;", t0 + 2, t0 + 1, EF);
@@ -1028,7 +1053,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
             o("ld.shared.f32 %%v0, [%%bb+%d];", q * 4);  // staged bias
             for (int j = 0; j < P; ++j) {
               const int pv = 16 + 2 * p.KS + j, rdo = 32 + p.KS + j;
-              o("ld.shared.f32 %%v1, [%%r54+%d];", ((q - b0) * p.T + j * NT) * 4);
+              o("ld.shared.f32 %%v1, [%%r54+%d];", ((q - b0) * p.T + j * NTc) * 4);
               o("add.rn.f32 %%v1, %%v1, %%v0;");
               if (relu) {
                 o("setp.gt.f32 %%p10, %%v1, 0f00000000;");
@@ -1092,7 +1117,7 @@ std::string gen_entry(const JitPlan& p, const std::vector<std::pair<int, int>>& 
   for (size_t u = 0; u < ranges.size(); ++u) o(".extern .func escoin_unit_%d%s;", int(u), sig);
   o(".visible .entry escoin_jit_sconv(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
     ".param .u32 p_relu, .param .u32 p_N, .param .u64 p_perm)");
-  o(".maxntid %d, 1, 1", p.warps * 32);
+  o(".maxntid %d, 1, 1", (p.warps + (p.pw ? 1 : 0)) * 32);
   o(".minnctapersm %d", p.minb);
   o("{");
   o(".reg .pred %%p<2>;");
@@ -1157,7 +1182,8 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   p.mb = p.mb > 0 ? 1 : 0;
   // the instruction-prefetch pass reads the last stage buffer, free until the first CTA barrier of
   // the main loop; the mbarrier pipeline has no such barrier, so it runs without the pass
-  p.pf = (p.pf < 0 || p.mb) ? 0 : 1;
+  p.pw = (p.pw > 0 && !p.mb && p.split <= 1 && p.perm <= 0) ? 1 : 0;
+  p.pf = (p.pf < 0 || p.mb || p.pw) ? 0 : 1;  // the prefetch warp replaces the prefetch pass
   n_hint = std::max(1, n_hint);
   if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0 && p.f2) {
     // FFMA2 shapes (P even): a lane's work is pipe-bound by its FFMA2s (2 FMA-pipe cycles each) as long
@@ -1635,8 +1661,8 @@ std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t*
 std::string jit_label(const JitModule& jm) {
   const JitPlan& p = jm.plan;
   char b[160];
-  snprintf(b, sizeof b, "jit_q%d_p%d%s%s_cc%d_ns%d_w%d_b%d_pf%d_mb%d_u%d_sw%d_v%d%s%s%s", p.Q, p.P,
-           p.f2 ? "x2" : "", p.Pi != p.P ? (p.co ? "h1" : "h0") : "", p.CC, p.NS, p.warps, p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V, jm.reordered ? "_ro" : "",
+  snprintf(b, sizeof b, "jit_q%d_p%d%s%s_cc%d_ns%d_w%d%s_b%d_pf%d_mb%d_u%d_sw%d_v%d%s%s%s", p.Q, p.P,
+           p.f2 ? "x2" : "", p.Pi != p.P ? (p.co ? "h1" : "h0") : "", p.CC, p.NS, p.warps, p.pw ? "p" : "", p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V, jm.reordered ? "_ro" : "",
            (p.perm > 0 && !jm.reordered && p.nphase > 0) ? "_dl" : "", p.sp > 1 ? ("_s" + std::to_string(p.sp)).c_str() : "");
   return b;
 }
@@ -1665,7 +1691,7 @@ int jit_launch(const JitModule& jm, const float* in, float* out, const float* bi
   const void* a_perm = jm.d_perm;
   void* args[] = {&a_in, &a_out, &a_bias, &relu_u, &n_u, &a_perm};
   const CUresult r = driver().launch(static_cast<CUfunction>(jm.func), unsigned(p.nmg), unsigned(tiles), 1,
-                                     unsigned(p.warps * 32), 1, 1, unsigned(p.smem_bytes), (CUstream)s, args,
+                                     unsigned((p.warps + (p.pw ? 1 : 0)) * 32), 1, 1, unsigned(p.smem_bytes), (CUstream)s, args,
                                      nullptr);
   return r == CUDA_SUCCESS ? 0 : -1;
 }

@@ -26,6 +26,9 @@ struct JitPlan {
   int units = 0;  // separately compiled modules the m-groups are split into (<= 0: by nnz, jit_build)
   int pair = 0;   // > 0: slot pairs (j, j+1) share one fma.rn.f32x2 (FFMA2, weight immediate broadcast) — needs
                   // P even; 0 = default (on when P is even), < 0 = one fma.rn.f32 per slot
+  int pw = 0;     // > 0: one extra "prefetch warp" per CTA walks the m-group's code one chunk ahead of the compute
+                  // warps (garbage data, no copies, no stores) so their instruction fetches hit the L1.5 cache
+                  // (straight-line barrier mode only; not with split / deal / mbarrier)
   int hp = 0;     // > 0: horizontal pixel pairs (stride 1, K <= 5, P even): a lane's pixel pair is (ow, ow+1) of one
                   // row, its taps come from ld.shared.v2 (K+1 words per filter row instead of 2K); 1 = pair origin
                   // parity by rule, 2 = origins at odd columns kept for vector staging
