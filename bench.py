@@ -55,7 +55,7 @@ WL_NAMES = {"alexnet": "pruned AlexNet conv2-conv5 (4 sparse CONV layers)",
 # escoin_csr_jit tunings compiled per layer (Q,P,CC,NS,warps,CTAs/SM; 0 = the library's model pick);
 # escoin_csr_autotune_ex keeps the fastest under the bench's flushed-L2 conditions
 # (Q is balanced over the groups: 48 -> 43 rows on 256 channels; "32,2,8,3,12,2,-1" = FFMA2 slot pairs, the
-# res2 winner in r03c; "-1" = no instruction-prefetch pass)
+# res2 winner in r02u; "-1" = no instruction-prefetch pass)
 DEFAULT_JIT_TUNINGS = "0;32,1,0,0,24,1;32,1,0,0,16,2;32,2,8,3,12,2,-1;32,1,0,0,32,1;48,1,0,0,16,2"
 METRIC = "sparse-conv images/s (whole stack of sparse layers, global batch 128)"
 

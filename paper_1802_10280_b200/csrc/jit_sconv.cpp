@@ -490,11 +490,12 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("add.u32 %%r9, %%r9, %%r7;");
   o("add.u32 %%r9, %%r9, %%r28;");        // item g of slot j = 0 (item slot ji adds 32 ji)
   if (p.pw) {
-    // prefetch warp (warp p.warps): items far past the last one — its lane bases clamp to valid words,
+    // prefetch warp (warp p.warps): its lanes read the tile's first items' windows (valid words of the
+    // stage buffers; garbage is fine) and, after the lane bases, take items far past the last one so
     // none of its stores is enabled; %pw1 = compute warp
     o("setp.eq.u32 %%pw0, %%r8, %d;", p.warps);
     o("not.pred %%pw1, %%pw0;");
-    o("selp.b32 %%r9, %d, %%r9, %%pw0;", 0x7FFF0000);
+    o("selp.b32 %%r9, %%r28, %%r9, %%pw0;");
     o("selp.b32 %%rbid, 2, 1, %%pw0;");               // its chunk barrier: 2 (lead limiter), compute: 1
     o("selp.b32 %%rbcnt, %d, %d, %%pw0;", NT, NTc);
   }
@@ -533,6 +534,7 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("shl.b32 %%r34, %%r34, 2;");
     o("add.u32 %%r%d, %%r34, %%r6;", 40 + j);
   }
+  if (p.pw) o("selp.b32 %%r9, %d, %%r9, %%pw0;", 0x7FFF0000);  // prefetch warp: no output item
   // Data-chunk staging slots k < KS: chunk d = tid + k*NT of the window's rows x (W/V) chunks;
   // d -> stacked row R = R_lo + d / cpr, chunk c = d % cpr, buffer word R*SWs + pad + c*V - q0 + bo.
   // Valid (predicate p(16+k)) iff R is an image row of an image < N and the V words lie inside the

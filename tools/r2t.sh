@@ -1,7 +1,7 @@
 #!/bin/bash
 # HP parity + FFMA2/HP A/B on res2a/res4a + ncu of res2a (scalar best, FFMA2, HP)
 cd "$(dirname "$0")/.."
-TAG=r03b
+TAG=r02t
 timeout 1200 python -m pytest tests/test_jit_gpu.py -x -q -k "horizontal or parity_grid" > gpurun_out/${TAG}_tests.log 2>&1
 echo "tests rc=$?" >> gpurun_out/${TAG}_tests.log
 H=0,0,0,0,0,0,0,0,1

@@ -1,7 +1,7 @@
 #!/bin/bash
 # i-cache microbench + res5 A/B (bank deal, stride model, chunking, Q, mbarrier, split)
 cd "$(dirname "$0")/.."
-TAG=r03d
+TAG=r02v
 nproc > gpurun_out/${TAG}_nproc.txt; free -g >> gpurun_out/${TAG}_nproc.txt
 timeout 600 python tools/icache_bench.py > gpurun_out/${TAG}_icache.jsonl 2> gpurun_out/${TAG}_icache.err
 export ESCOIN_JIT_CACHE=/tmp/jit_cache; mkdir -p $ESCOIN_JIT_CACHE

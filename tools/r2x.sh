@@ -1,9 +1,13 @@
 #!/bin/bash
-# prefetch-warp parity + A/B on one layer per ResNet-50 stage
+# prefetch-warp parity + memcheck + A/B on one layer per ResNet-50 stage
 cd "$(dirname "$0")/.."
-TAG=r03e
-timeout 900 python -m pytest tests/test_jit_gpu.py -x -q -k "parity_grid" > gpurun_out/${TAG}_tests.log 2>&1
+TAG=r02x
+timeout 900 python -m pytest tests/test_jit_gpu.py -x -q -k "parity_grid or horizontal" > gpurun_out/${TAG}_tests.log 2>&1
 echo "tests rc=$?" >> gpurun_out/${TAG}_tests.log
+timeout 900 compute-sanitizer --tool memcheck python tools/sanitize.py > gpurun_out/${TAG}_memcheck.log 2>&1
+echo "memcheck rc=$?" >> gpurun_out/${TAG}_memcheck.log
+timeout 900 compute-sanitizer --tool racecheck python tools/sanitize.py > gpurun_out/${TAG}_racecheck.log 2>&1
+echo "racecheck rc=$?" >> gpurun_out/${TAG}_racecheck.log
 export ESCOIN_JIT_CACHE=/tmp/jit_cache; mkdir -p $ESCOIN_JIT_CACHE
 W=0,0,0,0,0,0,0,0,0,0,1
 timeout 900 python tools/ab.py resnet50 res2a_branch2b "32,1,8,3,16,2;32,1,8,3,16,2,$W;32,1,8,3,24,1,$W;32,2,8,3,12,2,-1;32,2,8,3,12,1,$W" 20 > gpurun_out/${TAG}_ab.jsonl 2> gpurun_out/${TAG}_ab.err

@@ -44,7 +44,9 @@ def main():
         ref = None
         tunings = [dict(), dict(mbarrier=1, NS=4), dict(vec=1), dict(Q=8, units=3), dict(Q=8, reorder=1),
                    dict(Q=16, warps=4, minb=2, P=2), dict(Q=8, perm=1, reorder=-1), dict(Q=8, P=2, warps=4, perm=1,
-                                                                                      reorder=-1), dict(sws=-1)]
+                                                                                      reorder=-1), dict(sws=-1),
+                   dict(Q=8, pw=1), dict(Q=8, warps=2, pw=1, units=2), dict(Q=8, P=2, warps=2, pw=1),
+                   dict(Q=8, P=2, warps=2, hp=1), dict(Q=8, P=4, warps=2, pair=1)]
         for tun in tunings:
             csr = escoin.Csr.stretch(w, H, W, st, pad).to_device(0)
             try:
