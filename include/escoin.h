@@ -202,7 +202,7 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  * (same fp32 terms in the same ascending (c, kh, kw) order, R#10).
  *   n_hint     batch size the mosaic geometry is planned for (<= 0: 128);
  *              forwards accept any N.
- *   tunables   NULL or ntunables (<= 17) ints {Q output channels per CTA,
+ *   tunables   NULL or ntunables (<= 18) ints {Q output channels per CTA,
  *              P pixels per lane, CC channels per stage, NS stages, warps per
  *              CTA, CTAs per SM, instruction-prefetch pass (< 0 = off),
  *              mbarrier pipeline (> 0 = on: warps drift up to NS-2 chunks
@@ -241,7 +241,16 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              per CTA runs the output-channel group's code one chunk ahead
  *              of the compute warps on stale data — no copies, no stores —
  *              so their instruction fetches hit the L1.5 cache; replaces the
- *              prefetch pass; not with mbarrier / split / perm; same bits)};
+ *              prefetch pass; not with mbarrier / split / perm; same bits),
+ *              ks (> 1: each output-channel group's input channels are
+ *              split into ks contiguous chunk ranges, one CTA each, for
+ *              layers with too few CTAs (small planes, few output channels):
+ *              partial sums go to a workspace owned by the handle ([ks][N][M]
+ *              [E][F] fp32, allocated by the first forward that needs it —
+ *              run one forward before capturing a graph) and a reduce kernel
+ *              adds them in a fixed order, then bias and ReLU.  Deterministic
+ *              and independent of the batch slice, within the R#11 tolerance,
+ *              but NOT bitwise equal to the one-range kernels)};
  *              <= 0 entries take the defaults.
  * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
  * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE

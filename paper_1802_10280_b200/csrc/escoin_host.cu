@@ -867,13 +867,13 @@ int auto_kernel(const escoin_csr* h) {
 }
 
 // Pattern-specialised kernel (jit_sconv.cpp): plan, generate, compile, load.
-// tun = {Q, P, CC, NS, warps, minb, prefetch, mbarrier, units, vec, reorder, sws, perm, split, pair, hp, pw} (<= 0: default;
+// tun = {Q, P, CC, NS, warps, minb, prefetch, mbarrier, units, vec, reorder, sws, perm, split, pair, hp, pw, ks} (<= 0: default;
 // prefetch < 0 = off) or NULL.
 int build_jit(escoin_csr* h, int n_hint, const int* tun) {
   JitPlan p;
   if (tun) {
     p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6]; p.mb = tun[7];
-    p.units = tun[8]; p.vec = tun[9]; p.reorder = tun[10]; p.sws = tun[11]; p.perm = tun[12]; p.split = tun[13]; p.pair = tun[14]; p.hp = tun[15]; p.pw = tun[16];
+    p.units = tun[8]; p.vec = tun[9]; p.reorder = tun[10]; p.sws = tun[11]; p.perm = tun[12]; p.split = tun[13]; p.pair = tun[14]; p.hp = tun[15]; p.pw = tun[16]; p.ks = tun[17];
   }
   if (p.P > 8 || p.Q > 256 || p.CC > 64 || p.NS > 6 || p.warps > 32 || p.minb > 8 || p.units > 32)
     return ESCOIN_ERR_UNSUPPORTED;
@@ -886,7 +886,7 @@ int build_jit(escoin_csr* h, int n_hint, const int* tun) {
     return q.Q == p.Q && q.P == p.P && q.CC == p.CC && q.NS == p.NS && q.warps == p.warps && q.minb == p.minb &&
            q.pf == p.pf && q.mb == p.mb && q.units == p.units && q.T == p.T && q.L == p.L && q.SWs == p.SWs &&
            q.V == p.V && q.reorder == p.reorder && q.sws == p.sws && q.perm == p.perm &&
-           q.split == p.split && q.f2 == p.f2 && q.Pi == p.Pi && q.co == p.co && q.pw == p.pw;
+           q.split == p.split && q.f2 == p.f2 && q.Pi == p.Pi && q.co == p.co && q.pw == p.pw && q.ks == p.ks;
   };
   {
     std::lock_guard<std::mutex> lk(h->jit_mu);
@@ -1204,7 +1204,26 @@ int escoin_sconv_forward(int N, int C, int H, int W, int M, int K, int stride, i
   int rc;
   if (h->kernel == ESCOIN_KERNEL_JIT) {
     if (int64_t(N) * C * H * W > kInt32Max) return ESCOIN_ERR_OVERFLOW;
-    rc = jit_launch(*h->jit, in, out, bias, relu, N, s);
+    JitModule& jm = *h->jit;
+    if (jm.plan.ks > 1) {
+      // split channels: partial sums into the handle's workspace (grown here, outside any capture, when a
+      // larger batch arrives), then the fixed-order reduce + bias + ReLU
+      const int64_t total = int64_t(N) * M * h->E * h->F, need = total * jm.plan.ks;
+      if (need > jm.ws_elems) {
+        if (jm.d_ws) cudaFree(jm.d_ws);
+        jm.d_ws = nullptr;
+        jm.ws_elems = 0;
+        if (cudaMalloc(&jm.d_ws, size_t(need) * 4) != cudaSuccess) {
+          jm.d_ws = nullptr;
+          return ESCOIN_ERR_ALLOC;
+        }
+        jm.ws_elems = need;
+      }
+      rc = jit_launch(jm, in, out, bias, relu, N, s, jm.d_ws);
+      if (rc == 0) rc = launch_ks_reduce(jm.d_ws, jm.plan.ks, total, M, h->E * h->F, bias, relu, out, s);
+    } else {
+      rc = jit_launch(jm, in, out, bias, relu, N, s);
+    }
     if (rc == -2) return ESCOIN_ERR_OVERFLOW;
   } else if (h->kernel == ESCOIN_KERNEL_DENSE_TC) {
     rc = launch_dense_tc(in, h->d_dense, bias, out, N, C, H, W, M, K, stride, pad, relu ? 1 : 0, 3, s);
@@ -1436,8 +1455,8 @@ int escoin_csr_jit_stats(const escoin_csr* h, int* units, int* cache_hits, doubl
 int escoin_csr_jit(escoin_csr* h, int n_hint, const int* tunables, int ntunables) {
   if (!h) return ESCOIN_ERR_NULL;
   if (!h->on_device) return ESCOIN_ERR_NOT_ON_DEVICE;
-  if (ntunables < 0 || ntunables > 17 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
-  int tun[17] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (ntunables < 0 || ntunables > 18 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
+  int tun[18] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
   DeviceGuard g(h->device);
   if (!g.ok) return ESCOIN_ERR_CUDA;
@@ -1518,12 +1537,12 @@ int escoin_internal_plan(const escoin_csr* h, int id, int64_t* out) {
  * Two-call pattern: *len receives the size; the text is copied when cap >= size + 1. */
 int escoin_internal_jit_ptx(const escoin_csr* h, int n_hint, const int* tunables, int ntunables, char* buf,
                             int64_t cap, int64_t* len) {
-  if (!h || !len || ntunables < 0 || ntunables > 17 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
+  if (!h || !len || ntunables < 0 || ntunables > 18 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
   JitPlan p;
-  int tun[17] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int tun[18] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
   p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6];
-  p.mb = tun[7]; p.units = tun[8]; p.vec = tun[9]; p.reorder = tun[10]; p.sws = tun[11]; p.perm = tun[12]; p.split = tun[13]; p.pair = tun[14]; p.hp = tun[15]; p.pw = tun[16];
+  p.mb = tun[7]; p.units = tun[8]; p.vec = tun[9]; p.reorder = tun[10]; p.sws = tun[11]; p.perm = tun[12]; p.split = tun[13]; p.pair = tun[14]; p.hp = tun[15]; p.pw = tun[16]; p.ks = tun[17];
   const double density = double(h->nnz) / (double(h->M) * h->C * h->K * h->K);
   if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint > 0 ? n_hint : 128, density) != 0)
     return ESCOIN_ERR_UNSUPPORTED;
@@ -1537,12 +1556,12 @@ int escoin_internal_jit_ptx(const escoin_csr* h, int n_hint, const int* tunables
  * *count = units) and the PTX of m-groups [g_lo, g_hi) (two-call pattern as above). */
 int escoin_internal_jit_units(const escoin_csr* h, int n_hint, const int* tunables, int ntunables, int* ranges,
                               int cap, int* count, char* buf, int64_t bufcap, int64_t* len, int g_lo, int g_hi) {
-  if (!h || !count || ntunables < 0 || ntunables > 17 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
+  if (!h || !count || ntunables < 0 || ntunables > 18 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
   JitPlan p;
-  int tun[17] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int tun[18] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
   p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6];
-  p.mb = tun[7]; p.units = tun[8]; p.vec = tun[9]; p.reorder = tun[10]; p.sws = tun[11]; p.perm = tun[12]; p.split = tun[13]; p.pair = tun[14]; p.hp = tun[15]; p.pw = tun[16];
+  p.mb = tun[7]; p.units = tun[8]; p.vec = tun[9]; p.reorder = tun[10]; p.sws = tun[11]; p.perm = tun[12]; p.split = tun[13]; p.pair = tun[14]; p.hp = tun[15]; p.pw = tun[16]; p.ks = tun[17];
   const double density = double(h->nnz) / (double(h->M) * h->C * h->K * h->K);
   if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint > 0 ? n_hint : 128, density) != 0)
     return ESCOIN_ERR_UNSUPPORTED;
@@ -1565,13 +1584,13 @@ int escoin_internal_jit_units(const escoin_csr* h, int n_hint, const int* tunabl
  * link) — *units, *cubin_bytes; the compiler/linker log on failure into buf (cap bytes). */
 int escoin_internal_jit_cubin(const escoin_csr* h, int n_hint, const int* tunables, int ntunables, int* units,
                               int64_t* cubin_bytes, char* buf, int64_t cap) {
-  if (!h || !units || !cubin_bytes || ntunables < 0 || ntunables > 17 || (ntunables > 0 && !tunables))
+  if (!h || !units || !cubin_bytes || ntunables < 0 || ntunables > 18 || (ntunables > 0 && !tunables))
     return ESCOIN_ERR_NULL;
   JitPlan p;
-  int tun[17] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int tun[18] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
   p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6];
-  p.mb = tun[7]; p.units = tun[8]; p.vec = tun[9]; p.reorder = tun[10]; p.sws = tun[11]; p.perm = tun[12]; p.split = tun[13]; p.pair = tun[14]; p.hp = tun[15]; p.pw = tun[16];
+  p.mb = tun[7]; p.units = tun[8]; p.vec = tun[9]; p.reorder = tun[10]; p.sws = tun[11]; p.perm = tun[12]; p.split = tun[13]; p.pair = tun[14]; p.hp = tun[15]; p.pw = tun[16]; p.ks = tun[17];
   const double density = double(h->nnz) / (double(h->M) * h->C * h->K * h->K);
   if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint > 0 ? n_hint : 128, density) != 0)
     return ESCOIN_ERR_UNSUPPORTED;
@@ -1591,12 +1610,12 @@ int escoin_internal_jit_cubin(const escoin_csr* h, int n_hint, const int* tunabl
 /* Internal: label of the plan escoin_csr_jit would compile (host only, nothing compiled). */
 int escoin_internal_jit_label(const escoin_csr* h, int n_hint, const int* tunables, int ntunables, char* buf,
                               int cap) {
-  if (!h || !buf || cap < 1 || ntunables < 0 || ntunables > 17 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
+  if (!h || !buf || cap < 1 || ntunables < 0 || ntunables > 18 || (ntunables > 0 && !tunables)) return ESCOIN_ERR_NULL;
   JitPlan p;
-  int tun[17] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int tun[18] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = 0; i < ntunables; ++i) tun[i] = tunables[i];
   p.Q = tun[0]; p.P = tun[1]; p.CC = tun[2]; p.NS = tun[3]; p.warps = tun[4]; p.minb = tun[5]; p.pf = tun[6];
-  p.mb = tun[7]; p.units = tun[8]; p.vec = tun[9]; p.reorder = tun[10]; p.sws = tun[11]; p.perm = tun[12]; p.split = tun[13]; p.pair = tun[14]; p.hp = tun[15]; p.pw = tun[16];
+  p.mb = tun[7]; p.units = tun[8]; p.vec = tun[9]; p.reorder = tun[10]; p.sws = tun[11]; p.perm = tun[12]; p.split = tun[13]; p.pair = tun[14]; p.hp = tun[15]; p.pw = tun[16]; p.ks = tun[17];
   const double density = double(h->nnz) / (double(h->M) * h->C * h->K * h->K);
   if (jit_plan(p, h->C, h->H, h->W, h->M, h->K, h->stride, h->pad, n_hint > 0 ? n_hint : 128, density) != 0)
     return ESCOIN_ERR_UNSUPPORTED;

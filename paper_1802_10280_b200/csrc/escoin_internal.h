@@ -71,6 +71,9 @@ int launch_dense_tc(const float* in, const float* w, const float* bias, float* o
 // Device weight stretching (stretch_device.cu).
 int launch_stretch_count(const float* w, int M, int64_t crs, int* cnt, cudaStream_t s);
 int launch_stretch_scan(const int* cnt, int M, int32_t* rowptr, cudaStream_t s);
+// split-channel partial sums [ks][total] -> out (z order, + bias[(i / EF) % M], ReLU)
+int launch_ks_reduce(const float* ws, int ks, int64_t total, int M, int EF, const float* bias, int relu, float* out,
+                     cudaStream_t s);
 int launch_densify(const int32_t* rowptr, const int32_t* colidx, const float* value, int M, int C, int K, int Hp,
                    int Wp, float* w, cudaStream_t s);
 int launch_stretch_compact(const float* w, int M, int64_t crs, int K, int Hp, int Wp, const int32_t* rowptr,

@@ -387,12 +387,12 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   const std::string mgr = unit < 0 ? std::string("mgr") : "mgr" + std::to_string(unit);
   if (unit < 0) {
     o(".visible .entry escoin_jit_sconv(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
-      ".param .u32 p_relu, .param .u32 p_N, .param .u64 p_perm)");
+      ".param .u32 p_relu, .param .u32 p_N, .param .u64 p_perm, .param .u64 p_ws)");
     o(".maxntid %d, 1, 1", NT);
     o(".minnctapersm %d", p.minb);
   } else {
     o(".visible .func escoin_unit_%d(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
-      ".param .u32 p_relu, .param .u32 p_N, .param .u32 p_gy, .param .u64 p_perm)", unit);
+      ".param .u32 p_relu, .param .u32 p_N, .param .u32 p_gy, .param .u64 p_perm, .param .u64 p_ws)", unit);
   }
   o("{");
   o(".reg .pred %%p<%d>;", 16 + 2 * p.KS + P);
@@ -417,6 +417,11 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o(".reg .b16 %%rs<2>;");
   o(".reg .b32 %%s<5>;");
   o(".reg .b32 %%bb;");  // shared-memory address of the group's staged bias
+  if (p.ks > 1) {
+    o(".reg .b32 %%kz<4>;");
+    o(".reg .b64 %%rdz;");
+    o(".reg .pred %%pz<2>;");
+  }
   if (p.pw) {
     o(".reg .pred %%pw<2>;");
     o(".reg .b32 %%rbid, %%rbcnt;");
@@ -429,7 +434,21 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("ld.param.u64 %%rd2, [p_bias];");
   o("ld.param.u32 %%r0, [p_relu];");
   o("ld.param.u32 %%r1, [p_N];");
+  if (p.ks > 1) o("cvt.u64.u32 %%rd13, %%r1;");
   o("ld.param.u64 %%rd11, [p_perm];");
+  if (p.ks > 1) {
+    // split channels: this CTA (grid z) writes raw partial sums — no bias, no ReLU — to its slice
+    // ws + z*N*M*E*F of the workspace, same layout as the output
+    o("ld.param.u64 %%rd1, [p_ws];");
+    o("cvta.to.global.u64 %%rd1, %%rd1;");
+    o("mov.u32 %%kz0, %%ctaid.z;");
+    o("mul.lo.u32 %%kz1, %%kz0, %d;", p.M * p.E * p.F);
+    o("mul.wide.u32 %%rdz, %%kz1, 4;");
+    o("mul.lo.u64 %%rdz, %%rdz, %%rd13;");
+    o("add.s64 %%rd1, %%rd1, %%rdz;");
+    o("mov.u64 %%rd2, 0;");
+    o("mov.u32 %%r0, 0;");
+  }
   o("mov.u32 %%r2, %%tid.x;");
   // grid = (m-groups, pixel tiles): the m-groups of one tile are consecutive CTAs, so they run
   // together and read the tile's input from L2 instead of re-reading it from HBM
@@ -666,6 +685,26 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   o("add.s64 %%rd8, %%rd8, %%rd9;");
   o("ld.global.nc.u32 %%r20, [%%rd8];");    // k_lo
   o("ld.global.nc.u32 %%r21, [%%rd8+4];");  // k_hi
+  if (p.ks > 1) {
+    // this CTA's part of the active chunks [k_lo, k_hi): [k_lo + a, k_lo + b), a = floor(z*n/ks) and b =
+    // floor((z+1)*n/ks) rounded down to multiples of NS (b = n for the last z) — every part starts on
+    // stage buffer 0, like the whole range, so the compile-time buffer offsets hold; a part may be empty
+    o("sub.u32 %%kz2, %%r21, %%r20;");
+    o("mov.u32 %%kz0, %%ctaid.z;");
+    o("mul.lo.u32 %%kz1, %%kz0, %%kz2;");
+    o("div.u32 %%kz1, %%kz1, %d;", p.ks);
+    o("div.u32 %%kz1, %%kz1, %d;", p.NS);
+    o("mul.lo.u32 %%kz1, %%kz1, %d;", p.NS);
+    o("add.u32 %%kz3, %%kz0, 1;");
+    o("mul.lo.u32 %%kz3, %%kz3, %%kz2;");
+    o("div.u32 %%kz3, %%kz3, %d;", p.ks);
+    o("div.u32 %%kz3, %%kz3, %d;", p.NS);
+    o("mul.lo.u32 %%kz3, %%kz3, %d;", p.NS);
+    o("setp.eq.u32 %%pz0, %%kz0, %d;", p.ks - 1);
+    o("selp.b32 %%kz3, %%kz2, %%kz3, %%pz0;");
+    o("add.u32 %%r21, %%r20, %%kz3;");
+    o("add.u32 %%r20, %%r20, %%kz1;");
+  }
   // Copy-ahead distance D: chunks staged before the one being computed. Bar mode: NS - 1
   // (one cp.async group per chunk, wait_group + CTA barrier per chunk). mbarrier mode: NS - 2,
   // so a warp may run one chunk ahead of the slowest (a buffer is refilled only after every
@@ -820,10 +859,19 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     // sequential stream from its entry to the epilogue: no per-chunk jump back to a shared loop
     // head (the jumps restarted the sequential instruction prefetch three times per chunk; ncu
     // r02l: no_instructions was the top stall of the large-code layers).
-    std::string tgg = "tgg: .branchtargets ";
-    for (int g = 0; g < ng; ++g) tgg += std::string(g ? ", " : "") + "G" + std::to_string(g);
-    o("%s;", tgg.c_str());
-    o("brx.idx.uni %%r4, tgg;");
+    if (p.ks > 1) {  // enter the group's code at this CTA's first chunk
+      std::string tk = "tks: .branchtargets ";
+      for (int g = 0; g < ng; ++g)
+        for (int k = 0; k < p.nch; ++k) tk += std::string(g || k ? ", " : "") + "E" + std::to_string(g) + "_" + std::to_string(k);
+      o("%s;", tk.c_str());
+      o("mad.lo.u32 %%kz1, %%r4, %d, %%r20;", p.nch);
+      o("brx.idx.uni %%kz1, tks;");
+    } else {
+      std::string tgg = "tgg: .branchtargets ";
+      for (int g = 0; g < ng; ++g) tgg += std::string(g ? ", " : "") + "G" + std::to_string(g);
+      o("%s;", tgg.c_str());
+      o("brx.idx.uni %%r4, tgg;");
+    }
     for (int g = 0; g < ng; ++g) {
       o("G%d:", g);
       // prefetch warp: barrier 2 pairs its wait before chunk j with the compute warps' arrival at
@@ -831,6 +879,13 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
       // ahead and the next chunk's code is in the L1.5 instruction cache when the compute warps get there
       if (p.pw && klo[g] < khi[g]) o("@%%pw1 bar.arrive 2, %d;", NT);
       for (int k = klo[g]; k < khi[g]; ++k) {
+        if (p.ks > 1) {
+          if (k > klo[g]) {  // this CTA's part ends here
+            o("setp.le.u32 %%pz0, %%r21, %d;", k);
+            o("@%%pz0 bra.uni EPI;");
+          }
+          o("E%d_%d:", g, k);
+        }
         o("cp.async.wait_group %d;", p.NS - 2);
         if (p.pw) {
           o("bar.sync %%rbid, %%rbcnt;");
@@ -841,9 +896,14 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
           o("bar.sync 0;");
         }
         if (k + D < khi[g]) {
+          if (p.ks > 1) {  // not past this CTA's part
+            o("setp.le.u32 %%pz1, %%r21, %d;", k + D);
+            o("@%%pz1 bra.uni SK%d_%d;", g, k);
+          }
           o("mov.u32 %%r11, %d;", k + D);
           o("mov.u32 %%r12, %d;", ((k + D - klo[g]) % p.NS) * p.CC * p.Ls * 4);
           stage("%r11", "%r12");
+          if (p.ks > 1) o("SK%d_%d:", g, k);
         }
         o("cp.async.commit_group;");
         o("B%d_%d:", g, k);
@@ -852,11 +912,12 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
       }
       o("bra.uni EPI;");
     }
-    // entries of the prefetch table for chunks a group never runs (not taken)
+    // entries of the prefetch / split tables for chunks a group never runs (not taken)
     for (int g = 0; g < ng; ++g)
       for (int k = 0; k < p.nch; ++k)
         if (k < klo[g] || k >= khi[g]) {
           o("B%d_%d:", g, k);
+          if (p.ks > 1) o("E%d_%d:", g, k);
           o("bra.uni EPI;");
         }
   } else {
@@ -1115,22 +1176,23 @@ std::string gen_entry(const JitPlan& p, const std::vector<std::pair<int, int>>& 
   o(".target sm_100a");
   o(".address_size 64");
   const char* sig = "(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, .param .u32 p_relu, "
-                    ".param .u32 p_N, .param .u32 p_gy, .param .u64 p_perm)";
+                    ".param .u32 p_N, .param .u32 p_gy, .param .u64 p_perm, .param .u64 p_ws)";
   for (size_t u = 0; u < ranges.size(); ++u) o(".extern .func escoin_unit_%d%s;", int(u), sig);
   o(".visible .entry escoin_jit_sconv(.param .u64 p_in, .param .u64 p_out, .param .u64 p_bias, "
-    ".param .u32 p_relu, .param .u32 p_N, .param .u64 p_perm)");
+    ".param .u32 p_relu, .param .u32 p_N, .param .u64 p_perm, .param .u64 p_ws)");
   o(".maxntid %d, 1, 1", (p.warps + (p.pw ? 1 : 0)) * 32);
   o(".minnctapersm %d", p.minb);
   o("{");
   o(".reg .pred %%p<2>;");
   o(".reg .b32 %%r<8>;");
-  o(".reg .b64 %%rd<4>;");
+  o(".reg .b64 %%rd<5>;");
   o("ld.param.u64 %%rd0, [p_in];");
   o("ld.param.u64 %%rd1, [p_out];");
   o("ld.param.u64 %%rd2, [p_bias];");
   o("ld.param.u32 %%r0, [p_relu];");
   o("ld.param.u32 %%r1, [p_N];");
   o("ld.param.u64 %%rd3, [p_perm];");
+  o("ld.param.u64 %%rd4, [p_ws];");
   o("mov.u32 %%r2, %%ctaid.x;");
   for (size_t u = 0; u < ranges.size(); ++u) {
     o("setp.lt.u32 %%p0, %%r2, %d;", ranges[u].second);
@@ -1148,6 +1210,7 @@ std::string gen_entry(const JitPlan& p, const std::vector<std::pair<int, int>>& 
     o(".param .u32 a4;");
     o(".param .u32 a5;");
     o(".param .u64 a6;");
+    o(".param .u64 a7;");
     o("st.param.u64 [a0], %%rd0;");
     o("st.param.u64 [a1], %%rd1;");
     o("st.param.u64 [a2], %%rd2;");
@@ -1155,7 +1218,8 @@ std::string gen_entry(const JitPlan& p, const std::vector<std::pair<int, int>>& 
     o("st.param.u32 [a4], %%r1;");
     o("st.param.u32 [a5], %%r3;");
     o("st.param.u64 [a6], %%rd3;");
-    o("call.uni escoin_unit_%d, (a0, a1, a2, a3, a4, a5, a6);", int(u));
+    o("st.param.u64 [a7], %%rd4;");
+    o("call.uni escoin_unit_%d, (a0, a1, a2, a3, a4, a5, a6, a7);", int(u));
     o("}");
     o("ret;");
   }
@@ -1184,8 +1248,13 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   p.mb = p.mb > 0 ? 1 : 0;
   // the instruction-prefetch pass reads the last stage buffer, free until the first CTA barrier of
   // the main loop; the mbarrier pipeline has no such barrier, so it runs without the pass
-  p.pw = (p.pw > 0 && !p.mb && p.split <= 1 && p.perm <= 0) ? 1 : 0;
-  p.pf = (p.pf < 0 || p.mb || p.pw) ? 0 : 1;  // the prefetch warp replaces the prefetch pass
+  p.ks = (p.ks > 1 && !p.mb) ? std::min(p.ks, 64) : 1;
+  if (p.ks > 1) {  // split channels: plain straight-line barrier mode, identity grouping
+    p.perm = 0;
+    p.reorder = -1;
+  }
+  p.pw = (p.pw > 0 && !p.mb && p.split <= 1 && p.perm <= 0 && p.ks == 1) ? 1 : 0;
+  p.pf = (p.pf < 0 || p.mb || p.pw || p.ks > 1) ? 0 : 1;  // the prefetch warp replaces the prefetch pass
   n_hint = std::max(1, n_hint);
   if (p.Q <= 0 && p.warps <= 0 && p.minb <= 0 && p.f2) {
     // FFMA2 shapes (P even): a lane's work is pipe-bound by its FFMA2s (2 FMA-pipe cycles each) as long
@@ -1663,15 +1732,19 @@ std::string jit_ptx_text(const JitPlan& p, const int32_t* rowptr, const int32_t*
 std::string jit_label(const JitModule& jm) {
   const JitPlan& p = jm.plan;
   char b[160];
-  snprintf(b, sizeof b, "jit_q%d_p%d%s%s_cc%d_ns%d_w%d%s_b%d_pf%d_mb%d_u%d_sw%d_v%d%s%s%s", p.Q, p.P,
+  snprintf(b, sizeof b, "jit_q%d_p%d%s%s_cc%d_ns%d_w%d%s_b%d_pf%d_mb%d_u%d_sw%d_v%d%s%s%s%s", p.Q, p.P,
            p.f2 ? "x2" : "", p.Pi != p.P ? (p.co ? "h1" : "h0") : "", p.CC, p.NS, p.warps, p.pw ? "p" : "", p.minb, p.pf, p.mb, int(jm.units.size()), p.SWs, p.V, jm.reordered ? "_ro" : "",
-           (p.perm > 0 && !jm.reordered && p.nphase > 0) ? "_dl" : "", p.sp > 1 ? ("_s" + std::to_string(p.sp)).c_str() : "");
+           (p.perm > 0 && !jm.reordered && p.nphase > 0) ? "_dl" : "", p.sp > 1 ? ("_s" + std::to_string(p.sp)).c_str() : "",
+           p.ks > 1 ? ("_k" + std::to_string(p.ks)).c_str() : "");
   return b;
 }
 
 void jit_free(JitModule& jm) {
   if (jm.d_perm) cudaFree(jm.d_perm);
   jm.d_perm = nullptr;
+  if (jm.d_ws) cudaFree(jm.d_ws);
+  jm.d_ws = nullptr;
+  jm.ws_elems = 0;
   if (jm.module && driver().ok) driver().unload(static_cast<CUmodule>(jm.module));
   jm.module = nullptr;
   jm.func = nullptr;
@@ -1679,7 +1752,7 @@ void jit_free(JitModule& jm) {
 }
 
 int jit_launch(const JitModule& jm, const float* in, float* out, const float* bias, int relu, int N,
-               cudaStream_t s) {
+               cudaStream_t s, float* ws) {
   const JitPlan& p = jm.plan;
   const int64_t pixels = int64_t(N) * p.E * p.Fi;  // items (pixels or horizontal pairs)
   const int64_t tiles = (pixels + p.T - 1) / p.T;
@@ -1691,8 +1764,10 @@ int jit_launch(const JitModule& jm, const float* in, float* out, const float* bi
   void* a_out = out;
   const void* a_bias = bias;
   const void* a_perm = jm.d_perm;
-  void* args[] = {&a_in, &a_out, &a_bias, &relu_u, &n_u, &a_perm};
-  const CUresult r = driver().launch(static_cast<CUfunction>(jm.func), unsigned(p.nmg), unsigned(tiles), 1,
+  void* a_ws = ws;
+  if (p.ks > 1 && !ws) return -1;
+  void* args[] = {&a_in, &a_out, &a_bias, &relu_u, &n_u, &a_perm, &a_ws};
+  const CUresult r = driver().launch(static_cast<CUfunction>(jm.func), unsigned(p.nmg), unsigned(tiles), unsigned(p.ks),
                                      unsigned((p.warps + (p.pw ? 1 : 0)) * 32), 1, 1, unsigned(p.smem_bytes), (CUstream)s, args,
                                      nullptr);
   return r == CUDA_SUCCESS ? 0 : -1;

@@ -29,6 +29,9 @@ struct JitPlan {
   int pw = 0;     // > 0: one extra "prefetch warp" per CTA walks the m-group's code one chunk ahead of the compute
                   // warps (garbage data, no copies, no stores) so their instruction fetches hit the L1.5 cache
                   // (straight-line barrier mode only; not with split / deal / mbarrier)
+  int ks = 0;     // > 1: the group's channel chunks are split into ks contiguous ranges (split points on multiples of
+                  // NS), one CTA each (grid z); partial sums go to a workspace and a reduce kernel adds them in
+                  // z order + bias + ReLU — deterministic, within R#11, NOT bitwise equal to the one-range kernels
   int hp = 0;     // > 0: horizontal pixel pairs (stride 1, K <= 5, P even): a lane's pixel pair is (ow, ow+1) of one
                   // row, its taps come from ld.shared.v2 (K+1 words per filter row instead of 2K); 1 = pair origin
                   // parity by rule, 2 = origins at odd columns kept for vector staging
@@ -73,6 +76,8 @@ struct JitModule {
   int cache_hits = 0;              // units loaded from ESCOIN_JIT_CACHE instead of compiled
   bool reordered = false;          // output channels regrouped for load balance (row_order)
   void* d_perm = nullptr;          // device lane -> pixel deal table (uint16 [nphase][T]) or null
+  float* d_ws = nullptr;           // split-channel partial sums (ks > 1): [ks][N][M][E][F]
+  int64_t ws_elems = 0;
 };
 
 // 0 = supported (plan filled), < 0 = this layer has no JIT form (stride != 1, 2*pad != K-1, smem).
@@ -95,7 +100,8 @@ std::string jit_label(const JitModule& jm);
 void jit_free(JitModule& jm);
 // Compile PTX for sm_100a in-process without loading it (host only); 0 = OK.
 int jit_compile_only(const char* ptx, size_t* cubin_bytes);
+// ks > 1: writes the partial sums to ws ([ks][N][M][E][F], caller-sized) instead of out; the caller reduces.
 int jit_launch(const JitModule& jm, const float* in, float* out, const float* bias, int relu, int N,
-               cudaStream_t s);
+               cudaStream_t s, float* ws = nullptr);
 
 }  // namespace escoin

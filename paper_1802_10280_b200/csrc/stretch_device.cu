@@ -130,3 +130,35 @@ int launch_stretch_compact(const float* w, int M, int64_t crs, int K, int Hp, in
 }
 
 }  // namespace escoin
+
+// ------------------------------------------------------------------ split-channel reduce
+// out[i] = act(((ws[0][i] + ws[1][i]) + ... + ws[ks-1][i]) + bias[m]) for the specialised kernel's split
+// channels (JitPlan::ks): the partial sums are added in z order, then the bias (one fp32 add), then
+// ReLU v > 0 ? v : 0 (R#10) — a fixed order, so the result does not depend on the grid or the batch
+// slice; coalesced float4 when the total is a multiple of 4.
+namespace escoin {
+namespace {
+__global__ void ks_reduce_kernel(const float* __restrict__ ws, int ks, int64_t total, int M, int EF,
+                                 const float* __restrict__ bias, int relu, float* __restrict__ out) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    float v = ws[i];
+    for (int z = 1; z < ks; ++z) v = __fadd_rn(v, ws[int64_t(z) * total + i]);
+    if (bias) v = __fadd_rn(v, bias[(i / EF) % M]);
+    if (relu) v = v > 0.0f ? v : 0.0f;
+    out[i] = v;
+  }
+}
+}  // namespace
+
+int launch_ks_reduce(const float* ws, int ks, int64_t total, int M, int EF, const float* bias, int relu, float* out,
+                     cudaStream_t s) {
+  if (total <= 0) return 0;
+  const int threads = 256;
+  const int64_t want = (total + threads - 1) / threads;
+  const int blocks = int(want < 148 * 16 ? want : 148 * 16);
+  ks_reduce_kernel<<<blocks, threads, 0, s>>>(ws, ks, total, M, EF, bias, relu, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace escoin

@@ -247,11 +247,11 @@ class Csr:
         return buf.value.decode()
 
     def jit(self, n_hint=128, Q=0, P=0, CC=0, NS=0, warps=0, minb=0, prefetch=0, mbarrier=0, units=0,
-            vec=0, reorder=0, sws=0, perm=0, split=0, pair=0, hp=0, pw=0) -> "Csr":
+            vec=0, reorder=0, sws=0, perm=0, split=0, pair=0, hp=0, pw=0, ks=0) -> "Csr":
         """escoin_csr_jit: compile this layer's pattern-specialised kernel and select it."""
-        tun = (ctypes.c_int * 17)(Q, P, CC, NS, warps, minb, prefetch, mbarrier, units, vec, reorder, sws, perm,
-                                  split, pair, hp, pw)
-        _check("escoin_csr_jit", lib().escoin_csr_jit(self._h, n_hint, tun, 17))
+        tun = (ctypes.c_int * 18)(Q, P, CC, NS, warps, minb, prefetch, mbarrier, units, vec, reorder, sws, perm,
+                                  split, pair, hp, pw, ks)
+        _check("escoin_csr_jit", lib().escoin_csr_jit(self._h, n_hint, tun, 18))
         return self
 
     def jit_info(self):

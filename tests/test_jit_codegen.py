@@ -26,13 +26,13 @@ def _lib():
 def gen_ptx(csr, n_hint=16, **tun):
     # reorder defaults to -1 here (identity grouping: accumulator (g, q) is row g*Q + q)
     keys = ["Q", "P", "CC", "NS", "warps", "minb", "prefetch", "mbarrier", "units", "vec", "reorder", "sws",
-            "perm", "split", "pair", "hp"]
+            "perm", "split", "pair", "hp", "pw", "ks"]
     tun.setdefault("reorder", -1)
-    arr = (ctypes.c_int * 16)(*[tun.get(k, 0) for k in keys])
+    arr = (ctypes.c_int * 18)(*[tun.get(k, 0) for k in keys])
     L, n = _lib(), ctypes.c_int64()
-    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 16, None, 0, ctypes.byref(n)) == 0
+    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 18, None, 0, ctypes.byref(n)) == 0
     buf = ctypes.create_string_buffer(n.value + 1)
-    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 16, buf, n.value + 1, ctypes.byref(n)) == 0
+    assert L.escoin_internal_jit_ptx(csr.handle, n_hint, arr, 18, buf, n.value + 1, ctypes.byref(n)) == 0
     return buf.value.decode()
 
 
@@ -167,7 +167,8 @@ def test_generated_ptx_compiles_for_sm100a():
     L = workloads.TINY
     w = inputs.layer_weights("tiny", L, 800)
     csr = escoin.Csr.stretch(w, L.H, L.W, L.stride, L.pad)
-    for tun in [dict(), dict(mbarrier=1, NS=4), dict(Q=8, P=2, prefetch=-1), dict(Q=8, P=2), dict(Q=4, P=4, pair=1)]:
+    for tun in [dict(), dict(mbarrier=1, NS=4), dict(Q=8, P=2, prefetch=-1), dict(Q=8, P=2), dict(Q=4, P=4, pair=1),
+                dict(Q=8, pw=1), dict(Q=8, CC=4, ks=3), dict(Q=8, P=2, hp=1)]:
         n = ctypes.c_int64()
         assert _lib().escoin_internal_ptx_compile(gen_ptx(csr, n_hint=1, **tun).encode(), ctypes.byref(n)) == 0
         assert n.value > 0

@@ -481,3 +481,32 @@ def test_horizontal_pairs_bitwise(case, relu):
     check(out, ref, scale, b)
     csr.set_kernel(0)
     assert out.tobytes() == fwd(csr, x, b, relu).tobytes()
+
+
+KS_CASES = [  # N, C, H, W, M, K, stride, pad, tunables — split channels (few CTAs: small planes, few channels)
+    (3, 40, 7, 7, 24, 3, 1, 1, dict(Q=8, CC=4, NS=3, ks=3)), (2, 64, 7, 7, 16, 5, 1, 2, dict(Q=16, CC=4, NS=4, ks=4)),
+    (4, 96, 7, 7, 12, 1, 1, 0, dict(Q=12, CC=8, NS=3, ks=2)), (2, 30, 9, 11, 33, 3, 2, 1, dict(Q=16, CC=2, ks=5)),
+    (3, 20, 13, 13, 40, 3, 1, 1, dict(Q=16, CC=4, NS=2, ks=4, units=2)), (2, 9, 6, 6, 5, 3, 1, 1, dict(Q=8, CC=1, ks=16)),
+]
+
+
+@pytest.mark.parametrize("relu", [True, False])
+@pytest.mark.parametrize("case", KS_CASES)
+def test_split_channels_tolerance_and_determinism(case, relu):
+    # ks > 1: partial sums over channel ranges + fixed-order reduce: within R#11 of the oracle, identical
+    # bits across runs and batch slices (not bitwise equal to the one-range kernels — a different order)
+    N, C, H, W, M, K, st, p, tun = case
+    rng = np.random.default_rng(abs(hash(case[:8])) % 2**32 + 11)
+    x = rng.random((N, C, H, W)).astype(np.float32)
+    w = rng.standard_normal((M, C, K, K)).astype(np.float32)
+    w[rng.random(w.shape) >= 0.25] = 0.0
+    w[2] = 0.0
+    b = (rng.random(M) * 0.2 - 0.1).astype(np.float32)
+    ref, scale = oracle_ref(w, x, b, st, p, relu)
+    csr = escoin.Csr.stretch(w, H, W, st, p).to_device(0)
+    csr.jit(n_hint=N, **tun)
+    assert "_k%d" % tun["ks"] in csr.label()
+    out = fwd(csr, x, b, relu)
+    check(out, ref, scale, b)
+    assert fwd(csr, x, b, relu).tobytes() == out.tobytes()
+    assert fwd(csr, x[1:], b, relu).tobytes() == out[1:].tobytes()
