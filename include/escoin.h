@@ -250,7 +250,8 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              run one forward before capturing a graph) and a reduce kernel
  *              adds them in a fixed order, then bias and ReLU.  Deterministic
  *              and independent of the batch slice, within the R#11 tolerance,
- *              but NOT bitwise equal to the one-range kernels)};
+ *              but NOT bitwise equal to the one-range kernels; < 0: as many
+ *              parts as fill one wave of 148 x CTAs/SM, 1 if the grid does)};
  *              <= 0 entries take the defaults.
  * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
  * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE

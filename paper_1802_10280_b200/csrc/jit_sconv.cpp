@@ -424,7 +424,6 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
   }
   if (p.pw) {
     o(".reg .pred %%pw<2>;");
-    o(".reg .b32 %%rbid, %%rbcnt;");
   }
   // params, ids
   o("ld.param.u64 %%rd0, [p_in];");
@@ -515,8 +514,6 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     o("setp.eq.u32 %%pw0, %%r8, %d;", p.warps);
     o("not.pred %%pw1, %%pw0;");
     o("selp.b32 %%r9, %%r28, %%r9, %%pw0;");
-    o("selp.b32 %%rbid, 2, 1, %%pw0;");               // its chunk barrier: 2 (lead limiter), compute: 1
-    o("selp.b32 %%rbcnt, %d, %d, %%pw0;", NT, NTc);
   }
   if (permuted) {
     // lane -> pixel deal (perm_table): slot (warp*P + j, lane) of tile phase ph = tile mod nphase
@@ -874,10 +871,11 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
     }
     for (int g = 0; g < ng; ++g) {
       o("G%d:", g);
-      // prefetch warp: barrier 2 pairs its wait before chunk j with the compute warps' arrival at
-      // chunk j-1 (one arrival up front, one per chunk but the last), so it runs at most one chunk
-      // ahead and the next chunk's code is in the L1.5 instruction cache when the compute warps get there
-      if (p.pw && klo[g] < khi[g]) o("@%%pw1 bar.arrive 2, %d;", NT);
+      // prefetch warp: barrier 2 pairs the compute warps at chunk k with the prefetch warp at chunk k+1
+      // (compute warps sync on it at every chunk but the last, the prefetch warp at every chunk but the
+      // first), so the prefetch warp runs exactly one chunk ahead — the next chunk's code is in the L1.5
+      // instruction cache when the compute warps get there — and the compute warps wait if it lags.
+      // (A non-blocking arrive instead would let fast compute warps arrive twice in one phase.)
       for (int k = klo[g]; k < khi[g]; ++k) {
         if (p.ks > 1) {
           if (k > klo[g]) {  // this CTA's part ends here
@@ -888,8 +886,11 @@ std::string gen_ptx(const JitPlan& p, const int32_t* rowptr, const int32_t* coli
         }
         o("cp.async.wait_group %d;", p.NS - 2);
         if (p.pw) {
-          o("bar.sync %%rbid, %%rbcnt;");
-          if (k + 1 < khi[g]) o("@%%pw1 bar.arrive 2, %d;", NT);
+          o("@%%pw1 bar.sync 1, %d;", NTc);  // compute warps: this chunk's copies landed
+          const bool cw = k + 1 < khi[g], pf = k > klo[g];
+          if (cw && pf) o("bar.sync 2, %d;", NT);
+          else if (cw) o("@%%pw1 bar.sync 2, %d;", NT);
+          else if (pf) o("@%%pw0 bar.sync 2, %d;", NT);
         } else if (p.sp > 1) {
           o("bar.sync %%s3, %d;", NTh);
         } else {
@@ -1248,6 +1249,7 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   p.mb = p.mb > 0 ? 1 : 0;
   // the instruction-prefetch pass reads the last stage buffer, free until the first CTA barrier of
   // the main loop; the mbarrier pipeline has no such barrier, so it runs without the pass
+  const bool ks_auto = p.ks < 0;  // resolved below, once the grid is known
   p.ks = (p.ks > 1 && !p.mb) ? std::min(p.ks, 64) : 1;
   if (p.ks > 1) {  // split channels: plain straight-line barrier mode, identity grouping
     p.perm = 0;
@@ -1359,6 +1361,24 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
     if (Qb != p.Q) {
       p.Q = Qb;
       if (!plan_fit(p, n_hint)) return -1;
+    }
+  }
+  if (ks_auto && !p.mb) {
+    // ks < 0: split the channels when the (tiles x groups) grid covers less than one wave of
+    // 148 x CTAs/SM: enough parts to fill it, at least NS chunks each
+    // time ~ waves(ctas * ks) / ks, + 4% per extra part (partial-sum traffic, the reduce)
+    const double ctas = std::ceil(double(n_hint) * E * p.Fi / p.T) * p.nmg, slots = 148.0 * p.minb;
+    const int maxp = std::max(1, std::min(p.nch / p.NS, 64));
+    double best_t = 1e30;
+    for (int k = 1; k <= maxp; ++k) {
+      const double t = std::ceil(ctas * k / slots) / k * (1.0 + 0.04 * (k - 1));
+      if (t < best_t * 0.999) { best_t = t; p.ks = k; }
+    }
+    if (p.ks > 1) {
+      p.perm = 0;
+      p.reorder = -1;
+      p.pw = 0;
+      p.pf = 0;
     }
   }
   if (p.smem_bytes > 227 * 1024 / p.minb) return -1;
