@@ -56,7 +56,11 @@ WL_NAMES = {"alexnet": "pruned AlexNet conv2-conv5 (4 sparse CONV layers)",
 # escoin_csr_autotune_ex keeps the fastest under the bench's flushed-L2 conditions
 # (Q is balanced over the groups: 48 -> 43 rows on 256 channels; "32,2,8,3,12,2,-1" = FFMA2 slot pairs, the
 # res2 winner in r02u; "-1" = no instruction-prefetch pass)
-DEFAULT_JIT_TUNINGS = "0;32,1,0,0,24,1;32,1,0,0,16,2;32,2,8,3,12,2,-1;32,1,0,0,32,1;48,1,0,0,16,2"
+# The two split-channel entries (ks = -2: auto count, compiled only where the grid is below one wave —
+# GoogLeNet's 7x7 5x5 / 1x1 layers, r02y) are skipped on every other layer.
+_KS = ",0,0,0,0,0,0,0,0,0,0,0,-2"
+DEFAULT_JIT_TUNINGS = ("0;32,1,0,0,24,1;32,1,0,0,16,2;32,2,8,3,12,2,-1;32,1,0,0,32,1;48,1,0,0,16,2;"
+                       "32,1,8,2,8,1" + _KS + ";32,1,2,2,16,1" + _KS)
 METRIC = "sparse-conv images/s (whole stack of sparse layers, global batch 128)"
 
 
@@ -470,7 +474,8 @@ def main():
             fwd(escoin, runs[i], s_)
 
     graph = None if args.no_graph else capture_step(torch, step_fn)
-    launches_per_step = len(runs)  # one kernel launch per layer (linked units are one kernel)
+    # one kernel launch per layer (linked units are one kernel); split-channel layers (_k) add the reduce
+    launches_per_step = sum(2 if "_k" in r.kernel else 1 for r in runs)
 
     # ---------------- device-timed region (K steps, barrier + sync both sides)
     if world > 1:

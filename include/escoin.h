@@ -241,7 +241,8 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              per CTA runs the output-channel group's code one chunk ahead
  *              of the compute warps on stale data — no copies, no stores —
  *              so their instruction fetches hit the L1.5 cache; replaces the
- *              prefetch pass; not with mbarrier / split / perm; same bits),
+ *              prefetch pass; not with mbarrier / split / perm / units > 1;
+ *              same bits; measured slower, r02y),
  *              ks (> 1: each output-channel group's input channels are
  *              split into ks contiguous chunk ranges, one CTA each, for
  *              layers with too few CTAs (small planes, few output channels):
@@ -251,7 +252,9 @@ int escoin_csr_kernel_label(const escoin_csr* csr, char* buf, int cap);
  *              adds them in a fixed order, then bias and ReLU.  Deterministic
  *              and independent of the batch slice, within the R#11 tolerance,
  *              but NOT bitwise equal to the one-range kernels; < 0: as many
- *              parts as fill one wave of 148 x CTAs/SM, 1 if the grid does)};
+ *              parts as fill one wave of 148 x CTAs/SM, 1 if the grid does;
+ *              <= -2: the same, but UNSUPPORTED when no split is needed — a
+ *              tuning list entry that only compiles where it splits)};
  *              <= 0 entries take the defaults.
  * Compilation uses at most ESCOIN_JIT_THREADS (default: all host cores) concurrent
  * compiler threads across the process; if the environment variable ESCOIN_JIT_CACHE

@@ -1250,6 +1250,7 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
   // the instruction-prefetch pass reads the last stage buffer, free until the first CTA barrier of
   // the main loop; the mbarrier pipeline has no such barrier, so it runs without the pass
   const bool ks_auto = p.ks < 0;  // resolved below, once the grid is known
+  const bool ks_only = p.ks <= -2;  // ... and no kernel at all when no split is needed
   p.ks = (p.ks > 1 && !p.mb) ? std::min(p.ks, 64) : 1;
   if (p.ks > 1) {  // split channels: plain straight-line barrier mode, identity grouping
     p.perm = 0;
@@ -1379,6 +1380,8 @@ int jit_plan(JitPlan& p, int C, int H, int W, int M, int K, int stride, int pad,
       p.reorder = -1;
       p.pw = 0;
       p.pf = 0;
+    } else if (ks_only) {
+      return -1;
     }
   }
   if (p.smem_bytes > 227 * 1024 / p.minb) return -1;
@@ -1640,6 +1643,11 @@ int jit_cubin(JitModule& jm, const JitPlan& p, const int32_t* rowptr, const int3
   // One unit: a complete kernel.  Several: each unit is the device function of its m-groups,
   // compiled relocatable in its own host thread (register budget of the kernel's occupancy),
   // then linked with a small entry kernel that calls the unit of blockIdx.y — ONE launch.
+  if (U > 1 && p.pw) {  // a unit function with the prefetch warp's barriers exceeds the entry's register cap
+    if (log) *log = "the prefetch warp (pw) is not supported with linked units";
+    jm.units.clear();
+    return -2;
+  }
   const int maxreg = std::min(255, 65536 / (p.warps * 32 * p.minb)) & ~7;
   Opts uopts = {kOpts[0], kOpts[1]};
   if (U > 1) {

@@ -52,13 +52,18 @@ def test_bench_setup_every_output_vs_oracle(wl_name):
         x = r.h_x.numpy()
         rp, ci, v = oracle.csr_stretch(w, L.H, L.W, L.stride, L.pad)
         ref, scale = oracle.sconv(x, rp, ci, v, L.M, L.K, L.stride, L.pad, bias=b, relu=True)
-        err = np.abs(out.astype(np.float64) - ref)
         bound = TOL * (scale + np.abs(b.astype(np.float64))[None, :, None, None])
-        if (err > bound).any():
+
+        def within(o):
+            return not (np.abs(o.astype(np.float64) - ref) > bound).any()
+        if not within(out):
+            err = np.abs(out.astype(np.float64) - ref)
             failures.append("%s %s: max err/bound %.3g" % (L.name, label, float(np.max(err / bound))))
-        del ref, scale, err, bound
-        # every other compiled tuning: same bits (re-selecting a compiled tuning compiles nothing)
+        # every other compiled tuning (re-selecting a compiled tuning compiles nothing): the one-range
+        # kernels give the same bits as each other (R#12); split-channel ones (_k: a different summation
+        # order, JitPlan::ks) are checked against the oracle instead
         if r.csr.kernel() == escoin.KERNEL_JIT:
+            one_range = None if "_k" in label else out.tobytes()
             for tun in tunings:
                 try:
                     r.csr.jit(128, *tun)
@@ -66,6 +71,14 @@ def test_bench_setup_every_output_vs_oracle(wl_name):
                     continue
                 bench.fwd(escoin, r, s)
                 torch.cuda.synchronize()
-                if r.out.cpu().numpy().tobytes() != out.tobytes():
-                    failures.append("%s %s differs from %s" % (L.name, r.csr.label(), label))
+                o = r.out.cpu().numpy()
+                lab = r.csr.label()
+                if "_k" in lab:
+                    if not within(o):
+                        failures.append("%s %s: outside the tolerance" % (L.name, lab))
+                elif one_range is None:
+                    one_range = o.tobytes()
+                elif o.tobytes() != one_range:
+                    failures.append("%s %s differs from the other one-range kernels" % (L.name, lab))
+        del ref, scale, bound
     assert not failures, failures

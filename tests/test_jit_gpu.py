@@ -76,7 +76,7 @@ TUNINGS = [dict(), dict(Q=16, P=2, CC=3, NS=2), dict(Q=32, P=3, CC=5, NS=4, warp
            dict(Q=8, P=2, pair=-1), dict(Q=16, P=4, CC=3, warps=4), dict(Q=16, P=2, CC=3, NS=2, hp=1),
            dict(Q=8, P=4, warps=4, hp=2), dict(Q=16, P=2, NS=4, mbarrier=1, hp=1),
            # prefetch warp (one extra warp one chunk ahead; no copies, no stores)
-           dict(Q=16, warps=4, pw=1), dict(Q=8, P=2, CC=3, NS=2, warps=2, pw=1), dict(Q=16, CC=1, NS=4, pw=1, units=2)]
+           dict(Q=16, warps=4, pw=1), dict(Q=8, P=2, CC=3, NS=2, warps=2, pw=1), dict(Q=16, CC=1, NS=4, pw=1)]
 
 
 @pytest.mark.parametrize("tun", range(len(TUNINGS)))
