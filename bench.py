@@ -61,6 +61,16 @@ WL_NAMES = {"alexnet": "pruned AlexNet conv2-conv5 (4 sparse CONV layers)",
 _KS = ",0,0,0,0,0,0,0,0,0,0,0,-2"
 DEFAULT_JIT_TUNINGS = ("0;32,1,0,0,24,1;32,1,0,0,16,2;32,2,8,3,12,2,-1;32,1,0,0,32,1;48,1,0,0,16,2;"
                        "32,1,8,2,8,1" + _KS + ";32,1,2,2,16,1" + _KS)
+# ResNet-50 (the headline): only the three tunings that won a stage in r02u/r02z — FFMA2 q32 w12 b2 (res2),
+# q48->43 w16 b2 (res3, res4), q32 w24 b1 (res5) — which halves the fresh compile (the res5 kernels take
+# ~5 min of one host core each)
+RESNET_JIT_TUNINGS = "32,2,8,3,12,2,-1;48,1,0,0,16,2;32,1,0,0,24,1"
+WL_JIT_TUNINGS = {"resnet50": RESNET_JIT_TUNINGS, "resnet50_v15": RESNET_JIT_TUNINGS}
+
+
+def jit_tunings_for(workload):
+    """The escoin_csr_jit tunings bench.py compiles for this workload (--jit-tunings overrides)."""
+    return WL_JIT_TUNINGS.get(workload, DEFAULT_JIT_TUNINGS)
 METRIC = "sparse-conv images/s (whole stack of sparse layers, global batch 128)"
 
 
@@ -85,7 +95,7 @@ def parse():
     p.add_argument("--kernel", type=int, default=-1, help="sconv variant id (-1 = auto)")
     p.add_argument("--no-autotune", action="store_true", help="skip escoin_csr_autotune at setup")
     p.add_argument("--no-jit", action="store_true", help="skip the pattern-specialised kernels (escoin_csr_jit)")
-    p.add_argument("--jit-tunings", default=DEFAULT_JIT_TUNINGS,
+    p.add_argument("--jit-tunings", default=None,
                    help="';'-separated escoin_csr_jit tunings compiled per layer (0 = the library's model pick); "
                         "autotune keeps the fastest")
     p.add_argument("--no-baselines", action="store_true")
@@ -95,7 +105,10 @@ def parse():
     p.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N > 1 (tests use gloo)")
     p.add_argument("--same-device", action="store_true",
                    help="all ranks on cuda:0 (multi-rank test of the driver on a 1-GPU box; not a measurement)")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.jit_tunings is None:
+        a.jit_tunings = jit_tunings_for(a.workload)
+    return a
 
 
 # ------------------------------------------------------------------ clocks

@@ -1,7 +1,7 @@
 """Full-size parity of exactly what bench.py times (BASELINE configs at batch 128).
 
 For every layer of every workload the bench runs, this replays bench.setup() — the same
-stretch, the same escoin_csr_jit tunings (bench.DEFAULT_JIT_TUNINGS), the same flushed
+stretch, the same escoin_csr_jit tunings (bench.jit_tunings_for(workload)), the same flushed
 autotune — then compares EVERY output element of the selected kernel with the fp64 oracle
 (reading R#11: |gpu - ref| <= 1e-5 * (sum|w*x| + |bias|)), and checks that every other
 compiled tuning of the layer gives bitwise the same tensor (R#12), so each kernel the
@@ -25,7 +25,7 @@ TOL = 1e-5
 def _setup(wl_name):
     W = workloads.workload(wl_name)
     args = argparse.Namespace(batch=None, weak=False, sparsity=800, kernel=-1, no_jit=False, no_autotune=False,
-                              tune_variants=False, jit_tunings=bench.DEFAULT_JIT_TUNINGS)
+                              tune_variants=False, jit_tunings=bench.jit_tunings_for(wl_name))
     dev = torch.device("cuda", 0)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     runs, n0, B, GB, _ = bench.setup(args, W, dev, 0, 1, torch, escoin, flush)
@@ -38,7 +38,7 @@ def _setup(wl_name):
 def test_bench_setup_every_output_vs_oracle(wl_name):
     W, runs = _setup(wl_name)
     tunings = [[int(v) for v in t.split(",")] if t.strip() not in ("", "0") else []
-               for t in bench.DEFAULT_JIT_TUNINGS.split(";")]
+               for t in bench.jit_tunings_for(wl_name).split(";")]
     s = torch.cuda.current_stream().cuda_stream
     failures = []
     for r in runs:
