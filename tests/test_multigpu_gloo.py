@@ -91,3 +91,24 @@ def test_bench_strong_scaling_ranges(world):
     assert seen == list(range(128))
     args.weak = True
     assert bench.batch_range(args, wl, 1, world) == (128, 128, 128 * world)
+
+
+def test_bench_jit_tunings_per_workload():
+    # host logic of bench.py's tuning lists: ResNet-50 (v1 and v1.5) compiles its three stage winners,
+    # every other workload the full list; every entry parses into <= 18 escoin_csr_jit tunables, and the
+    # split-channel entries ask for "auto count, only where a split is needed" (ks = -2, index 17)
+    import sys
+    sys.argv = ["bench.py", "--workload", "resnet50"]
+    import bench
+    assert bench.parse().jit_tunings == bench.RESNET_JIT_TUNINGS
+    sys.argv = ["bench.py", "--workload", "googlenet"]
+    assert bench.parse().jit_tunings == bench.DEFAULT_JIT_TUNINGS
+    sys.argv = ["bench.py", "--workload", "alexnet", "--jit-tunings", "0;32,1"]
+    assert bench.parse().jit_tunings == "0;32,1"
+    for wl in ["resnet50", "resnet50_v15", "alexnet", "googlenet", "googlenet_1x1"]:
+        entries = [[int(v) for v in t.split(",")] for t in bench.jit_tunings_for(wl).split(";") if t.strip() != "0"]
+        assert entries and all(len(e) <= 18 for e in entries)
+    ks = [e for e in ([int(v) for v in t.split(",")] for t in bench.DEFAULT_JIT_TUNINGS.split(";") if t != "0")
+          if len(e) == 18]
+    assert len(ks) == 2 and all(e[17] == -2 for e in ks)
+    assert len(bench.RESNET_JIT_TUNINGS.split(";")) == 3
