@@ -7,16 +7,19 @@
 // and compiles the layer's nonzero PATTERN and VALUES into the instruction
 // stream: for every (output-channel group, input channel) the generated PTX
 // loads the input taps the group uses from the shared-memory slab and issues
-// one `fma.rn.f32 acc, x, <weight immediate>, acc` per (nonzero, pixel).
-// There is no per-nonzero dispatch, no record stream and no weight load at
-// all (the weight is an FFMA immediate), which is what the register-tiled
-// interpreter kernels (sconv_tiled.cuh) spend most of their issue slots on.
+// one `fma.rn.f32 acc, x, <weight immediate>, acc` per (nonzero, pixel) — or,
+// with P even, one `fma.rn.f32x2` (FFMA2, the weight broadcast as a 32-bit
+// immediate) per (nonzero, pixel pair).  There is no per-nonzero dispatch, no
+// record stream and no weight load at all (the weight is an immediate), which
+// is what the register-tiled interpreter kernels (sconv_tiled.cuh) spend most
+// of their issue slots on.
 //
 // Semantics are exactly escoin_sconv_forward's (Alg.2 P:389-410 with the
 // stride/pad generalisation R#1, R#9, R#10): each accumulator starts at 0.0f
 // and receives its CSR terms in ascending (c, kh, kw) = colidx order with
 // fma.rn.f32, then acc + bias[m] and ReLU — bit-identical to every other
-// variant (tested).
+// variant (tested).  Exception: split channels (JitPlan::ks > 1) add per-range
+// partial sums in a fixed order (deterministic, within R#11).
 //
 // Geometry: a CTA owns T consecutive output pixels g = (n*E + oh)*F + ow (tile
 // blockIdx.y; lane l of warp w: g0 + (w*P + j)*32 + l, no idle lanes) and
@@ -27,8 +30,8 @@
 // reads tap (kh, kw) at pos(g) + kh*SWs + kw: the stretched offset f(0, kh, kw)
 // of P:428 with the stacked row stride, an immediate offset from the lane's
 // base register.  Per pipeline stage CC channels of the window
-// [pos(g0), pos(g0) + L) are copied with 4-byte cp.async (zero-fill = the
-// virtual padding, R#9).
+// [pos(g0), pos(g0) + L) are staged: data chunks with 16/8/4-byte cp.async,
+// the padding words zeroed once per CTA (the virtual padding, R#9).
 //
 // Compilation: PTX text -> nvPTXCompiler (static, in-process) -> cubin ->
 // driver module (entry points via cudaGetDriverEntryPoint, so the library
